@@ -1,0 +1,131 @@
+/*
+ * hp.h -- C ABI of the B200 co-executed prefill/decode hot path
+ * (libb200hot.so, sm_100a only).
+ *
+ * The reference (smshare, /root/reference/pkg/src/smshare) has no native code:
+ * its device boundary is the Python `GroundTruthOracle` (engine.py:159-208),
+ * whose `prefill_layer_s(es)` / `decode_step_s(es)` stand in for "one prefill
+ * layer on pm SMs" and "one decode step on dm SMs".  This library is what
+ * those two calls execute on a B200.  Every entry point below names the
+ * reference interface (file:line) whose work it performs.
+ *
+ * Conventions
+ *   - All device memory is owned by the caller (PyTorch); pointers are raw
+ *     device addresses, never freed here.  bf16 tensors are row-major.
+ *   - Every compute call is asynchronous on `stream` (a cudaStream_t, e.g.
+ *     torch.cuda.Stream.cuda_stream or a green-context stream from
+ *     hp_partition_stream) and returns 0 or a negative HP_ERR_* code;
+ *     hp_last_error() describes the failure.  No CPU fallback exists.
+ *   - `max_ctas` is the persistent grid size: the SM count of the partition
+ *     the launch is confined to (times resident CTAs per SM).
+ */
+#ifndef HP_H_
+#define HP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_ABI_VERSION 1
+
+#define HP_OK 0
+#define HP_ERR_INVALID (-1)
+#define HP_ERR_CUDA (-2)
+#define HP_ERR_UNSUPPORTED (-3)
+#define HP_ERR_NO_DEVICE (-4)
+
+/* GEMM epilogues: the fused tails of the reference's kernel groups */
+#define HP_EPI_STORE 0 /* qkv projection          (workload.py:164-170) */
+#define HP_EPI_RESID 1 /* o_proj / mlp_down + residual (workload.py:191-194, 205-209) */
+#define HP_EPI_SILU 2  /* mlp_up_gate, silu(g)*u  (workload.py:198-204) */
+
+/* ---------------------------------------------------------------- runtime */
+int hp_abi_version(void);
+const char* hp_last_error(void);
+/* Number of visible CUDA devices (0 on a GPU-less host; never fails). */
+int hp_device_count(void);
+/* SM count of `device`; the `N` of GpuSpec (perf_model.py:38-57). */
+int hp_device_sms(int device, int* sms);
+
+/* ------------------------------------------------------- wave accounting */
+/* wave_stats(g, b, n) -- perf_model.py:157-169.  Bit-identical integers and
+ * the same IEEE double idle ratio (n - tail) / (n * waves). */
+int hp_wave_stats(int64_t g, int64_t b, int64_t n, int64_t* waves, int64_t* tail_sms,
+                  double* idle_ratio);
+
+/* ---------------------------------------------------- SM partitions
+ * Realises `_request_partition` / `_apply_partitions` (engine.py:440-452):
+ * a green-context pair splitting the device into a decode share of
+ * `decode_sms` SMs (multiple of 8, CC>=9 rule) and a prefill share holding
+ * the remainder.  Each side owns one stream; kernels launched into it run
+ * only on that side's SMs.  Switching partitions = launching into another
+ * pair's streams (the reference's `reconfig_s`, engine.py:132). */
+typedef struct hp_partition hp_partition;
+int hp_partition_create(int device, int decode_sms, hp_partition** out);
+/* phase: 0 = prefill, 1 = decode. */
+int hp_partition_stream(hp_partition* part, int phase, void** stream);
+int hp_partition_sms(hp_partition* part, int phase, int* sms);
+int hp_partition_destroy(hp_partition* part);
+
+/* ---------------------------------------------------- layer kernels */
+/* Pre-attention / pre-MLP RMSNorm (traffic folded into qkv / mlp_up_gate
+ * bytes, workload.py:164-168, 200-202): out = x * rsqrt(mean(x^2)+eps) * w. */
+int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out, int ldo, int rows, int cols,
+               float eps, int max_ctas, void* stream);
+
+/* Token-major tcgen05 GEMM (prefill): Y[T,N] = epi(X[T,K] . W[N,K]^T).
+ * SILU: W rows interleaved in blocks of 64 (gate, up), Y has N/2 columns.
+ * The qkv / o_proj / mlp_up_gate / mlp_down kernels of layer_kernels
+ * (workload.py:162-210) at phase "prefill". */
+int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
+            int ldr, int T, int N, int K, int epilogue, int max_ctas, void* stream);
+
+/* Swap-AB split-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
+ * hp_gemm; W streams through UMMA-M, split along K over `k_splits` CTAs
+ * (<=0: automatic).  workspace: fp32 [N, ceil(T/BN)*BN] zeroed before the
+ * first call (kept zero by the kernel); counters: int [N/128 * ceil(T/BN)]
+ * zeroed likewise.  layer_kernels phase "decode" (workload.py:153-210). */
+int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
+                 int ldr, int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes,
+                 int* counters, int n_counters, int k_splits, int max_ctas, void* stream);
+int hp_gemm_swap_splits(int T, int N, int K, int max_ctas);
+
+/* RoPE on q,k in the fused qkv buffer [T, (Hq+2Hkv)*d] (in place) and the
+ * paged KV-cache write of k,v (the `kv_write` bytes of the attention kernel,
+ * workload.py:180-182).  cos_sin: fp32 [max_pos, d] = [cos(d/2) | sin(d/2)].
+ * slot_mapping[t] = block * page + offset; kcache/vcache: [blocks, Hkv, page, d]. */
+int hp_rope_kv_write(void* qkv, int ldqkv, int T, int Hq, int Hkv, int d, const int* positions,
+                     const float* cos_sin, const int* slot_mapping, void* kcache, void* vcache,
+                     int page, int max_ctas, void* stream);
+
+/* Causal GQA prefill attention over the new span (workload.py:176-183 with
+ * prior_lens = 0): O[T, Hq*d] = softmax(Q K^T * scale, causal) V.
+ * cu_seqlens: int [nseq+1] token offsets of the packed sequences (host-side
+ * total_tokens = cu_seqlens[nseq] bounds the TMA views). */
+int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
+                    void* o, int ldo, const int* cu_seqlens, int nseq, int total_tokens,
+                    int max_seqlen, int Hq, int Hkv, int d, float scale, int max_ctas,
+                    void* stream);
+
+/* Paged decode attention (workload.py:184-188): one query token per
+ * sequence over ctx_lens[b] cached positions.  q: [B, Hq*d]; out: [B, Hq*d];
+ * block_table: int [B, max_pages]; workspace: fp32, hp_decode_attn_ws_bytes. */
+size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits);
+int hp_decode_attn(const void* q, int ldq, const void* kcache, const void* vcache,
+                   const int* block_table, int max_pages, const int* ctx_lens, void* out, int ldo,
+                   int B, int Hq, int Hkv, int d, int page, int num_blocks, float scale,
+                   void* workspace, size_t ws_bytes, int max_ctas, void* stream);
+
+/* ---------------------------------------------------- instrumentation */
+/* Per-CTA probe: out[i] = {smid, start_ns, end_ns} for `ctas` CTAs spinning
+ * `spin_ns` each -- partition confinement (%smid) and measured idle. */
+int hp_probe(int ctas, int threads, int64_t spin_ns, uint64_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HP_H_ */

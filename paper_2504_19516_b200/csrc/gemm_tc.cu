@@ -1,0 +1,415 @@
+// tcgen05 / TMEM / TMA GEMM for the four linear kernels of a Llama layer.
+//
+//   D = A . B^T  with A [Ma, K] and B [Nb, K] bf16, both K-major (torch
+//   [out, in] weight layout), fp32 accumulation in TMEM.
+//
+// Two operand placements share one kernel body:
+//   * prefill ("token-major"): A = activations X [T, K], B = weights W [N, K];
+//     D tile = 128 tokens x BN features, epilogue writes Y [T, N] directly.
+//   * decode ("swap-AB"): A = W [N, K], B = X [T<=256, K]; D tile = 128
+//     features x BN tokens.  The token count is tiny, so the weight stream is
+//     split along K across CTAs; partial tiles are reduced with vector
+//     red.global.add into an fp32 workspace and the last-arriving CTA of a
+//     tile runs the epilogue (counter-based, self-cleaning).
+//
+// Epilogues (reference kernel groups, workload.py:164-209):
+//   STORE  : Y = D                               (qkv projection)
+//   RESID  : Y = D + R                           (o_proj / mlp_down residual)
+//   SILU   : Y = silu(D_gate) * D_up             (mlp_up_gate; W rows are
+//            interleaved in blocks of 64: [g0..g63, u0..u63, g64.., ...])
+//
+// Persistent: grid = min(work units, max_ctas) where max_ctas is the SM
+// count of the partition the launch is confined to; units are walked in a
+// static round-robin so the rounds equal wave_stats(units, 1, grid).
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// single-thread UMMA issuer, warps 2..5 = epilogue (TMEM lane quarter = warp%4).
+#include "common.cuh"
+#include "runtime.h"
+#include "../../include/hp.h"
+
+#include <algorithm>
+
+namespace hp {
+
+enum { EPI_STORE = 0, EPI_RESID = 1, EPI_SILU = 2 };
+
+struct GemmParams {
+  int Ma, Nb, K;
+  int m_tiles, n_tiles, k_splits, kb_per_split, num_kb;
+  __nv_bfloat16* out;
+  int ldo;
+  const __nv_bfloat16* resid;
+  int ldr;
+  float* ws;      // swap mode: [Ma, ws_ld] fp32, zero on entry and exit
+  int ws_ld;
+  int* counters;  // swap mode: [m_tiles * n_tiles], zero on entry and exit
+  int epi;
+};
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ void store_row32(__nv_bfloat16* dst, const float* v) {
+  uint4 w[4];
+  uint32_t* u = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) u[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) d[j] = w[j];
+}
+
+__device__ __forceinline__ void add_row32(float* v, const __nv_bfloat16* src) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 w = s[j];
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(&w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[8 * j + 2 * k] += bf16lo(u[k]);
+      v[8 * j + 2 * k + 1] += bf16hi(u[k]);
+    }
+  }
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+template <int BN, bool SWAP>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const GemmParams p) {
+  using C = GemmCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total = p.m_tiles * p.n_tiles * p.k_splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        const int tile = u / p.k_splits, ks = u % p.k_splits;
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mt * BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        const int ks = u % p.k_splits;
+        const int kb0 = ks * p.kb_per_split;
+        const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;       // accumulator row owned by this thread
+    const int et = (warp - 2) * 32 + lane;  // 0..127 epilogue thread index
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      const int tile = u / p.k_splits;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      if constexpr (!SWAP) {
+        const int gm = mt * BM + row;
+        const bool ok = gm < p.Ma;
+        if (p.epi == EPI_SILU) {
+#pragma unroll 1
+          for (int h = 0; h < BN / 128; ++h) {
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              float g[32], v[32];
+              tmem_ld32(taddr + h * 128 + c * 32, g);
+              tmem_ld32(taddr + h * 128 + 64 + c * 32, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = silu(g[j]) * v[j];
+              if (ok) store_row32(p.out + size_t(gm) * p.ldo + nt * (BN / 2) + h * 64 + c * 32, v);
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+            tmem_ld32(taddr + c * 32, v);
+            tmem_ld_wait();
+            const int col = nt * BN + c * 32;
+            if (ok) {
+              if (p.epi == EPI_RESID) add_row32(v, p.resid + size_t(gm) * p.ldr + col);
+              store_row32(p.out + size_t(gm) * p.ldo + col, v);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        // partial tile (features x tokens) -> fp32 workspace
+        float* wrow = p.ws + size_t(mt * BM + row) * p.ws_ld + nt * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) red_add_v4(wrow + c * 32 + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) {
+          const int prev = atomicAdd(p.counters + tile, 1);
+          *last_flag = (prev == p.k_splits - 1) ? 1 : 0;
+        }
+        named_bar_sync(1, 128);
+        if (*last_flag) {
+          __threadfence();
+          const int T = p.Nb;
+          if (p.epi == EPI_SILU) {
+            const int r = et & 63;
+            const int half = et >> 6;
+            float* gw = p.ws + size_t(mt * BM + r) * p.ws_ld + nt * BN;
+            float* uw = gw + size_t(64) * p.ws_ld;
+            const int o = mt * 64 + r;
+            for (int j = half; j < BN; j += 2) {
+              const int t = nt * BN + j;
+              const float gv = __ldcg(gw + j), uv = __ldcg(uw + j);
+              __stcg(gw + j, 0.f);
+              __stcg(uw + j, 0.f);
+              if (t < T) p.out[size_t(t) * p.ldo + o] = __float2bfloat16(silu(gv) * uv);
+            }
+          } else {
+            const int o = mt * BM + et;
+            float* w = p.ws + size_t(o) * p.ws_ld + nt * BN;
+            for (int j = 0; j < BN; ++j) {
+              const int t = nt * BN + j;
+              float v = __ldcg(w + j);
+              __stcg(w + j, 0.f);
+              if (t < T) {
+                if (p.epi == EPI_RESID) v += __bfloat162float(p.resid[size_t(t) * p.ldr + o]);
+                p.out[size_t(t) * p.ldo + o] = __float2bfloat16(v);
+              }
+            }
+          }
+          if (et == 0) p.counters[tile] = 0;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN, bool SWAP>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
+                  cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tc<BN, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(C::SMEM)));
+    attr_set = true;
+  }
+  k_gemm_tc<BN, SWAP><<<grid, 192, C::SMEM, st>>>(ta, tb, p);
+  HP_LAUNCH_CHECK("k_gemm_tc");
+  return HP_OK;
+}
+
+static int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
+                       const void* R, int ldr, int T, int N, int K, int epilogue, int max_ctas,
+                       void* stream) {
+  HP_CHECK_ARG(X && W && Y, "hp_gemm: null pointer");
+  HP_CHECK_ARG(T >= 1 && N >= 1 && K >= 1, "hp_gemm: empty problem");
+  HP_CHECK_ARG(K % BK == 0, "hp_gemm: K must be a multiple of 64");
+  HP_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SILU, "hp_gemm: bad epilogue");
+  HP_CHECK_ARG(epilogue != EPI_RESID || R != nullptr, "hp_gemm: residual epilogue needs R");
+  HP_CHECK_ARG(max_ctas >= 1, "hp_gemm: max_ctas must be >= 1");
+  const int BN = (N % 256 == 0) ? 256 : 128;
+  HP_CHECK_ARG(N % 128 == 0, "hp_gemm: N must be a multiple of 128");
+  HP_CHECK_ARG(epilogue != EPI_SILU || N % 128 == 0, "hp_gemm: SiLU needs N multiple of 128");
+  CUtensorMap ta, tb;
+  int rc = cached_tmap_bf16(&ta, X, T, K, ldx, BM, BK, true);
+  if (rc) return rc;
+  rc = cached_tmap_bf16(&tb, W, N, K, ldw, BN, BK, true);
+  if (rc) return rc;
+  GemmParams p{};
+  p.Ma = T;
+  p.Nb = N;
+  p.K = K;
+  p.m_tiles = ceil_div(T, BM);
+  p.n_tiles = N / BN;
+  p.k_splits = 1;
+  p.num_kb = K / BK;
+  p.kb_per_split = p.num_kb;
+  p.out = static_cast<__nv_bfloat16*>(Y);
+  p.ldo = ldy;
+  p.resid = static_cast<const __nv_bfloat16*>(R);
+  p.ldr = ldr;
+  p.epi = epilogue;
+  const int units = p.m_tiles * p.n_tiles;
+  const int grid = std::min(units, max_ctas);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return BN == 256 ? launch<256, false>(ta, tb, p, grid, st) : launch<128, false>(ta, tb, p, grid, st);
+}
+
+extern "C" int hp_gemm_swap_splits(int T, int N, int K, int max_ctas) {
+  const int m_tiles = N / BM;
+  const int BN = T <= 32 ? 32 : (T <= 64 ? 64 : (T <= 128 ? 128 : 256));
+  const int tiles = m_tiles * ceil_div(T, BN);
+  const int num_kb = K / BK;
+  int ks = ceil_div(2 * max_ctas, tiles);
+  ks = std::max(1, std::min(ks, std::max(1, num_kb / 4)));
+  return ks;
+}
+
+extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
+                            const void* R, int ldr, int T, int N, int K, int epilogue,
+                            void* workspace, size_t ws_bytes, int* counters, int n_counters,
+                            int k_splits, int max_ctas, void* stream) {
+  HP_CHECK_ARG(X && W && Y && workspace && counters, "hp_gemm_swap: null pointer");
+  HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
+  HP_CHECK_ARG(N % BM == 0, "hp_gemm_swap: N must be a multiple of 128");
+  HP_CHECK_ARG(K % BK == 0, "hp_gemm_swap: K must be a multiple of 64");
+  HP_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SILU, "hp_gemm_swap: bad epilogue");
+  HP_CHECK_ARG(epilogue != EPI_RESID || R != nullptr, "hp_gemm_swap: residual epilogue needs R");
+  HP_CHECK_ARG(max_ctas >= 1, "hp_gemm_swap: max_ctas must be >= 1");
+  const int BN = T <= 32 ? 32 : (T <= 64 ? 64 : (T <= 128 ? 128 : 256));
+  GemmParams p{};
+  p.Ma = N;
+  p.Nb = T;
+  p.K = K;
+  p.m_tiles = N / BM;
+  p.n_tiles = ceil_div(T, BN);
+  p.num_kb = K / BK;
+  if (k_splits <= 0) k_splits = hp_gemm_swap_splits(T, N, K, max_ctas);
+  k_splits = std::min(k_splits, p.num_kb);
+  p.kb_per_split = ceil_div(p.num_kb, k_splits);
+  p.k_splits = ceil_div(p.num_kb, p.kb_per_split);
+  p.out = static_cast<__nv_bfloat16*>(Y);
+  p.ldo = ldy;
+  p.resid = static_cast<const __nv_bfloat16*>(R);
+  p.ldr = ldr;
+  p.ws = static_cast<float*>(workspace);
+  p.ws_ld = p.n_tiles * BN;
+  p.counters = counters;
+  p.epi = epilogue;
+  HP_CHECK_ARG(ws_bytes >= size_t(N) * p.ws_ld * sizeof(float), "hp_gemm_swap: workspace too small");
+  HP_CHECK_ARG(n_counters >= p.m_tiles * p.n_tiles, "hp_gemm_swap: too few counters");
+  CUtensorMap ta, tb;
+  int rc = cached_tmap_bf16(&ta, W, N, K, ldw, BM, BK, true);
+  if (rc) return rc;
+  rc = cached_tmap_bf16(&tb, X, T, K, ldx, BN, BK, true);
+  if (rc) return rc;
+  const int units = p.m_tiles * p.n_tiles * p.k_splits;
+  const int grid = std::min(units, max_ctas);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (BN) {
+    case 32: return launch<32, true>(ta, tb, p, grid, st);
+    case 64: return launch<64, true>(ta, tb, p, grid, st);
+    case 128: return launch<128, true>(ta, tb, p, grid, st);
+    default: return launch<256, true>(ta, tb, p, grid, st);
+  }
+}

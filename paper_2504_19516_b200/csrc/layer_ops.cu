@@ -1,0 +1,130 @@
+// Memory-bound layer glue: RMSNorm and RoPE + paged KV-cache write.
+// Both are single-pass, 16-byte vectorised and grid-strided over a persistent
+// grid sized to the partition (HBM-bound; no shared-memory staging needed).
+#include "common.cuh"
+#include "runtime.h"
+#include "../../include/hp.h"
+
+#include <algorithm>
+
+namespace hp {
+
+// One warp per row; cols % 256 == 0.  Two passes over the row (the second is
+// an L1 hit): sum of squares, then scale and write.
+__global__ void k_rmsnorm(const __nv_bfloat16* __restrict__ x, int ldx,
+                          const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out,
+                          int ldo, int rows, int cols, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(r) * ldx);
+    float ss = 0.f;
+    for (int c = lane; c < cols / 8; c += 32) {
+      uint4 v = xr[c];
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = bf16lo(u[k]), b = bf16hi(u[k]);
+        ss += a * a + b * b;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float inv = rsqrtf(ss / float(cols) + eps);
+    const uint4* wr = reinterpret_cast<const uint4*>(w);
+    uint4* orow = reinterpret_cast<uint4*>(out + size_t(r) * ldo);
+    for (int c = lane; c < cols / 8; c += 32) {
+      uint4 v = xr[c], g = wr[c], o;
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
+      const uint32_t* gg = reinterpret_cast<const uint32_t*>(&g);
+      uint32_t* oo = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        oo[k] = pack_bf16(bf16lo(u[k]) * inv * bf16lo(gg[k]), bf16hi(u[k]) * inv * bf16hi(gg[k]));
+      orow[c] = o;
+    }
+  }
+}
+
+// Thread per (token, head, 2 rotary pairs).  q heads: rotate in place.
+// k heads: rotate in place and write to the paged cache.  v heads: copy.
+// Rotary convention (Llama / rotate_half): for i < d/2,
+//   y[i] = x[i] cos - x[i+d/2] sin,  y[i+d/2] = x[i+d/2] cos + x[i] sin.
+__global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, int Hq, int Hkv,
+                                int d, const int* __restrict__ pos, const float* __restrict__ cs,
+                                const int* __restrict__ slots, __nv_bfloat16* __restrict__ kc,
+                                __nv_bfloat16* __restrict__ vc, int page) {
+  const int half = d / 2;
+  const int pairs = half / 2;             // threads per head (2 rotary dims each)
+  const int per_tok = (Hq + 2 * Hkv) * pairs;
+  const long total = long(T) * per_tok;
+  for (long idx = blockIdx.x * long(blockDim.x) + threadIdx.x; idx < total;
+       idx += long(gridDim.x) * blockDim.x) {
+    const int t = int(idx / per_tok);
+    const int rem = int(idx % per_tok);
+    const int head = rem / pairs;          // 0..Hq+2Hkv-1 across q | k | v blocks
+    const int i = (rem % pairs) * 2;       // rotary dim pair start (< d/2)
+    __nv_bfloat16* row = qkv + size_t(t) * ld + size_t(head) * d;
+    const int slot = (head >= Hq) ? slots[t] : 0;
+    const int blk = slot / page, off = slot % page;
+    if (head < Hq + Hkv) {
+      const float* c = cs + size_t(pos[t]) * d;
+      const float c0 = c[i], c1 = c[i + 1], s0 = c[half + i], s1 = c[half + i + 1];
+      const uint32_t lo = *reinterpret_cast<const uint32_t*>(row + i);
+      const uint32_t hi = *reinterpret_cast<const uint32_t*>(row + half + i);
+      const float x0 = bf16lo(lo), x1 = bf16hi(lo), y0 = bf16lo(hi), y1 = bf16hi(hi);
+      const uint32_t nlo = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
+      const uint32_t nhi = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
+      *reinterpret_cast<uint32_t*>(row + i) = nlo;
+      *reinterpret_cast<uint32_t*>(row + half + i) = nhi;
+      if (head >= Hq) {
+        const int kh = head - Hq;
+        __nv_bfloat16* dst = kc + ((size_t(blk) * Hkv + kh) * page + off) * d;
+        *reinterpret_cast<uint32_t*>(dst + i) = nlo;
+        *reinterpret_cast<uint32_t*>(dst + half + i) = nhi;
+      }
+    } else {
+      const int vh = head - Hq - Hkv;
+      __nv_bfloat16* dst = vc + ((size_t(blk) * Hkv + vh) * page + off) * d;
+      *reinterpret_cast<uint32_t*>(dst + i) = *reinterpret_cast<const uint32_t*>(row + i);
+      *reinterpret_cast<uint32_t*>(dst + half + i) = *reinterpret_cast<const uint32_t*>(row + half + i);
+    }
+  }
+}
+
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out, int ldo, int rows,
+                          int cols, float eps, int max_ctas, void* stream) {
+  HP_CHECK_ARG(x && weight && out, "hp_rmsnorm: null pointer");
+  HP_CHECK_ARG(rows >= 1 && cols >= 8 && cols % 8 == 0, "hp_rmsnorm: cols must be a multiple of 8");
+  HP_CHECK_ARG(ldx % 8 == 0 && ldo % 8 == 0, "hp_rmsnorm: row pitch must be a multiple of 8");
+  HP_CHECK_ARG(max_ctas >= 1, "hp_rmsnorm: max_ctas must be >= 1");
+  const int wpb = 8;
+  const int grid = std::min((rows + wpb - 1) / wpb, max_ctas * 4);
+  k_rmsnorm<<<grid, wpb * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(weight),
+      static_cast<__nv_bfloat16*>(out), ldo, rows, cols, eps);
+  HP_LAUNCH_CHECK("k_rmsnorm");
+  return HP_OK;
+}
+
+extern "C" int hp_rope_kv_write(void* qkv, int ldqkv, int T, int Hq, int Hkv, int d,
+                                const int* positions, const float* cos_sin, const int* slot_mapping,
+                                void* kcache, void* vcache, int page, int max_ctas, void* stream) {
+  HP_CHECK_ARG(qkv && positions && cos_sin && slot_mapping && kcache && vcache, "hp_rope_kv_write: null pointer");
+  HP_CHECK_ARG(T >= 1 && Hq >= 1 && Hkv >= 1 && d % 4 == 0, "hp_rope_kv_write: bad shape");
+  HP_CHECK_ARG(ldqkv >= (Hq + 2 * Hkv) * d && ldqkv % 2 == 0, "hp_rope_kv_write: bad row pitch");
+  HP_CHECK_ARG(page >= 1 && max_ctas >= 1, "hp_rope_kv_write: bad page/max_ctas");
+  const long total = long(T) * (Hq + 2 * Hkv) * (d / 4);
+  const int threads = 256;
+  const long want = (total + threads - 1) / threads;
+  const int grid = int(std::min<long>(want, long(max_ctas) * 8));
+  k_rope_kv_write<<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<__nv_bfloat16*>(qkv), ldqkv, T, Hq, Hkv, d, positions, cos_sin, slot_mapping,
+      static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), page);
+  HP_LAUNCH_CHECK("k_rope_kv_write");
+  return HP_OK;
+}

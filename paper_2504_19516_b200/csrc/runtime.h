@@ -1,0 +1,72 @@
+// Host-side runtime support shared by the C-ABI entry points: error state,
+// driver entry points resolved at run time (so the .so has no libcuda link
+// dependency and loads on a GPU-less host), and a tensor-map cache.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/hp.h"
+
+namespace hp {
+
+// ---- error handling: every C entry point returns 0 or a negative code and
+// leaves a message retrievable with hp_last_error().
+
+int set_error(int code, const std::string& msg);
+const char* last_error();
+
+#define HP_CHECK_ARG(cond, msg)                                  \
+  do {                                                           \
+    if (!(cond)) return ::hp::set_error(HP_ERR_INVALID, msg); \
+  } while (0)
+
+#define HP_CUDA_TRY(expr)                                                            \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return ::hp::set_error(HP_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define HP_LAUNCH_CHECK(name)                                                        \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess)                                                           \
+      return ::hp::set_error(HP_ERR_CUDA, std::string(name ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---- driver API (resolved lazily through cudaGetDriverEntryPoint)
+struct Driver {
+  bool loaded = false;
+  decltype(&::cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
+  decltype(&::cuDeviceGetDevResource) deviceGetDevResource = nullptr;
+  decltype(&::cuDevSmResourceSplitByCount) devSmResourceSplitByCount = nullptr;
+  decltype(&::cuDevResourceGenerateDesc) devResourceGenerateDesc = nullptr;
+  decltype(&::cuGreenCtxCreate) greenCtxCreate = nullptr;
+  decltype(&::cuGreenCtxDestroy) greenCtxDestroy = nullptr;
+  decltype(&::cuGreenCtxStreamCreate) greenCtxStreamCreate = nullptr;
+  decltype(&::cuStreamDestroy) streamDestroy = nullptr;
+  decltype(&::cuDeviceGet) deviceGet = nullptr;
+  decltype(&::cuGetErrorString) getErrorString = nullptr;
+};
+
+// Returns nullptr (with hp_last_error set) when the driver is unavailable.
+const Driver* driver();
+std::string cu_error_string(CUresult r);
+
+// 2-D bf16 row-major tensor map: rows x cols, row pitch `ld` elements,
+// box = box_rows x box_cols (box_cols * 2 bytes must be 128 for SW128).
+int make_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                   uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+// Cached variant keyed on all arguments (pointers and shapes are stable
+// across steps for weights and persistent activation buffers).
+int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
+                     uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+int device_sm_count();
+
+}  // namespace hp

@@ -1,0 +1,210 @@
+"""ctypes binding of ``libb200hot.so`` (the C ABI declared in include/hp.h).
+
+This module is the only place Python touches the native library.  There is no
+fallback: if the library is missing or a call fails, `HotPathError` is raised
+with the library's own error string.  Tensor helpers accept torch tensors and
+pass raw device pointers plus the current (or given) CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from ..errors import InvalidArgumentError
+
+LIB_PATH = Path(__file__).resolve().parent.parent / "_lib" / "libb200hot.so"
+
+EPI_STORE, EPI_RESID, EPI_SILU = 0, 1, 2
+
+# Every symbol include/hp.h declares, with (restype, argtypes).
+_i, _u64, _p, _f, _sz, _i64 = C.c_int, C.c_uint64, C.c_void_p, C.c_float, C.c_size_t, C.c_int64
+SIGNATURES = {
+    "hp_abi_version": (_i, []),
+    "hp_last_error": (C.c_char_p, []),
+    "hp_device_count": (_i, []),
+    "hp_device_sms": (_i, [_i, C.POINTER(_i)]),
+    "hp_wave_stats": (_i, [_i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(C.c_double)]),
+    "hp_partition_create": (_i, [_i, _i, C.POINTER(_p)]),
+    "hp_partition_stream": (_i, [_p, _i, C.POINTER(_p)]),
+    "hp_partition_sms": (_i, [_p, _i, C.POINTER(_i)]),
+    "hp_partition_destroy": (_i, [_p]),
+    "hp_rmsnorm": (_i, [_p, _i, _p, _p, _i, _i, _i, _f, _i, _p]),
+    "hp_gemm": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
+    "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _i, _p]),
+    "hp_gemm_swap_splits": (_i, [_i, _i, _i, _i]),
+    "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
+    "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
+    "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
+    "hp_decode_attn": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _f, _p, _sz, _i, _p]),
+    "hp_probe": (_i, [_i, _i, _i64, _p, _p]),
+}
+
+
+class HotPathError(RuntimeError):
+    """A call into libb200hot.so failed (message from hp_last_error)."""
+
+
+_LIB = None
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the ctypes handle; raises if the .so is absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise HotPathError(
+            f"{p} not found: build it with `python -m paper_2504_19516_b200.build` "
+            "(there is no CPU fallback for the hot path)")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = load().hp_last_error().decode(errors="replace")
+        if rc == -1:
+            raise InvalidArgumentError(f"{what}: {msg}")
+        raise HotPathError(f"{what} failed ({rc}): {msg}")
+
+
+def wave_stats(g: int, b: int, n: int) -> tuple[int, int, float]:
+    w, t, idle = _i64(), _i64(), C.c_double()
+    check(load().hp_wave_stats(g, b, n, C.byref(w), C.byref(t), C.byref(idle)), "hp_wave_stats")
+    return w.value, t.value, idle.value
+
+
+# --------------------------------------------------------------- torch glue
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def device_sms(device: int = 0) -> int:
+    n = _i()
+    check(load().hp_device_sms(device, C.byref(n)), "hp_device_sms")
+    return n.value
+
+
+def rmsnorm(x, weight, out, eps: float, max_ctas: int, stream=None) -> None:
+    rows, cols = x.shape
+    check(load().hp_rmsnorm(_ptr(x), x.stride(0), _ptr(weight), _ptr(out), out.stride(0), rows, cols,
+                            eps, max_ctas, _stream(stream)), "hp_rmsnorm")
+
+
+def gemm(x, w, y, epilogue: int = EPI_STORE, resid=None, max_ctas: int = 148, stream=None) -> None:
+    T, K = x.shape
+    N = w.shape[0]
+    check(load().hp_gemm(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
+                         _ptr(resid), resid.stride(0) if resid is not None else 0, T, N, K,
+                         epilogue, max_ctas, _stream(stream)), "hp_gemm")
+
+
+def gemm_swap(x, w, y, ws, counters, epilogue: int = EPI_STORE, resid=None, k_splits: int = 0,
+              max_ctas: int = 148, stream=None) -> None:
+    T, K = x.shape
+    N = w.shape[0]
+    check(load().hp_gemm_swap(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
+                              _ptr(resid), resid.stride(0) if resid is not None else 0, T, N, K,
+                              epilogue, _ptr(ws), ws.numel() * ws.element_size(), _ptr(counters),
+                              counters.numel(), k_splits, max_ctas, _stream(stream)), "hp_gemm_swap")
+
+
+def rope_kv_write(qkv, Hq: int, Hkv: int, d: int, positions, cos_sin, slots, kcache, vcache,
+                  page: int, max_ctas: int = 148, stream=None) -> None:
+    T = qkv.shape[0]
+    check(load().hp_rope_kv_write(_ptr(qkv), qkv.stride(0), T, Hq, Hkv, d, _ptr(positions),
+                                  _ptr(cos_sin), _ptr(slots), _ptr(kcache), _ptr(vcache), page,
+                                  max_ctas, _stream(stream)), "hp_rope_kv_write")
+
+
+def prefill_attn(q, k, v, o, cu_seqlens, nseq: int, max_seqlen: int, Hq: int, Hkv: int, d: int,
+                 scale: float, max_ctas: int = 148, stream=None) -> None:
+    check(load().hp_prefill_attn(_ptr(q), q.stride(0), _ptr(k), k.stride(0), _ptr(v), v.stride(0),
+                                 _ptr(o), o.stride(0), _ptr(cu_seqlens), nseq, q.shape[0], max_seqlen, Hq, Hkv,
+                                 d, scale, max_ctas, _stream(stream)), "hp_prefill_attn")
+
+
+def decode_attn_ws_bytes(B: int, Hq: int, d: int, max_splits: int) -> int:
+    return load().hp_decode_attn_ws_bytes(B, Hq, d, max_splits)
+
+
+def decode_attn(q, kcache, vcache, block_table, ctx_lens, out, Hq: int, Hkv: int, d: int,
+                page: int, scale: float, ws=None, max_ctas: int = 148, stream=None) -> None:
+    B = q.shape[0]
+    check(load().hp_decode_attn(_ptr(q), q.stride(0), _ptr(kcache), _ptr(vcache), _ptr(block_table),
+                                block_table.shape[1], _ptr(ctx_lens), _ptr(out), out.stride(0), B, Hq,
+                                Hkv, d, page, kcache.shape[0], scale, _ptr(ws),
+                                0 if ws is None else ws.numel() * ws.element_size(), max_ctas,
+                                _stream(stream)), "hp_decode_attn")
+
+
+def probe(out, ctas: int, threads: int = 128, spin_ns: int = 20000, stream=None) -> None:
+    check(load().hp_probe(ctas, threads, spin_ns, _ptr(out), _stream(stream)), "hp_probe")
+
+
+class Partition:
+    """A green-context SM split: `decode_sms` SMs for decode, the rest for prefill.
+
+    Realises the reference's partition masks (engine.py:440-452) on hardware;
+    `stream(phase)` returns a torch ExternalStream confined to that side.
+    """
+
+    def __init__(self, decode_sms: int, device: int = 0):
+        h = _p()
+        check(load().hp_partition_create(device, decode_sms, C.byref(h)), "hp_partition_create")
+        self._h = h
+        self.device = device
+        self.sms = {}
+        self._streams = {}
+        for phase in (0, 1):
+            n = _i()
+            check(load().hp_partition_sms(h, phase, C.byref(n)), "hp_partition_sms")
+            self.sms[phase] = n.value
+            s = _p()
+            check(load().hp_partition_stream(h, phase, C.byref(s)), "hp_partition_stream")
+            self._streams[phase] = s.value
+
+    @property
+    def prefill_sms(self) -> int:
+        return self.sms[0]
+
+    @property
+    def decode_sms(self) -> int:
+        return self.sms[1]
+
+    def raw_stream(self, phase: int) -> int:
+        return self._streams[phase]
+
+    def stream(self, phase: int):
+        import torch
+
+        return torch.cuda.ExternalStream(self._streams[phase], device=torch.device("cuda", self.device))
+
+    def close(self) -> None:
+        if self._h is not None:
+            load().hp_partition_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass

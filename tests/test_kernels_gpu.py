@@ -1,0 +1,272 @@
+"""Kernel-level numerics of libb200hot.so against torch fp32 references.
+
+Floating-point kernels are compared with a plain fp32 restatement of the same
+op (bf16 inputs upcast); tolerances are stated per test.  Run on a B200 with
+`pytest -m gpu`.
+"""
+
+import math
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2504_19516_b200.device import lib  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def rel_err(got, ref):
+    got = got.float()
+    ref = ref.float()
+    return ((got - ref).abs().max() / ref.abs().max().clamp_min(1e-6)).item()
+
+
+def bf(shape, scale=1.0, gen=None):
+    return (torch.randn(*shape, generator=gen, device=DEV) * scale).to(torch.bfloat16)
+
+
+@pytest.fixture(scope="module")
+def gen():
+    g = torch.Generator(device=DEV)
+    g.manual_seed(1234)
+    return g
+
+
+# ------------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("T,N,K", [(128, 256, 256), (200, 384, 512), (1024, 6144, 4096),
+                                   (77, 4096, 4096), (4096, 1024, 1024)])
+def test_gemm_store(T, N, K, gen):
+    x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
+    y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
+    lib.gemm(x, w, y, lib.EPI_STORE, max_ctas=148)
+    ref = x.float() @ w.float().T
+    torch.cuda.synchronize()
+    assert rel_err(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("max_ctas", [1, 16, 148])
+def test_gemm_grid_sizes(max_ctas, gen):
+    T, N, K = 300, 512, 640
+    x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
+    y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
+    lib.gemm(x, w, y, lib.EPI_STORE, max_ctas=max_ctas)
+    assert rel_err(y, x.float() @ w.float().T) < 1e-2
+
+
+def test_gemm_resid(gen):
+    T, N, K = 333, 4096, 1024
+    x, w, r = bf((T, K), gen=gen), bf((N, K), 0.05, gen), bf((T, N), gen=gen)
+    y = torch.empty_like(r)
+    lib.gemm(x, w, y, lib.EPI_RESID, resid=r)
+    assert rel_err(y, x.float() @ w.float().T + r.float()) < 1e-2
+    # in place (out aliases the residual), as the layer uses it
+    r2 = r.clone()
+    lib.gemm(x, w, r2, lib.EPI_RESID, resid=r2)
+    assert rel_err(r2, x.float() @ w.float().T + r.float()) < 1e-2
+
+
+def silu_ref(z):
+    return z * torch.sigmoid(z)
+
+
+def interleave_ref(N2, K, gen):
+    """Weight with gate/up rows interleaved in blocks of 64, plus the plain halves."""
+    g, u = bf((N2, K), 0.05, gen), bf((N2, K), 0.05, gen)
+    w = torch.stack([g.view(-1, 64, K), u.view(-1, 64, K)], dim=1).reshape(2 * N2, K)
+    return w.contiguous(), g, u
+
+
+@pytest.mark.parametrize("T", [64, 257])
+def test_gemm_silu(T, gen):
+    N2, K = 1024, 512
+    w, g, u = interleave_ref(N2, K, gen)
+    x = bf((T, K), gen=gen)
+    y = torch.empty(T, N2, device=DEV, dtype=torch.bfloat16)
+    lib.gemm(x, w, y, lib.EPI_SILU)
+    ref = silu_ref(x.float() @ g.float().T) * (x.float() @ u.float().T)
+    assert rel_err(y, ref) < 2e-2
+
+
+def _ws(N, T):
+    bn = 32 if T <= 32 else 64 if T <= 64 else 128 if T <= 128 else 256
+    cols = -(-T // bn) * bn
+    ws = torch.zeros(N, cols, device=DEV, dtype=torch.float32)
+    cnt = torch.zeros((N // 128) * (-(-T // bn)), device=DEV, dtype=torch.int32)
+    return ws, cnt
+
+
+@pytest.mark.parametrize("T,N,K,splits", [(1, 128, 256, 1), (8, 6144, 4096, 0), (32, 4096, 4096, 0),
+                                          (33, 1024, 1024, 3), (100, 512, 2048, 0), (256, 256, 512, 2)])
+def test_gemm_swap_store(T, N, K, splits, gen):
+    x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
+    y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
+    ws, cnt = _ws(N, T)
+    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, k_splits=splits, max_ctas=64)
+    assert rel_err(y, x.float() @ w.float().T) < 1e-2
+    # workspace and counters are left clean for the next call
+    torch.cuda.synchronize()
+    assert ws.abs().max().item() == 0.0 and cnt.abs().max().item() == 0
+    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, k_splits=splits, max_ctas=64)
+    assert rel_err(y, x.float() @ w.float().T) < 1e-2
+
+
+def test_gemm_swap_resid_silu(gen):
+    T, K = 32, 1024
+    x, r = bf((T, K), gen=gen), bf((T, 4096), gen=gen)
+    w = bf((4096, K), 0.05, gen)
+    ws, cnt = _ws(4096, T)
+    y = r.clone()
+    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_RESID, resid=y, max_ctas=32)
+    assert rel_err(y, x.float() @ w.float().T + r.float()) < 1e-2
+    wi, g, u = interleave_ref(1024, K, gen)
+    ws2, cnt2 = _ws(2048, T)
+    y2 = torch.empty(T, 1024, device=DEV, dtype=torch.bfloat16)
+    lib.gemm_swap(x, wi, y2, ws2, cnt2, lib.EPI_SILU, max_ctas=32)
+    ref = silu_ref(x.float() @ g.float().T) * (x.float() @ u.float().T)
+    assert rel_err(y2, ref) < 2e-2
+
+
+# ------------------------------------------------------------- RMSNorm / RoPE
+def test_rmsnorm(gen):
+    x, wt = bf((77, 4096), gen=gen), bf((4096,), 1.0, gen)
+    out = torch.empty_like(x)
+    lib.rmsnorm(x, wt, out, 1e-5, max_ctas=16)
+    xf = x.float()
+    ref = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5) * wt.float()
+    assert rel_err(out, ref) < 1e-2
+
+
+def rope_table(max_pos, d, theta=500000.0):
+    inv = 1.0 / (theta ** (torch.arange(0, d, 2, dtype=torch.float64) / d))
+    ang = torch.arange(max_pos, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.cat([ang.cos(), ang.sin()], dim=1).float().to(DEV)
+
+
+def test_rope_kv_write(gen):
+    T, Hq, Hkv, d, page = 100, 8, 2, 128, 64
+    qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
+    orig = qkv.float().clone()
+    pos = torch.randint(0, 4000, (T,), device=DEV, dtype=torch.int32)
+    nblk = 8
+    slots = torch.randperm(nblk * page, device=DEV)[:T].to(torch.int32)
+    kc = torch.zeros(nblk, Hkv, page, d, device=DEV, dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    cs = rope_table(4096, d)
+    lib.rope_kv_write(qkv, Hq, Hkv, d, pos, cs, slots, kc, vc, page)
+    cos, sin = cs[pos.long(), : d // 2], cs[pos.long(), d // 2:]
+
+    def rot(x):  # [T, H, d]
+        x1, x2 = x[..., : d // 2], x[..., d // 2:]
+        c, s = cos[:, None, :], sin[:, None, :]
+        return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
+
+    o3 = orig.view(T, Hq + 2 * Hkv, d)
+    q_ref, k_ref, v_ref = rot(o3[:, :Hq]), rot(o3[:, Hq:Hq + Hkv]), o3[:, Hq + Hkv:]
+    got = qkv.float().view(T, Hq + 2 * Hkv, d)
+    assert rel_err(got[:, :Hq], q_ref) < 1e-2
+    assert rel_err(got[:, Hq:Hq + Hkv], k_ref) < 1e-2
+    blk, off = (slots // page).long(), (slots % page).long()
+    assert rel_err(kc[blk, :, off], k_ref) < 1e-2
+    assert torch.equal(vc[blk, :, off].float(), v_ref)
+
+
+# ------------------------------------------------------------- attention
+def attn_ref(q, k, v, causal, scale):
+    """q [Tq, Hq, d], k/v [Tk, Hkv, d] fp32; causal aligns the last query to the last key."""
+    Hq, Hkv = q.shape[1], k.shape[1]
+    k = k.repeat_interleave(Hq // Hkv, dim=1)
+    v = v.repeat_interleave(Hq // Hkv, dim=1)
+    s = torch.einsum("qhd,khd->hqk", q, k) * scale
+    if causal:
+        Tq, Tk = q.shape[0], k.shape[0]
+        mask = torch.ones(Tq, Tk, dtype=torch.bool, device=q.device).tril(Tk - Tq)
+        s = s.masked_fill(~mask, float("-inf"))
+    return torch.einsum("hqk,khd->qhd", s.softmax(-1), v)
+
+
+@pytest.mark.parametrize("lens,Hq,Hkv", [([128], 4, 1), ([1000], 8, 2), ([64, 130, 7], 4, 4),
+                                         ([2048], 32, 8)])
+def test_prefill_attn(lens, Hq, Hkv, gen):
+    d = 128
+    T = sum(lens)
+    qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
+    q, k, v = qkv[:, : Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
+    o = torch.zeros(T, Hq * d, device=DEV, dtype=torch.bfloat16)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), device=DEV, dtype=torch.int32)
+    scale = 1.0 / math.sqrt(d)
+    lib.prefill_attn(q, k, v, o, cu, len(lens), max(lens), Hq, Hkv, d, scale)
+    s0 = 0
+    for L in lens:
+        sl = slice(s0, s0 + L)
+        ref = attn_ref(q[sl].float().view(L, Hq, d), k[sl].float().view(L, Hkv, d),
+                       v[sl].float().view(L, Hkv, d), True, scale)
+        got = o[sl].float().view(L, Hq, d)
+        assert (got - ref).abs().max().item() < 2e-2
+        s0 += L
+
+
+def make_cache(B, ctx, Hkv, d, page, gen, extra_blocks=3):
+    pages = [-(-c // page) for c in ctx]
+    nblk = sum(pages) + extra_blocks
+    kc = bf((nblk, Hkv, page, d), gen=gen)
+    vc = bf((nblk, Hkv, page, d), gen=gen)
+    perm = torch.randperm(nblk, device=DEV).to(torch.int32)
+    max_pages = max(pages)
+    bt = torch.zeros(B, max_pages, device=DEV, dtype=torch.int32)
+    i = 0
+    for b, p in enumerate(pages):
+        bt[b, :p] = perm[i:i + p]
+        i += p
+    return kc, vc, bt
+
+
+@pytest.mark.parametrize("ctx,Hq,Hkv", [([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2),
+                                        ([2048] * 32, 32, 8), ([1], 8, 1), ([5000, 33], 64, 8)])
+@pytest.mark.parametrize("max_ctas", [8, 148])
+def test_decode_attn(ctx, Hq, Hkv, max_ctas, gen):
+    d, page = 128, 64
+    B = len(ctx)
+    kc, vc, bt = make_cache(B, ctx, Hkv, d, page, gen)
+    q = bf((B, Hq * d), gen=gen)
+    out = torch.zeros(B, Hq * d, device=DEV, dtype=torch.bfloat16)
+    ctx_t = torch.tensor(ctx, device=DEV, dtype=torch.int32)
+    ws = torch.empty(lib.decode_attn_ws_bytes(B, Hq, d, 256) // 4, device=DEV, dtype=torch.float32)
+    scale = 1.0 / math.sqrt(d)
+    lib.decode_attn(q, kc, vc, bt, ctx_t, out, Hq, Hkv, d, page, scale, ws=ws, max_ctas=max_ctas)
+    for b, c in enumerate(ctx):
+        np_ = -(-c // page)
+        blocks = bt[b, :np_].long()
+        k = kc[blocks].permute(0, 2, 1, 3).reshape(-1, Hkv, d)[:c].float()
+        v = vc[blocks].permute(0, 2, 1, 3).reshape(-1, Hkv, d)[:c].float()
+        ref = attn_ref(q[b].float().view(1, Hq, d), k, v, False, scale)
+        got = out[b].float().view(1, Hq, d)
+        assert (got - ref).abs().max().item() < 2e-2, f"seq {b} ctx {c}"
+
+
+# ------------------------------------------------------------- partitions
+def test_wave_stats_native():
+    assert lib.wave_stats(216, 2, 108) == (1, 108, 0.0)
+    assert lib.wave_stats(110, 1, 108) == (2, 2, 106 / 216)
+    assert lib.wave_stats(384, 1, 148) == (3, 88, (148 - 88) / (148 * 3))
+
+
+def test_partition_confinement():
+    n = lib.device_sms(0)
+    part = lib.Partition(16)
+    assert part.decode_sms == 16 and part.prefill_sms == n - 16
+    outs = {}
+    for phase in (0, 1):
+        buf = torch.zeros(4 * n, 3, device=DEV, dtype=torch.int64)
+        lib.probe(buf, 4 * n, spin_ns=50000, stream=part.raw_stream(phase))
+        torch.cuda.synchronize()
+        outs[phase] = set(buf[:, 0].tolist())
+    assert len(outs[1]) <= 16
+    assert len(outs[0]) <= n - 16
+    assert not (outs[0] & outs[1])
+    part.close()
