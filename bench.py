@@ -1,0 +1,354 @@
+"""Benchmark: co-executed prefill + decode on SM partitions of one B200
+(BASELINE.json config 2, Llama-3-8B single layer, bf16).
+
+One STEP = one prefill layer over a T-token chunk (default 4096) on a
+green-context partition of pm SMs, co-executed with n decode layer-steps
+(batch 32, context 2048, paged KV) on the remaining dm SMs.  n is the number
+of decode steps that fit in one prefill layer at that split.  The split
+(pm, dm) is chosen during warm-up on the 8-SM green-context grid: the
+highest tokens/s whose p50 TTFT/TPOT proxies are no worse than the
+time-sliced baseline's (same kernels, one full-GPU stream, prefill layer and
+decode step alternating).
+
+Metric: tokens/s = (T + 32 n) per step / device time (layer-tokens; divide by
+32 layers for model-equivalent tokens).  Inputs (weights 436 MB + KV 269 MB
++ activations per step) exceed the 126 MB L2, so no explicit flush.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun): independent replicas, one per GPU (the path has no
+exchange step); value = total tokens / max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tokens/sec with co-executed prefill+decode per B200; p50 TTFT/TPOT; SM idle %"
+UNIT = "tokens/s"
+DECODE_BATCH, DECODE_CTX = 32, 2048
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- CPU oracle
+def cpu_reference_step(T: int, B: int, C: int, seed: int = 0):
+    """Time one bounded sample of the workload with the numpy CPU oracle:
+    one Llama-3-8B prefill layer over T tokens + one decode layer-step for
+    B sequences of context C.  Returns (seconds, tokens)."""
+    import numpy as np
+
+    from oracle import numerics as O
+    from paper_2504_19516_b200.workload import MODEL_PRESETS
+
+    m = MODEL_PRESETS["llama3-8b"]
+    rng = np.random.default_rng(seed)
+    h, I, d, Hq, Hkv = m.hidden, m.intermediate, m.head_dim, m.num_heads, m.num_kv_heads
+
+    def w(*s):
+        return (rng.standard_normal(s, dtype=np.float32) * 0.02)
+
+    W = O.LayerWeights(w(m.qkv_out_dim, h), w(h, h), w(I, h), w(I, h), w(h, I),
+                       np.ones(h, np.float32), np.ones(h, np.float32))
+    table = O.rope_table(max(T, C) + 1, d)
+    x = rng.standard_normal((T, h), dtype=np.float32)
+    pages = -(-C // 64)
+    kc = rng.standard_normal((B * pages, Hkv, 64, d), dtype=np.float32)
+    vc = rng.standard_normal((B * pages, Hkv, 64, d), dtype=np.float32)
+    bt = rng.permutation(B * pages).reshape(B, pages)
+    ctx = np.full(B, C)
+    xd = rng.standard_normal((B, h), dtype=np.float32)
+    t0 = time.perf_counter()
+    O.layer_prefill(x, W, Hq, Hkv, d, np.arange(T), table, bf16_boundaries=False)
+    O.layer_decode(xd, W, Hq, Hkv, d, ctx, table, kc, vc, bt, bf16_boundaries=False)
+    return time.perf_counter() - t0, T + B
+
+
+def cpu_threads() -> int:
+    try:
+        import numpy as np  # noqa: F401
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(n[0]) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count() or 1
+
+
+CPU_SAMPLE_T = 512
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference path's CPU implementation (the numpy
+    oracle port; the reference itself has no numerics) on the host cores."""
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX)
+    secs, toks = 0.0, 0
+    for _ in range(args.steps):
+        s, t = cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX)
+        secs += s
+        toks += t
+    v = toks / secs
+    sample = f"1 prefill layer x {CPU_SAMPLE_T} tokens + 1 decode step (B={DECODE_BATCH}, ctx {DECODE_CTX}), Llama-3-8B layer, numpy fp32"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "llama3-8b 1 layer: prefill chunk + decode batch 32 ctx 2048 (CPU sample)",
+                       "prefill_tokens": CPU_SAMPLE_T, "decode_batch": DECODE_BATCH,
+                       "decode_ctx": DECODE_CTX, "parallelism": "replicas"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--prefill-tokens", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return 0
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+
+    from paper_2504_19516_b200.device.corun import CoRunner
+    from paper_2504_19516_b200.device.partition import DECODE, PREFILL
+    from paper_2504_19516_b200.workload import MODEL_PRESETS
+
+    hbm_gbs, tf_burst, tf_sus, peak_src = _peaks()
+    model = MODEL_PRESETS["llama3-8b"]
+    T = args.prefill_tokens
+    cr = CoRunner(model, T, DECODE_BATCH, DECODE_CTX, device=local, seed=1234 + rank)
+    N = cr.n
+
+    # ---- warm-up: isolated latencies, baseline, split selection
+    t_p_full = cr.isolated(PREFILL, N)
+    t_d_full = cr.isolated(DECODE, N)
+    ts_ttft = ts_tpot = t_p_full + t_d_full  # alternating: every decode step waits one prefill layer
+    ts_alt = cr.time_sliced(args.warmup, 1)
+    candidates = []
+    for dm in range(8, 72, 8):
+        pm = N - dm
+        t_d = cr.isolated(DECODE, dm, reps=3)
+        t_p = cr.isolated(PREFILL, pm, reps=3)
+        n = max(1, round(t_p / t_d))
+        r = cr.corun(pm, dm, 2, n)
+        ok = r.p50(r.decode_layer_s) <= ts_tpot and r.p50(r.prefill_layer_s) <= ts_ttft
+        candidates.append({"pm": pm, "dm": dm, "n": n, "tokens_per_s": r.tokens_per_s,
+                           "ttft_p50_us": 1e6 * r.p50(r.prefill_layer_s),
+                           "tpot_p50_us": 1e6 * r.p50(r.decode_layer_s), "slo_ok": ok})
+    ok = [c for c in candidates if c["slo_ok"]] or candidates
+    best = max(ok, key=lambda c: c["tokens_per_s"])
+    if dist is not None:  # identical split on every replica (rank 0 decides)
+        t = torch.tensor([best["dm"], best["n"]], device="cuda")
+        dist.broadcast(t, 0)
+        dmv, nv = int(t[0]), int(t[1])
+        best = next((c for c in candidates if c["dm"] == dmv), dict(best, dm=dmv, pm=N - dmv))
+        best["n"] = nv
+    pm, dm, n = best["pm"], best["dm"], best["n"]
+    for _ in range(args.warmup):
+        cr.corun(pm, dm, 1, n)
+
+    # ---- timed region (device time, max over ranks)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        res = cr.corun(pm, dm, args.steps, n, time_upgate=True)
+    torch.cuda.synchronize()
+    span = res.span_s
+    tokens = res.tokens
+    if dist is not None:
+        t = torch.tensor([span], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        span = float(t.item())
+        tk = torch.tensor([tokens], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tk)
+        tokens = int(tk.item())
+        dist.barrier()
+    value = tokens / span
+
+    # ---- end to end: pinned host buffers, H2D inputs + D2H outputs per step
+    h = model.hidden
+    pin_px = torch.empty(T, h, dtype=torch.bfloat16, pin_memory=True)
+    pin_py = torch.empty(T, h, dtype=torch.bfloat16, pin_memory=True)
+    pin_dx = torch.empty(DECODE_BATCH, h, dtype=torch.bfloat16, pin_memory=True)
+    pin_dy = torch.empty(DECODE_BATCH, h, dtype=torch.bfloat16, pin_memory=True)
+    pin_px.copy_(cr.px.cpu())
+    pin_dx.copy_(cr.dx.cpu())
+
+    def copy_in(phase, stream):
+        if phase == PREFILL:
+            cr.px.copy_(pin_px, non_blocking=True)
+        else:
+            cr.dx.copy_(pin_dx, non_blocking=True)
+
+    def copy_out(phase, stream):
+        if phase == PREFILL:
+            pin_py.copy_(cr.py, non_blocking=True)
+        else:
+            pin_dy.copy_(cr.dy, non_blocking=True)
+
+    e2e_res = cr.corun(pm, dm, args.steps, n, copy_in=copy_in, copy_out=copy_out)
+    e2e_span = e2e_res.span_s
+    e2e_tokens = e2e_res.tokens
+    if dist is not None:
+        t = torch.tensor([e2e_span], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_span = float(t.item())
+        e2e_tokens *= world
+    h2d = T * h * 2 + n * DECODE_BATCH * h * 2
+    d2h = h2d
+
+    # ---- time-sliced baseline (same kernels, full GPU, alternating)
+    ts_eq = cr.time_sliced(args.steps, n)  # equal work
+
+    # ---- roofline of the dominant kernel (mlp_up_gate GEMM, tensor-bound)
+    ug = statistics.mean(res.upgate_s)
+    achieved = cr.upgate_flops() / ug / 1e12
+    peak = tf_sus * pm / N
+    traffic = None
+    prof = ROOT / "profiles" / "roofline_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("mlp_up_gate_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        secs, toks = 0.0, 0
+        for _ in range(2):
+            s, t = cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX)
+            secs += s
+            toks += t
+        cpu = {"value": toks / secs, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+               "sample": f"numpy oracle: 1 prefill layer x {CPU_SAMPLE_T} tokens + 1 decode step "
+                         f"(B={DECODE_BATCH}, ctx {DECODE_CTX}), x2"}
+
+    per_step_launches = 8 + n * cr.launches_per_decode_step()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * span / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init Llama-3-8B layer weights, N(0,1) activations and KV)",
+        "config": {"workload": f"llama3-8b 1 layer: prefill chunk {T} tok on {pm} SMs || decode batch "
+                               f"{DECODE_BATCH} ctx {DECODE_CTX} on {dm} SMs (green contexts)",
+                   "model": "llama3-8b (1 layer)", "prefill_tokens": T, "decode_batch": DECODE_BATCH,
+                   "decode_ctx": DECODE_CTX, "pm": pm, "dm": dm, "decode_steps_per_prefill_layer": n,
+                   "parallelism": f"replicas x{world}", "l2": "inputs exceed L2 (weights+KV 1.1 GB/step)"},
+        "p50_ttft_us": 1e6 * res.p50(res.prefill_layer_s),
+        "p50_tpot_us": 1e6 * res.p50(res.decode_layer_s),
+        "time_sliced": {
+            "alternating": {"tokens_per_s": ts_alt.tokens_per_s, "p50_ttft_us": 1e6 * ts_ttft,
+                            "p50_tpot_us": 1e6 * ts_tpot},
+            "equal_work": {"tokens_per_s": ts_eq.tokens_per_s, "span_ratio": ts_eq.span_s / res.span_s},
+        },
+        "split_sweep": candidates,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "mlp_up_gate (tcgen05 GEMM + SiLU)",
+                     "peak_basis": f"bf16_tflops_sustained ({peak_src}) x pm/N = {tf_sus} x {pm}/{N}"},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_tokens / e2e_span, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": args.steps * per_step_launches,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

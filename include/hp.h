@@ -83,15 +83,16 @@ int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out, int ldo, i
 int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
             int ldr, int T, int N, int K, int epilogue, int max_ctas, void* stream);
 
-/* Swap-AB split-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
- * hp_gemm; W streams through UMMA-M, split along K over `k_splits` CTAs
- * (<=0: automatic).  workspace: fp32 [N, ceil(T/BN)*BN] zeroed before the
- * first call (kept zero by the kernel); counters: int [N/128 * ceil(T/BN)]
- * zeroed likewise.  layer_kernels phase "decode" (workload.py:153-210). */
+/* Swap-AB stream-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
+ * hp_gemm; W streams through UMMA-M and the (tile, k-block) space is split
+ * evenly over `max_ctas` CTAs.  workspace: fp32, hp_gemm_swap_ws_bytes()
+ * bytes (contents irrelevant); counters: int [N/128 * ceil(T/BN)], zero
+ * before the first call (the kernel leaves them zero).  layer_kernels phase
+ * "decode" (workload.py:153-210). */
+size_t hp_gemm_swap_ws_bytes(int T, int N, int K, int max_ctas);
 int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
                  int ldr, int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes,
-                 int* counters, int n_counters, int k_splits, int max_ctas, void* stream);
-int hp_gemm_swap_splits(int T, int N, int K, int max_ctas);
+                 int* counters, int n_counters, int max_ctas, void* stream);
 
 /* RoPE on q,k in the fused qkv buffer [T, (Hq+2Hkv)*d] (in place) and the
  * paged KV-cache write of k,v (the `kv_write` bytes of the attention kernel,

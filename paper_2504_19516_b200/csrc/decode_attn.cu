@@ -3,21 +3,28 @@
 // ctx_lens[b] cached positions.  HBM-bound: every cached K/V byte is read
 // once per step.
 //
-// Layout: kcache/vcache [num_blocks, Hkv, page, d] bf16 (page = 64, d = 128),
-// so one (block, kv head) page is a contiguous 16 KB run.  The cache is viewed
-// as a 2-D tensor [num_blocks*Hkv*page, d] and streamed with TMA in tiles of
-// 32 tokens (half a page, 128B-swizzled) into a 12-stage shared-memory ring
-// filled by a dedicated producer warp -- ~190 KB in flight per SM.
+// Layout: kcache/vcache [num_blocks, Hkv, page, D] bf16 (page a multiple of
+// 32, D in {64, 128}), so one (block, kv head) page is a contiguous run.  The
+// cache is viewed as a 2-D tensor [num_blocks*Hkv*page, D] and streamed with
+// TMA in tiles of 32 tokens (128B-swizzled boxes of 64 dims) into a 12-stage
+// shared-memory ring filled by a dedicated producer warp (~190 KB in flight
+// per SM at D = 128).  The producer pre-loads block-table windows and the
+// next unit's metadata so no dependent global load sits between two TMA
+// issues.
 //
 // Work unit = (sequence b, kv head, split of `tps` 32-token tiles).  Four
 // consumer warps take the unit's tiles round-robin; each computes the GQA
 // group's scores with tensor cores in "swap" orientation
-//     S^T[32 tok, 8 heads] = K[32, 128] . Q^T[128, 8]     (mma.m16n8k16)
-//     O^T[128, 8]         += V^T[128, 32] . P^T[32, 8]
-// so the tiny query group (<= 8 heads) sits in the MMA's N=8 dimension,
-// keeps an online softmax (warp-shuffle max/sum), and the warps merge their
+//     S^T[32 tok, 8 heads] = K[32, D] . Q^T[D, 8]        (mma.m16n8k16)
+//     O^T[D, 8]           += V^T[D, 32] . P^T[32, 8]
+// so the query group (<= 8 heads) sits in the MMA's N=8 dimension, keeps an
+// exp2 online softmax with warp-shuffle max/sum, and the warps merge their
 // (m, l, O) at the unit end.  Multi-split sequences write fp32 partials that
 // k_decode_combine merges by log-sum-exp.
+//
+// Caches must not hold NaN/Inf in unused slots of partially filled pages
+// (allocate them zeroed): masked probabilities are exactly 0, but 0 * NaN is
+// NaN inside the MMA.
 #include "common.cuh"
 #include "runtime.h"
 #include "../../include/hp.h"
@@ -27,17 +34,22 @@
 
 namespace hp {
 
-constexpr int DA_D = 128;
 constexpr int DA_TILE = 32;
 constexpr int DA_STAGES = 12;
 constexpr int DA_CONSUMERS = 4;
 constexpr int DA_THREADS = (DA_CONSUMERS + 1) * 32;
-constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;           // 32 rows x 128 B
-constexpr uint32_t DA_STAGE_BYTES = 4 * DA_BOX_BYTES;          // K lo/hi + V lo/hi
-constexpr int DA_PROW = 40;                                    // padded P^T row (bf16)
-constexpr size_t DA_SMEM = 1024 + size_t(DA_STAGES) * DA_STAGE_BYTES +
-                           DA_CONSUMERS * (8 * 128 + 16) * sizeof(float) +
-                           DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * DA_STAGES * 8 + 64;
+constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;  // 32 rows x 128 B
+constexpr int DA_PROW = 40;                          // padded P^T row (bf16)
+
+template <int D>
+struct DaCfg {
+  static constexpr int NBOX = D / 64;                           // 128B boxes per row
+  static constexpr uint32_t STAGE_BYTES = 2 * NBOX * DA_BOX_BYTES;
+  static constexpr int CB = 8 * D + 16;                         // per-warp merge buffer (floats)
+  static constexpr size_t SMEM = 1024 + size_t(DA_STAGES) * STAGE_BYTES +
+                                 DA_CONSUMERS * CB * sizeof(float) +
+                                 DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * DA_STAGES * 8 + 64;
+};
 
 struct DecodeParams {
   const __nv_bfloat16* q;
@@ -51,18 +63,34 @@ struct DecodeParams {
   int tps;          // tiles per split
   int max_splits;
   float scale_log2;
-  float* ws_o;      // [B, Hq, max_splits, d]
+  float* ws_o;      // [B, Hq, max_splits, D]
   float* ws_ml;     // [B, Hq, max_splits, 2]
 };
 
+struct UnitId {
+  int b, kvh, s;
+};
+
+__device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
+  UnitId id;
+  id.s = u % p.max_splits;
+  const int bh = u / p.max_splits;
+  id.kvh = bh % p.Hkv;
+  id.b = bh / p.Hkv;
+  return id;
+}
+
+template <int D>
 __global__ void __launch_bounds__(DA_THREADS, 1)
     k_decode_attn(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const DecodeParams p) {
+  using C = DaCfg<D>;
+  constexpr int KK = D / 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
-  float* cbuf = reinterpret_cast<float*>(ring + DA_STAGES * DA_STAGE_BYTES);  // [4][8*128 + 16]
-  __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * (8 * 128 + 16));
+  float* cbuf = reinterpret_cast<float*>(ring + DA_STAGES * C::STAGE_BYTES);
+  __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * C::CB);
   uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + DA_CONSUMERS * 8 * DA_PROW);
   uint64_t* empty = full + DA_STAGES;
 
@@ -81,84 +109,131 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
 
   const int total = p.B * p.Hkv * p.max_splits;
   const int page_tiles = p.page / DA_TILE;
-  uint32_t gtile = 0;  // running tile counter across this CTA's units (ring position)
+
+  if (warp == DA_CONSUMERS) {
+    // ------------------------------------------------------------ producer
+    // Lane j holds the block id of page (window_first + j); the next unit's
+    // context length and first window are loaded one unit ahead.
+    uint32_t gtile = 0;
+    int u = blockIdx.x;
+    int ctx_cur = 0, blk_cur = 0;
+    if (u < total) {
+      const UnitId id = unit_of(p, u);
+      ctx_cur = p.ctx_lens[id.b];
+      const int pg = (id.s * p.tps) / page_tiles + lane;
+      blk_cur = pg < p.max_pages ? p.block_table[size_t(id.b) * p.max_pages + pg] : 0;
+    }
+    for (; u < total; u += gridDim.x) {
+      const UnitId id = unit_of(p, u);
+      const int un = u + gridDim.x;
+      int ctx_nxt = 0, blk_nxt = 0;
+      if (un < total) {  // prefetch: consumed only at the next iteration
+        const UnitId nid = unit_of(p, un);
+        ctx_nxt = p.ctx_lens[nid.b];
+        const int pg = (nid.s * p.tps) / page_tiles + lane;
+        blk_nxt = pg < p.max_pages ? p.block_table[size_t(nid.b) * p.max_pages + pg] : 0;
+      }
+      const int ntiles = (ctx_cur + DA_TILE - 1) / DA_TILE;
+      const int t0 = id.s * p.tps;
+      const int t1 = min(ntiles, t0 + p.tps);
+      if (t0 < t1) {
+        const int* bt = p.block_table + size_t(id.b) * p.max_pages;
+        int win_first = t0 / page_tiles;  // first page covered by blk_cur
+        int blk_win = blk_cur;
+        for (int t = t0; t < t1; ++t) {
+          const int pg = t / page_tiles;
+          if (pg >= win_first + 32) {  // slide the window (rare: > 32 pages per unit)
+            win_first += 32;
+            const int pj = win_first + lane;
+            blk_win = pj < p.max_pages ? bt[pj] : 0;
+          }
+          const int blk = __shfl_sync(0xffffffffu, blk_win, pg - win_first);
+          if (lane == 0) {
+            const uint32_t g = gtile + (t - t0);
+            const int st = g % DA_STAGES;
+            const uint32_t ph = (g / DA_STAGES) & 1;
+            const int row = (blk * p.Hkv + id.kvh) * p.page + (t % page_tiles) * DA_TILE;
+            mbar_wait(&empty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
+            uint8_t* sb = ring + st * C::STAGE_BYTES;
+#pragma unroll
+            for (int bx = 0; bx < C::NBOX; ++bx) {
+              tma_load_2d(sb + bx * DA_BOX_BYTES, &tmK, &full[st], bx * 64, row);
+              tma_load_2d(sb + (C::NBOX + bx) * DA_BOX_BYTES, &tmV, &full[st], bx * 64, row);
+            }
+          }
+          __syncwarp();
+        }
+        gtile += t1 - t0;
+      }
+      ctx_cur = ctx_nxt;
+      blk_cur = blk_nxt;
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int g8 = lane >> 2;  // MMA group id
+  const int t4 = lane & 3;   // thread in group
+  const int mat = lane >> 3;
+  __nv_bfloat16* pw = pbuf + warp * 8 * DA_PROW;
+  float* cw = cbuf + warp * C::CB;
+  uint32_t gtile = 0;
+
+  auto load_q = [&](int u, uint32_t (&qf)[KK][2], int& ctx) {
+    const UnitId id = unit_of(p, u);
+    ctx = p.ctx_lens[id.b];
+    const bool hv = g8 < p.G;
+    const __nv_bfloat16* qrow = p.q + size_t(id.b) * p.ldq + size_t(id.kvh * p.G + (hv ? g8 : 0)) * D;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      const uint32_t lo = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4);
+      const uint32_t hi = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4 + 8);
+      qf[kk][0] = hv ? lo : 0u;
+      qf[kk][1] = hv ? hi : 0u;
+    }
+  };
+
+  uint32_t qcur[KK][2];
+  int ctx_cur = 0;
+  if (blockIdx.x < total) load_q(blockIdx.x, qcur, ctx_cur);
 
   for (int u = blockIdx.x; u < total; u += gridDim.x) {
-    const int s = u % p.max_splits;
-    const int bh = u / p.max_splits;
-    const int kvh = bh % p.Hkv;
-    const int b = bh / p.Hkv;
-    const int ctx = p.ctx_lens[b];
+    const UnitId id = unit_of(p, u);
+    uint32_t qnxt[KK][2];
+    int ctx_nxt = 0;
+    if (u + int(gridDim.x) < total) load_q(u + gridDim.x, qnxt, ctx_nxt);
+    const int ctx = ctx_cur;
     const int ntiles = (ctx + DA_TILE - 1) / DA_TILE;
-    const int t0 = s * p.tps;
+    const int t0 = id.s * p.tps;
     const int t1 = min(ntiles, t0 + p.tps);
-    if (t0 >= t1) continue;  // empty split (uniform across the CTA)
-    const int nt = t1 - t0;
-
-    if (warp == DA_CONSUMERS) {
-      // ---------------------------------------------------------- producer
-      if (lane == 0) {
-        const int* bt = p.block_table + size_t(b) * p.max_pages;
-        for (int i = 0; i < nt; ++i) {
-          const uint32_t g = gtile + i;
-          const int st = g % DA_STAGES;
-          const uint32_t ph = (g / DA_STAGES) & 1;
-          const int t = t0 + i;
-          const int blk = bt[t / page_tiles];
-          const int row = (blk * p.Hkv + kvh) * p.page + (t % page_tiles) * DA_TILE;
-          mbar_wait(&empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&full[st], DA_STAGE_BYTES);
-          uint8_t* sb = ring + st * DA_STAGE_BYTES;
-          tma_load_2d(sb, &tmK, &full[st], 0, row);
-          tma_load_2d(sb + DA_BOX_BYTES, &tmK, &full[st], 64, row);
-          tma_load_2d(sb + 2 * DA_BOX_BYTES, &tmV, &full[st], 0, row);
-          tma_load_2d(sb + 3 * DA_BOX_BYTES, &tmV, &full[st], 64, row);
-        }
-      }
-    } else {
-      // ---------------------------------------------------------- consumers
-      const int g8 = lane >> 2;  // MMA group id
-      const int t4 = lane & 3;   // thread in group
-      // Q^T fragments (B operand): n = head g8 of this kv group, k = d
-      uint32_t qf[8][2];
-      {
-        const bool hv = g8 < p.G;
-        const __nv_bfloat16* qrow = p.q + size_t(b) * p.ldq + size_t(kvh * p.G + (hv ? g8 : 0)) * DA_D;
+    if (t0 < t1) {
+      const int nt = t1 - t0;
+      float o[KK][4];
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          uint32_t lo = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4);
-          uint32_t hi = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4 + 8);
-          qf[kk][0] = hv ? lo : 0u;
-          qf[kk][1] = hv ? hi : 0u;
-        }
-      }
-      float o[8][4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      for (int i = 0; i < KK; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
       float m0 = -INFINITY, m1 = -INFINITY;  // running max for heads 2t4, 2t4+1
       float l0 = 0.f, l1 = 0.f;              // per-lane partial sums
-      __nv_bfloat16* pw = pbuf + warp * 8 * DA_PROW;
 
       for (int i = warp; i < nt; i += DA_CONSUMERS) {
         const uint32_t g = gtile + i;
         const int st = g % DA_STAGES;
         const uint32_t ph = (g / DA_STAGES) & 1;
         mbar_wait(&full[st], ph);
-        const uint32_t kb = smem_u32(ring + st * DA_STAGE_BYTES);
-        const uint32_t vb = kb + 2 * DA_BOX_BYTES;
+        const uint32_t kb = smem_u32(ring + st * C::STAGE_BYTES);
+        const uint32_t vb = kb + C::NBOX * DA_BOX_BYTES;
         // ---- S^T = K . Q^T  (two 16-token m tiles)
         float sc[2][4];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const int mat = lane >> 3;
+          for (int kk = 0; kk < KK; ++kk) {
             const uint32_t r = mt * 16 + (mat & 1) * 8 + (lane & 7);
             const uint32_t c = (kk & 3) * 2 + (mat >> 1);
             uint32_t a[4];
             ldmatrix_x4(kb + (kk >> 2) * DA_BOX_BYTES + sw128(r, c), a[0], a[1], a[2], a[3]);
-            mma_bf16_16816(sc[mt], a, qf[kk]);
+            mma_bf16_16816(sc[mt], a, qcur[kk]);
           }
         }
         // ---- mask, scale, online softmax
@@ -168,8 +243,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int tok = tokbase + mt * 16 + g8 + h * 8;
-            const bool valid = tok < ctx;
+            const bool valid = tokbase + mt * 16 + g8 + h * 8 < ctx;
             sc[mt][2 * h] = valid ? sc[mt][2 * h] * p.scale_log2 : -INFINITY;
             sc[mt][2 * h + 1] = valid ? sc[mt][2 * h + 1] * p.scale_log2 : -INFINITY;
             tm0 = fmaxf(tm0, sc[mt][2 * h]);
@@ -188,7 +262,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         l0 *= a0;
         l1 *= a1;
 #pragma unroll
-        for (int dm = 0; dm < 8; ++dm) {
+        for (int dm = 0; dm < KK; ++dm) {
           o[dm][0] *= a0;
           o[dm][2] *= a0;
           o[dm][1] *= a1;
@@ -216,10 +290,9 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
           pf[kt][1] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4 + 8);
         }
 #pragma unroll
-        for (int dm = 0; dm < 8; ++dm) {
+        for (int dm = 0; dm < KK; ++dm) {
 #pragma unroll
           for (int kt = 0; kt < 2; ++kt) {
-            const int mat = lane >> 3;
             const uint32_t r = kt * 16 + (mat >> 1) * 8 + (lane & 7);
             const uint32_t c = (dm & 3) * 2 + (mat & 1);
             uint32_t a[4];
@@ -236,62 +309,68 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         l0 += __shfl_xor_sync(0xffffffffu, l0, off);
         l1 += __shfl_xor_sync(0xffffffffu, l1, off);
       }
-      float* cw = cbuf + warp * (8 * 128 + 16);
 #pragma unroll
-      for (int dm = 0; dm < 8; ++dm) {
-        cw[(2 * t4) * 128 + dm * 16 + g8] = o[dm][0];
-        cw[(2 * t4 + 1) * 128 + dm * 16 + g8] = o[dm][1];
-        cw[(2 * t4) * 128 + dm * 16 + g8 + 8] = o[dm][2];
-        cw[(2 * t4 + 1) * 128 + dm * 16 + g8 + 8] = o[dm][3];
+      for (int dm = 0; dm < KK; ++dm) {
+        cw[(2 * t4) * D + dm * 16 + g8] = o[dm][0];
+        cw[(2 * t4 + 1) * D + dm * 16 + g8] = o[dm][1];
+        cw[(2 * t4) * D + dm * 16 + g8 + 8] = o[dm][2];
+        cw[(2 * t4 + 1) * D + dm * 16 + g8 + 8] = o[dm][3];
       }
       if (g8 == 0) {
-        cw[8 * 128 + 2 * t4] = m0;
-        cw[8 * 128 + 2 * t4 + 1] = m1;
-        cw[8 * 128 + 8 + 2 * t4] = l0;
-        cw[8 * 128 + 8 + 2 * t4 + 1] = l1;
+        cw[8 * D + 2 * t4] = m0;
+        cw[8 * D + 2 * t4 + 1] = m1;
+        cw[8 * D + 8 + 2 * t4] = l0;
+        cw[8 * D + 8 + 2 * t4 + 1] = l1;
       }
       named_bar_sync(1, DA_CONSUMERS * 32);
       const int nsplit = (ntiles + p.tps - 1) / p.tps;
-      for (int e = threadIdx.x; e < p.G * 32; e += DA_CONSUMERS * 32) {
-        const int h = e >> 5;
-        const int d4 = (e & 31) * 4;
+      constexpr int Q4 = D / 4;  // float4 groups per head row
+      for (int e = threadIdx.x; e < p.G * Q4; e += DA_CONSUMERS * 32) {
+        const int h = e / Q4;
+        const int d4 = (e % Q4) * 4;
         float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < DA_CONSUMERS; ++w) M = fmaxf(M, cbuf[w * (8 * 128 + 16) + 8 * 128 + h]);
+        for (int w = 0; w < DA_CONSUMERS; ++w) M = fmaxf(M, cbuf[w * C::CB + 8 * D + h]);
         float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int w = 0; w < DA_CONSUMERS; ++w) {
-          const float* c = cbuf + w * (8 * 128 + 16);
-          const float mw = c[8 * 128 + h];
+          const float* c = cbuf + w * C::CB;
+          const float mw = c[8 * D + h];
           const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-          L += f * c[8 * 128 + 8 + h];
+          L += f * c[8 * D + 8 + h];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] += f * c[h * 128 + d4 + j];
+          for (int j = 0; j < 4; ++j) acc[j] += f * c[h * D + d4 + j];
         }
-        const int head = kvh * p.G + h;
+        const int head = id.kvh * p.G + h;
         if (nsplit == 1) {
           const float inv = 1.f / L;
           uint2 w;
           w.x = pack_bf16(acc[0] * inv, acc[1] * inv);
           w.y = pack_bf16(acc[2] * inv, acc[3] * inv);
-          *reinterpret_cast<uint2*>(p.out + size_t(b) * p.ldo + size_t(head) * DA_D + d4) = w;
+          *reinterpret_cast<uint2*>(p.out + size_t(id.b) * p.ldo + size_t(head) * D + d4) = w;
         } else {
-          const size_t slot = (size_t(b) * p.Hq + head) * p.max_splits + s;
-          float4 w = make_float4(acc[0], acc[1], acc[2], acc[3]);
-          *reinterpret_cast<float4*>(p.ws_o + slot * DA_D + d4) = w;
-          if ((e & 31) == 0) {
+          const size_t slot = (size_t(id.b) * p.Hq + head) * p.max_splits + id.s;
+          *reinterpret_cast<float4*>(p.ws_o + slot * D + d4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          if (e % Q4 == 0) {
             p.ws_ml[slot * 2] = M;
             p.ws_ml[slot * 2 + 1] = L;
           }
         }
       }
       named_bar_sync(1, DA_CONSUMERS * 32);
+      gtile += nt;
     }
-    gtile += nt;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      qcur[kk][0] = qnxt[kk][0];
+      qcur[kk][1] = qnxt[kk][1];
+    }
+    ctx_cur = ctx_nxt;
   }
 }
 
 // One warp per (sequence, head): log-sum-exp merge of the split partials.
+template <int D>
 __global__ void k_decode_combine(const DecodeParams p) {
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -304,21 +383,42 @@ __global__ void k_decode_combine(const DecodeParams p) {
   const size_t base = (size_t(b) * p.Hq + head) * p.max_splits;
   float M = -INFINITY;
   for (int s = 0; s < nsplit; ++s) M = fmaxf(M, p.ws_ml[(base + s) * 2]);
-  float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  constexpr int PER = D / 32;  // dims per lane (2 or 4)
+  float L = 0.f, acc[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) acc[j] = 0.f;
   for (int s = 0; s < nsplit; ++s) {
     const float f = exp2f(p.ws_ml[(base + s) * 2] - M);
     L += f * p.ws_ml[(base + s) * 2 + 1];
-    const float4 v = *reinterpret_cast<const float4*>(p.ws_o + (base + s) * DA_D + lane * 4);
-    acc[0] += f * v.x;
-    acc[1] += f * v.y;
-    acc[2] += f * v.z;
-    acc[3] += f * v.w;
+    const float* src = p.ws_o + (base + s) * D + lane * PER;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) acc[j] += f * src[j];
   }
   const float inv = 1.f / L;
-  uint2 w;
-  w.x = pack_bf16(acc[0] * inv, acc[1] * inv);
-  w.y = pack_bf16(acc[2] * inv, acc[3] * inv);
-  *reinterpret_cast<uint2*>(p.out + size_t(b) * p.ldo + size_t(head) * DA_D + lane * 4) = w;
+  __nv_bfloat16* dst = p.out + size_t(b) * p.ldo + size_t(head) * D + lane * PER;
+#pragma unroll
+  for (int j = 0; j < PER; j += 2)
+    *reinterpret_cast<uint32_t*>(dst + j) = pack_bf16(acc[j] * inv, acc[j + 1] * inv);
+}
+
+template <int D>
+static int launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const DecodeParams& p,
+                         int max_ctas, cudaStream_t st) {
+  using C = DaCfg<D>;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    attr = true;
+  }
+  const int units = p.B * p.Hkv * p.max_splits;
+  k_decode_attn<D><<<std::min(units, max_ctas), DA_THREADS, C::SMEM, st>>>(tk, tv, p);
+  HP_LAUNCH_CHECK("k_decode_attn");
+  if (p.max_splits > 1) {
+    const int warps = p.B * p.Hq;
+    k_decode_combine<D><<<(warps + 7) / 8, 256, 0, st>>>(p);
+    HP_LAUNCH_CHECK("k_decode_combine");
+  }
+  return HP_OK;
 }
 
 }  // namespace hp
@@ -335,7 +435,7 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
                               float scale, void* workspace, size_t ws_bytes, int max_ctas,
                               void* stream) {
   HP_CHECK_ARG(q && kcache && vcache && block_table && ctx_lens && out, "hp_decode_attn: null pointer");
-  HP_CHECK_ARG(d == DA_D, "hp_decode_attn: head_dim must be 128");
+  HP_CHECK_ARG(d == 64 || d == 128, "hp_decode_attn: head_dim must be 64 or 128");
   HP_CHECK_ARG(page % DA_TILE == 0 && page >= DA_TILE, "hp_decode_attn: page must be a multiple of 32");
   HP_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0 && Hq / Hkv <= 8, "hp_decode_attn: GQA group must be <= 8");
   HP_CHECK_ARG(B >= 1 && max_pages >= 1 && num_blocks >= 1, "hp_decode_attn: empty batch/cache");
@@ -366,9 +466,12 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
     HP_CHECK_ARG(workspace != nullptr, "hp_decode_attn: workspace required for split contexts");
     if (ws_bytes < hp_decode_attn_ws_bytes(B, Hq, d, p.max_splits)) {
       // not enough scratch for this split: fall back to fewer, longer splits
-      int ms = int(ws_bytes / (size_t(B) * Hq * (d + 2) * sizeof(float)));
-      HP_CHECK_ARG(ms >= 1, "hp_decode_attn: workspace too small");
-      p.tps = (max_tiles + ms - 1) / ms;
+      const int ms = int(ws_bytes / (size_t(B) * Hq * (d + 2) * sizeof(float)));
+      if (ms <= 1) {
+        p.tps = max_tiles;
+      } else {
+        p.tps = (max_tiles + ms - 1) / ms;
+      }
       p.max_splits = (max_tiles + p.tps - 1) / p.tps;
     }
     p.ws_o = static_cast<float*>(workspace);
@@ -380,19 +483,6 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   if (rc) return rc;
   rc = cached_tmap_bf16(&tv, vcache, rows, d, d, DA_TILE, 64, true);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_decode_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DA_SMEM)));
-    attr = true;
-  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int units = B * Hkv * p.max_splits;
-  k_decode_attn<<<std::min(units, max_ctas), DA_THREADS, DA_SMEM, st>>>(tk, tv, p);
-  HP_LAUNCH_CHECK("k_decode_attn");
-  if (p.max_splits > 1) {
-    const int warps = B * Hq;
-    k_decode_combine<<<(warps + 7) / 8, 256, 0, st>>>(p);
-    HP_LAUNCH_CHECK("k_decode_combine");
-  }
-  return HP_OK;
+  return d == 128 ? launch_decode<128>(tk, tv, p, max_ctas, st) : launch_decode<64>(tk, tv, p, max_ctas, st);
 }

@@ -1,0 +1,396 @@
+// Decode-side GEMMs (reference kernel groups qkv / o_proj / mlp_up_gate /
+// mlp_down at phase "decode", workload.py:153-210): Y[T, N] = epi(X . W^T)
+// with T <= 256 tokens.  The work is a pure weight stream (AI ~ 31), so the
+// kernel is built to keep HBM busy from any partition size:
+//
+//   * swap-AB: W [N, K] is the UMMA A operand (M = 128 output features per
+//     tile), X [T, K] the B operand (UMMA N = BN >= T), accumulator in TMEM;
+//   * stream-K: the (tile, k-block) iteration space is cut into equal
+//     contiguous ranges, one per CTA of the persistent grid, so every SM
+//     streams the same number of weight bytes regardless of how many output
+//     tiles exist (no wave quantization on the decode partition);
+//   * tiles split across CTAs leave fp32 partials in a workspace; the last
+//     contributor (arrival counter, self-resetting) sums them and runs the
+//     epilogue.  Tiles owned by one CTA go straight from TMEM to the output.
+//
+// Epilogues: STORE, RESID (+R), SILU (W rows interleaved in 64-row gate/up
+// blocks, so a 128-row tile yields 64 outputs).  Outputs are written through
+// a padded shared-memory transpose so stores along the feature dim coalesce.
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM alloc + UMMA
+// issuer, warps 2..5 epilogue (TMEM lane quarter = warp % 4).
+#include "common.cuh"
+#include "runtime.h"
+#include "../../include/hp.h"
+
+#include <algorithm>
+
+namespace hp {
+
+namespace {
+
+constexpr int SBM = 128;
+constexpr int SBK = 64;
+constexpr int VLD = 33;  // padded fp32 row of the epilogue transpose buffer
+
+template <int BN>
+struct SwapCfg {
+  static constexpr uint32_t A_BYTES = SBM * SBK * 2;
+  static constexpr uint32_t B_BYTES = BN * SBK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : (BN >= 64 ? 8 : 10));
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
+  static constexpr size_t VBUF = size_t(SBM) * VLD * 4;
+  static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + VBUF + 256;
+};
+
+struct SwapParams {
+  int N, T, K;
+  int m_tiles, n_tiles, num_kb;
+  int ipc;          // k-block iterations per CTA
+  int total_iters;  // m_tiles * n_tiles * num_kb
+  int max_contrib;
+  __nv_bfloat16* out;
+  int ldo;
+  const __nv_bfloat16* resid;
+  int ldr;
+  float* ws;        // [tiles][max_contrib][128][BN]
+  int* counters;    // [tiles], zero on entry and exit
+  int epi;
+};
+
+struct Seg {
+  int tile, kb0, kb1;
+};
+
+__device__ __forceinline__ bool next_seg(const SwapParams& p, int& it, int end, Seg& s) {
+  if (it >= end) return false;
+  s.tile = it / p.num_kb;
+  s.kb0 = it - s.tile * p.num_kb;
+  s.kb1 = min(p.num_kb, s.kb0 + (end - it));
+  it += s.kb1 - s.kb0;
+  return true;
+}
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+// Epilogue-warp barrier (128 threads, named barrier 1).
+__device__ __forceinline__ void epi_sync() { named_bar_sync(1, 128); }
+
+// Write a 128 x 32 fp32 chunk held in smem V (row = feature, col = token
+// offset c0..c0+31) to the output.  et: 0..127 epilogue thread index.
+template <int BN>
+__device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, int mt, int nt,
+                                           int c0, int et) {
+  const int lane = et & 31, w = et >> 5;
+  if (p.epi == HP_EPI_SILU) {
+    // 64 outputs per tile: feature r (gate) pairs with r + 64 (up)
+    for (int j = w; j < 32; j += 4) {
+      const int t = nt * BN + c0 + j;
+      if (t >= p.T) break;
+      const int r = 2 * lane;
+      const float g0 = V[r * VLD + j], g1 = V[(r + 1) * VLD + j];
+      const float u0 = V[(r + 64) * VLD + j], u1 = V[(r + 65) * VLD + j];
+      *reinterpret_cast<uint32_t*>(p.out + size_t(t) * p.ldo + mt * 64 + r) =
+          pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+    }
+  } else {
+    for (int j = w; j < 32; j += 4) {
+      const int t = nt * BN + c0 + j;
+      if (t >= p.T) break;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = h * 64 + 2 * lane;
+        float v0 = V[r * VLD + j], v1 = V[(r + 1) * VLD + j];
+        const int o = mt * SBM + r;
+        if (p.epi == HP_EPI_RESID) {
+          const uint32_t rr = *reinterpret_cast<const uint32_t*>(p.resid + size_t(t) * p.ldr + o);
+          v0 += bf16lo(rr);
+          v1 += bf16hi(rr);
+        }
+        *reinterpret_cast<uint32_t*>(p.out + size_t(t) * p.ldo + o) = pack_bf16(v0, v1);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_swap_sk(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                   const SwapParams p) {
+  using C = SwapCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  float* V = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(V) + C::VBUF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int begin = blockIdx.x * p.ipc;
+  const int end = min(begin + p.ipc, p.total_iters);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t w_policy = l2_policy_evict_first();  // weights: read once per step
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = begin;
+      Seg s;
+      while (next_seg(p, it, end, s)) {
+        const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
+        for (int kb = s.kb0; kb < s.kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d_hint(sA + stage * C::A_BYTES, &tmW, &full[stage], kb * SBK, mt * SBM, w_policy);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(SBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int it = begin;
+      Seg s;
+      while (next_seg(p, it, end, s)) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = s.kb0; kb < s.kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < SBK / 16; ++k)
+            umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                      (kb > s.kb0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int et = (warp - 2) * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = begin;
+    Seg s;
+    while (next_seg(p, it, end, s)) {
+      const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
+      const int first = (s.tile * p.num_kb) / p.ipc;
+      const int last = ((s.tile + 1) * p.num_kb - 1) / p.ipc;
+      const bool single = first == last;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      if (single) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_ld_wait();
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          epi_sync();  // previous chunk's readers are done with V
+#pragma unroll
+          for (int j = 0; j < 32; ++j) V[row * VLD + j] = v[j];
+          epi_sync();
+          emit_chunk<BN>(p, V, mt, nt, c * 32, et);
+        }
+      } else {
+        float* mine = p.ws + (size_t(s.tile) * p.max_contrib + (blockIdx.x - first)) * (SBM * BN) +
+                      size_t(row) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(mine + c * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        epi_sync();
+        if (et == 0) {
+          const int prev = atomicAdd(p.counters + s.tile, 1);
+          *last_flag = (prev == last - first) ? 1 : 0;
+        }
+        epi_sync();
+        if (*last_flag) {
+          __threadfence();
+          const int ncontrib = last - first + 1;
+          const float* base = p.ws + size_t(s.tile) * p.max_contrib * (SBM * BN);
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            // 128 rows x 32 cols chunk: 1024 float4, 8 per thread
+            float4 a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < ncontrib; ++k) {
+              const float* src = base + size_t(k) * (SBM * BN);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int f = i * 128 + et;          // float4 index within the chunk
+                const int r = f >> 3, cc = (f & 7) * 4;
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(src + size_t(r) * BN + c * 32 + cc));
+                a[i].x += x.x; a[i].y += x.y; a[i].z += x.z; a[i].w += x.w;
+              }
+            }
+            epi_sync();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int f = i * 128 + et;
+              const int r = f >> 3, cc = (f & 7) * 4;
+              V[r * VLD + cc] = a[i].x;
+              V[r * VLD + cc + 1] = a[i].y;
+              V[r * VLD + cc + 2] = a[i].z;
+              V[r * VLD + cc + 3] = a[i].w;
+            }
+            epi_sync();
+            emit_chunk<BN>(p, V, mt, nt, c * 32, et);
+          }
+          if (et == 0) p.counters[s.tile] = 0;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN>
+static int launch_swap(const CUtensorMap& tw, const CUtensorMap& tx, const SwapParams& p, int grid,
+                       cudaStream_t st) {
+  using C = SwapCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_swap_sk<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    attr_set = true;
+  }
+  k_gemm_swap_sk<BN><<<grid, 192, C::SMEM, st>>>(tw, tx, p);
+  HP_LAUNCH_CHECK("k_gemm_swap_sk");
+  return HP_OK;
+}
+
+static inline int swap_bn(int T) { return T <= 32 ? 32 : (T <= 64 ? 64 : (T <= 128 ? 128 : 256)); }
+
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" size_t hp_gemm_swap_ws_bytes(int T, int N, int K, int max_ctas) {
+  const int BN = swap_bn(T);
+  const int tiles = (N / SBM) * ((T + BN - 1) / BN);
+  const int num_kb = K / SBK;
+  const int total = tiles * num_kb;
+  const int grid = std::max(1, std::min(max_ctas, total));
+  const int ipc = (total + grid - 1) / grid;
+  const int max_contrib = (num_kb + ipc - 1) / ipc + 1;
+  return size_t(tiles) * max_contrib * SBM * BN * sizeof(float);
+}
+
+extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
+                            const void* R, int ldr, int T, int N, int K, int epilogue,
+                            void* workspace, size_t ws_bytes, int* counters, int n_counters,
+                            int max_ctas, void* stream) {
+  HP_CHECK_ARG(X && W && Y, "hp_gemm_swap: null pointer");
+  HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
+  HP_CHECK_ARG(N % SBM == 0, "hp_gemm_swap: N must be a multiple of 128");
+  HP_CHECK_ARG(K % SBK == 0, "hp_gemm_swap: K must be a multiple of 64");
+  HP_CHECK_ARG(epilogue >= HP_EPI_STORE && epilogue <= HP_EPI_SILU, "hp_gemm_swap: bad epilogue");
+  HP_CHECK_ARG(epilogue != HP_EPI_RESID || R != nullptr, "hp_gemm_swap: residual epilogue needs R");
+  HP_CHECK_ARG(max_ctas >= 1, "hp_gemm_swap: max_ctas must be >= 1");
+  HP_CHECK_ARG(ldy % 2 == 0 && (R == nullptr || ldr % 2 == 0), "hp_gemm_swap: odd output pitch");
+  const int BN = swap_bn(T);
+  SwapParams p{};
+  p.N = N;
+  p.T = T;
+  p.K = K;
+  p.m_tiles = N / SBM;
+  p.n_tiles = (T + BN - 1) / BN;
+  p.num_kb = K / SBK;
+  p.total_iters = p.m_tiles * p.n_tiles * p.num_kb;
+  const int grid = std::min(max_ctas, p.total_iters);
+  p.ipc = (p.total_iters + grid - 1) / grid;
+  p.max_contrib = (p.num_kb + p.ipc - 1) / p.ipc + 1;
+  p.out = static_cast<__nv_bfloat16*>(Y);
+  p.ldo = ldy;
+  p.resid = static_cast<const __nv_bfloat16*>(R);
+  p.ldr = ldr;
+  p.ws = static_cast<float*>(workspace);
+  p.counters = counters;
+  p.epi = epilogue;
+  const bool any_split = p.ipc % p.num_kb != 0 || p.ipc < p.num_kb;
+  if (any_split) {
+    HP_CHECK_ARG(workspace && counters, "hp_gemm_swap: split tiles need workspace and counters");
+    HP_CHECK_ARG(ws_bytes >= hp_gemm_swap_ws_bytes(T, N, K, max_ctas), "hp_gemm_swap: workspace too small");
+    HP_CHECK_ARG(n_counters >= p.m_tiles * p.n_tiles, "hp_gemm_swap: too few counters");
+  }
+  CUtensorMap tw, tx;
+  int rc = cached_tmap_bf16(&tw, W, N, K, ldw, SBM, SBK, true);
+  if (rc) return rc;
+  rc = cached_tmap_bf16(&tx, X, T, K, ldx, BN, SBK, true);
+  if (rc) return rc;
+  const int g = (p.total_iters + p.ipc - 1) / p.ipc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (BN) {
+    case 32: return launch_swap<32>(tw, tx, p, g, st);
+    case 64: return launch_swap<64>(tw, tx, p, g, st);
+    case 128: return launch_swap<128>(tw, tx, p, g, st);
+    default: return launch_swap<256>(tw, tx, p, g, st);
+  }
+}

@@ -3,14 +3,10 @@
 //   D = A . B^T  with A [Ma, K] and B [Nb, K] bf16, both K-major (torch
 //   [out, in] weight layout), fp32 accumulation in TMEM.
 //
-// Two operand placements share one kernel body:
-//   * prefill ("token-major"): A = activations X [T, K], B = weights W [N, K];
-//     D tile = 128 tokens x BN features, epilogue writes Y [T, N] directly.
-//   * decode ("swap-AB"): A = W [N, K], B = X [T<=256, K]; D tile = 128
-//     features x BN tokens.  The token count is tiny, so the weight stream is
-//     split along K across CTAs; partial tiles are reduced with vector
-//     red.global.add into an fp32 workspace and the last-arriving CTA of a
-//     tile runs the epilogue (counter-based, self-cleaning).
+// Token-major operand placement for prefill: A = activations X [T, K],
+// B = weights W [N, K]; D tile = 128 tokens x BN features, and the epilogue
+// writes Y [T, N] rows directly from TMEM.  (Decode's skinny GEMMs use the
+// swap-AB stream-K kernel in gemm_swap.cu.)
 //
 // Epilogues (reference kernel groups, workload.py:164-209):
 //   STORE  : Y = D                               (qkv projection)
@@ -41,9 +37,6 @@ struct GemmParams {
   int ldo;
   const __nv_bfloat16* resid;
   int ldr;
-  float* ws;      // swap mode: [Ma, ws_ld] fp32, zero on entry and exit
-  int ws_ld;
-  int* counters;  // swap mode: [m_tiles * n_tiles], zero on entry and exit
   int epi;
 };
 
@@ -86,13 +79,7 @@ __device__ __forceinline__ void add_row32(float* v, const __nv_bfloat16* src) {
   }
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
-               "f"(c), "f"(d)
-               : "memory");
-}
-
-template <int BN, bool SWAP>
+template <int BN>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const GemmParams p) {
@@ -107,7 +94,6 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -190,7 +176,6 @@ __global__ void __launch_bounds__(192, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;       // accumulator row owned by this thread
-    const int et = (warp - 2) * 32 + lane;  // 0..127 epilogue thread index
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
@@ -199,7 +184,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      if constexpr (!SWAP) {
+      {
         const int gm = mt * BM + row;
         const bool ok = gm < p.Ma;
         if (p.epi == EPI_SILU) {
@@ -232,58 +217,6 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-      } else {
-        // partial tile (features x tokens) -> fp32 workspace
-        float* wrow = p.ws + size_t(mt * BM + row) * p.ws_ld + nt * BN;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(taddr + c * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) red_add_v4(wrow + c * 32 + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (et == 0) {
-          const int prev = atomicAdd(p.counters + tile, 1);
-          *last_flag = (prev == p.k_splits - 1) ? 1 : 0;
-        }
-        named_bar_sync(1, 128);
-        if (*last_flag) {
-          __threadfence();
-          const int T = p.Nb;
-          if (p.epi == EPI_SILU) {
-            const int r = et & 63;
-            const int half = et >> 6;
-            float* gw = p.ws + size_t(mt * BM + r) * p.ws_ld + nt * BN;
-            float* uw = gw + size_t(64) * p.ws_ld;
-            const int o = mt * 64 + r;
-            for (int j = half; j < BN; j += 2) {
-              const int t = nt * BN + j;
-              const float gv = __ldcg(gw + j), uv = __ldcg(uw + j);
-              __stcg(gw + j, 0.f);
-              __stcg(uw + j, 0.f);
-              if (t < T) p.out[size_t(t) * p.ldo + o] = __float2bfloat16(silu(gv) * uv);
-            }
-          } else {
-            const int o = mt * BM + et;
-            float* w = p.ws + size_t(o) * p.ws_ld + nt * BN;
-            for (int j = 0; j < BN; ++j) {
-              const int t = nt * BN + j;
-              float v = __ldcg(w + j);
-              __stcg(w + j, 0.f);
-              if (t < T) {
-                if (p.epi == EPI_RESID) v += __bfloat162float(p.resid[size_t(t) * p.ldr + o]);
-                p.out[size_t(t) * p.ldo + o] = __float2bfloat16(v);
-              }
-            }
-          }
-          if (et == 0) p.counters[tile] = 0;
-        }
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -297,17 +230,17 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <int BN, bool SWAP>
+template <int BN>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
                   cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tc<BN, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(C::SMEM)));
     attr_set = true;
   }
-  k_gemm_tc<BN, SWAP><<<grid, 192, C::SMEM, st>>>(ta, tb, p);
+  k_gemm_tc<BN><<<grid, 192, C::SMEM, st>>>(ta, tb, p);
   HP_LAUNCH_CHECK("k_gemm_tc");
   return HP_OK;
 }
@@ -352,64 +285,6 @@ extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, 
   const int units = p.m_tiles * p.n_tiles;
   const int grid = std::min(units, max_ctas);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return BN == 256 ? launch<256, false>(ta, tb, p, grid, st) : launch<128, false>(ta, tb, p, grid, st);
+  return BN == 256 ? launch<256>(ta, tb, p, grid, st) : launch<128>(ta, tb, p, grid, st);
 }
 
-extern "C" int hp_gemm_swap_splits(int T, int N, int K, int max_ctas) {
-  const int m_tiles = N / BM;
-  const int BN = T <= 32 ? 32 : (T <= 64 ? 64 : (T <= 128 ? 128 : 256));
-  const int tiles = m_tiles * ceil_div(T, BN);
-  const int num_kb = K / BK;
-  int ks = ceil_div(2 * max_ctas, tiles);
-  ks = std::max(1, std::min(ks, std::max(1, num_kb / 4)));
-  return ks;
-}
-
-extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
-                            const void* R, int ldr, int T, int N, int K, int epilogue,
-                            void* workspace, size_t ws_bytes, int* counters, int n_counters,
-                            int k_splits, int max_ctas, void* stream) {
-  HP_CHECK_ARG(X && W && Y && workspace && counters, "hp_gemm_swap: null pointer");
-  HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
-  HP_CHECK_ARG(N % BM == 0, "hp_gemm_swap: N must be a multiple of 128");
-  HP_CHECK_ARG(K % BK == 0, "hp_gemm_swap: K must be a multiple of 64");
-  HP_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SILU, "hp_gemm_swap: bad epilogue");
-  HP_CHECK_ARG(epilogue != EPI_RESID || R != nullptr, "hp_gemm_swap: residual epilogue needs R");
-  HP_CHECK_ARG(max_ctas >= 1, "hp_gemm_swap: max_ctas must be >= 1");
-  const int BN = T <= 32 ? 32 : (T <= 64 ? 64 : (T <= 128 ? 128 : 256));
-  GemmParams p{};
-  p.Ma = N;
-  p.Nb = T;
-  p.K = K;
-  p.m_tiles = N / BM;
-  p.n_tiles = ceil_div(T, BN);
-  p.num_kb = K / BK;
-  if (k_splits <= 0) k_splits = hp_gemm_swap_splits(T, N, K, max_ctas);
-  k_splits = std::min(k_splits, p.num_kb);
-  p.kb_per_split = ceil_div(p.num_kb, k_splits);
-  p.k_splits = ceil_div(p.num_kb, p.kb_per_split);
-  p.out = static_cast<__nv_bfloat16*>(Y);
-  p.ldo = ldy;
-  p.resid = static_cast<const __nv_bfloat16*>(R);
-  p.ldr = ldr;
-  p.ws = static_cast<float*>(workspace);
-  p.ws_ld = p.n_tiles * BN;
-  p.counters = counters;
-  p.epi = epilogue;
-  HP_CHECK_ARG(ws_bytes >= size_t(N) * p.ws_ld * sizeof(float), "hp_gemm_swap: workspace too small");
-  HP_CHECK_ARG(n_counters >= p.m_tiles * p.n_tiles, "hp_gemm_swap: too few counters");
-  CUtensorMap ta, tb;
-  int rc = cached_tmap_bf16(&ta, W, N, K, ldw, BM, BK, true);
-  if (rc) return rc;
-  rc = cached_tmap_bf16(&tb, X, T, K, ldx, BN, BK, true);
-  if (rc) return rc;
-  const int units = p.m_tiles * p.n_tiles * p.k_splits;
-  const int grid = std::min(units, max_ctas);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  switch (BN) {
-    case 32: return launch<32, true>(ta, tb, p, grid, st);
-    case 64: return launch<64, true>(ta, tb, p, grid, st);
-    case 128: return launch<128, true>(ta, tb, p, grid, st);
-    default: return launch<256, true>(ta, tb, p, grid, st);
-  }
-}

@@ -20,16 +20,20 @@
 
 namespace hp {
 
-constexpr int PA_D = 128;
 constexpr int PA_BQ = 64;
 constexpr int PA_BK = 64;
 constexpr int PA_STAGES = 2;
 constexpr int PA_CONSUMERS = 4;
 constexpr int PA_THREADS = (PA_CONSUMERS + 1) * 32;
-constexpr uint32_t PA_BOX = 64 * 64 * 2;                 // 64 rows x 128 B
-constexpr uint32_t PA_TILE_BYTES = 2 * PA_BOX;           // 64 rows x 128 d
-constexpr uint32_t PA_STAGE_BYTES = 2 * PA_TILE_BYTES;   // K + V
-constexpr size_t PA_SMEM = 1024 + PA_TILE_BYTES + PA_STAGES * PA_STAGE_BYTES + 128;
+constexpr uint32_t PA_BOX = 64 * 64 * 2;                 // 64 rows x 128 B (64 dims)
+
+template <int D>
+struct PaCfg {
+  static constexpr int NBOX = D / 64;
+  static constexpr uint32_t TILE_BYTES = NBOX * PA_BOX;  // 64 rows x D
+  static constexpr uint32_t STAGE_BYTES = 2 * TILE_BYTES;  // K + V
+  static constexpr size_t SMEM = 1024 + TILE_BYTES + PA_STAGES * STAGE_BYTES + 128;
+};
 
 struct PrefillParams {
   const int* cu_seqlens;
@@ -39,9 +43,14 @@ struct PrefillParams {
   float scale_log2;
 };
 
+template <int D>
 __global__ void __launch_bounds__(PA_THREADS, 1)
     k_prefill_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const PrefillParams p) {
+  using C = PaCfg<D>;
+  constexpr int KK = D / 16;
+  constexpr uint32_t PA_TILE_BYTES = C::TILE_BYTES;
+  constexpr uint32_t PA_STAGE_BYTES = C::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -87,8 +96,9 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       if (lane == 0) {
         mbar_wait(qempty, qphase ^ 1);
         mbar_arrive_expect_tx(qfull, PA_TILE_BYTES);
-        tma_load_2d(sQ, &tmQ, qfull, head * PA_D, s0 + q0);
-        tma_load_2d(sQ + PA_BOX, &tmQ, qfull, head * PA_D + 64, s0 + q0);
+#pragma unroll
+        for (int bx = 0; bx < C::NBOX; ++bx)
+          tma_load_2d(sQ + bx * PA_BOX, &tmQ, qfull, head * D + bx * 64, s0 + q0);
         for (int j = 0; j < nkv; ++j) {
           const uint32_t g = gtile + j;
           const int st = g % PA_STAGES;
@@ -97,10 +107,11 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
           mbar_arrive_expect_tx(&full[st], PA_STAGE_BYTES);
           uint8_t* sb = ring + st * PA_STAGE_BYTES;
           const int row = s0 + j * PA_BK;
-          tma_load_2d(sb, &tmK, &full[st], kvh * PA_D, row);
-          tma_load_2d(sb + PA_BOX, &tmK, &full[st], kvh * PA_D + 64, row);
-          tma_load_2d(sb + PA_TILE_BYTES, &tmV, &full[st], kvh * PA_D, row);
-          tma_load_2d(sb + PA_TILE_BYTES + PA_BOX, &tmV, &full[st], kvh * PA_D + 64, row);
+#pragma unroll
+          for (int bx = 0; bx < C::NBOX; ++bx) {
+            tma_load_2d(sb + bx * PA_BOX, &tmK, &full[st], kvh * D + bx * 64, row);
+            tma_load_2d(sb + PA_TILE_BYTES + bx * PA_BOX, &tmV, &full[st], kvh * D + bx * 64, row);
+          }
         }
       }
     } else {
@@ -109,11 +120,11 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       const int mat = lane >> 3;
       // ---- Q fragments (A operand, 16 rows per warp)
       mbar_wait(qfull, qphase);
-      uint32_t qf[8][4];
+      uint32_t qf[KK][4];
       {
         const uint32_t qb = smem_u32(sQ);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = 0; kk < KK; ++kk) {
           const uint32_t r = warp * 16 + (mat & 1) * 8 + (lane & 7);
           const uint32_t c = (kk & 3) * 2 + (mat >> 1);
           ldmatrix_x4(qb + (kk >> 2) * PA_BOX + sw128(r, c), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
@@ -122,9 +133,9 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(qempty);
 
-      float o[16][4];
+      float o[2 * KK][4];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      for (int i = 0; i < 2 * KK; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
       float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
       const int qi0 = q0 + warp * 16 + g8;  // rows owned: qi0 and qi0 + 8
       const int qi1 = qi0 + 8;
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = 0; kk < KK; ++kk) {
 #pragma unroll
           for (int np = 0; np < 4; ++np) {
             // two n8 tiles (16 kv tokens) per ldmatrix.x4
@@ -189,7 +200,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
         l0 *= a0;
         l1 *= a1;
 #pragma unroll
-        for (int dn = 0; dn < 16; ++dn) {
+        for (int dn = 0; dn < 2 * KK; ++dn) {
           o[dn][0] *= a0;
           o[dn][1] *= a0;
           o[dn][2] *= a1;
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
 #pragma unroll
         for (int kt = 0; kt < 4; ++kt) {
 #pragma unroll
-          for (int dp = 0; dp < 8; ++dp) {
+          for (int dp = 0; dp < KK; ++dp) {
             // V^T fragments for two n8 d-tiles via transposed ldmatrix
             const uint32_t r = kt * 16 + (mat & 1) * 8 + (lane & 7);
             const uint32_t c = (dp & 3) * 2 + (mat >> 1);
@@ -229,10 +240,10 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
       const float i0 = l0 > 0.f ? 1.f / l0 : 0.f;
       const float i1 = l1 > 0.f ? 1.f / l1 : 0.f;
-      __nv_bfloat16* orow0 = p.out + size_t(s0 + qi0) * p.ldo + size_t(head) * PA_D;
-      __nv_bfloat16* orow1 = p.out + size_t(s0 + qi1) * p.ldo + size_t(head) * PA_D;
+      __nv_bfloat16* orow0 = p.out + size_t(s0 + qi0) * p.ldo + size_t(head) * D;
+      __nv_bfloat16* orow1 = p.out + size_t(s0 + qi1) * p.ldo + size_t(head) * D;
 #pragma unroll
-      for (int dn = 0; dn < 16; ++dn) {
+      for (int dn = 0; dn < 2 * KK; ++dn) {
         const int col = dn * 8 + 2 * t4;
         if (qi0 < len) *reinterpret_cast<uint32_t*>(orow0 + col) = pack_bf16(o[dn][0] * i0, o[dn][1] * i0);
         if (qi1 < len) *reinterpret_cast<uint32_t*>(orow1 + col) = pack_bf16(o[dn][2] * i1, o[dn][3] * i1);
@@ -243,6 +254,20 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   }
 }
 
+template <int D>
+static int launch_prefill(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                          const PrefillParams& p, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_prefill_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(PaCfg<D>::SMEM)));
+    attr = true;
+  }
+  k_prefill_attn<D><<<grid, PA_THREADS, PaCfg<D>::SMEM, st>>>(tq, tk, tv, p);
+  HP_LAUNCH_CHECK("k_prefill_attn");
+  return HP_OK;
+}
+
 }  // namespace hp
 
 using namespace hp;
@@ -251,7 +276,7 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
                                void* o, int ldo, const int* cu_seqlens, int nseq, int total_tokens, int max_seqlen,
                                int Hq, int Hkv, int d, float scale, int max_ctas, void* stream) {
   HP_CHECK_ARG(q && k && v && o && cu_seqlens, "hp_prefill_attn: null pointer");
-  HP_CHECK_ARG(d == PA_D, "hp_prefill_attn: head_dim must be 128");
+  HP_CHECK_ARG(d == 64 || d == 128, "hp_prefill_attn: head_dim must be 64 or 128");
   HP_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0, "hp_prefill_attn: Hkv must divide Hq");
   HP_CHECK_ARG(nseq >= 1 && max_seqlen >= 1, "hp_prefill_attn: empty batch");
   HP_CHECK_ARG(max_ctas >= 1, "hp_prefill_attn: max_ctas must be >= 1");
@@ -275,13 +300,8 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
   p.out = static_cast<__nv_bfloat16*>(o);
   p.ldo = ldo;
   p.scale_log2 = scale * 1.4426950408889634f;
-  static bool attr = false;
-  if (!attr) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_prefill_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PA_SMEM)));
-    attr = true;
-  }
   const int units = nseq * p.n_qt * Hq;
-  k_prefill_attn<<<std::min(units, max_ctas), PA_THREADS, PA_SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, p);
-  HP_LAUNCH_CHECK("k_prefill_attn");
-  return HP_OK;
+  const int grid = std::min(units, max_ctas);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return d == 128 ? launch_prefill<128>(tq, tk, tv, p, grid, st) : launch_prefill<64>(tq, tk, tv, p, grid, st);
 }

@@ -1,0 +1,240 @@
+"""Concurrent prefill/decode layer driver (the reference's `_launch_prefill` /
+`_maybe_launch_decode` pair, engine.py:583-600 and 640-682, run for real).
+
+A `CoRunner` holds one Llama layer in HBM with a prefill workload (one
+sequence of T new tokens) and a decode workload (batch B over a paged KV
+cache of context C).  It can execute, on the B200:
+
+  * `isolated(phase, sms)`   one phase alone on a partition of `sms` SMs;
+  * `corun(pm, dm, ...)`     prefill layers on a pm-SM green context while
+                             decode layer-steps run on the dm-SM side;
+  * `time_sliced(...)`       the non-partitioned baseline: the same work on
+                             one full-GPU stream, prefill and decode
+                             alternating (temporal sharing).
+
+Decode steps are captured once per partition into a CUDA graph (one launch
+per layer-step instead of nine).  All times come from CUDA events recorded
+on the launching streams.
+"""
+
+from __future__ import annotations
+
+import math
+import statistics
+from dataclasses import dataclass, field
+
+import torch
+
+from ..workload import ModelSpec
+from . import lib
+from .layer import (PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch,
+                    decode_slots)
+from .partition import DECODE, PREFILL, PartitionPool, PhaseStreams
+
+
+def _ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+@dataclass
+class CoRunResult:
+    pm: int
+    dm: int
+    steps: int
+    decode_steps: int
+    span_s: float
+    prefill_tokens: int
+    decode_tokens: int
+    prefill_layer_s: list = field(default_factory=list)   # per prefill layer
+    decode_layer_s: list = field(default_factory=list)    # per decode layer-step
+    upgate_s: list = field(default_factory=list)          # dominant kernel launches
+
+    @property
+    def tokens(self) -> int:
+        return self.prefill_tokens + self.decode_tokens
+
+    @property
+    def tokens_per_s(self) -> float:
+        return self.tokens / self.span_s
+
+    def p50(self, xs) -> float:
+        return statistics.median(xs) if xs else 0.0
+
+
+class CoRunner:
+    def __init__(self, model: ModelSpec, prefill_tokens: int, decode_batch: int, decode_ctx: int,
+                 device: int = 0, seed: int = 0, pool: PartitionPool | None = None):
+        self.model = model
+        self.dev = torch.device("cuda", device)
+        self.T = prefill_tokens
+        self.B = decode_batch
+        self.C = decode_ctx
+        gen = torch.Generator(device="cpu")
+        gen.manual_seed(seed)
+        self.layer = DeviceLayer(model, LayerWeights.random(model, self.dev, gen), self.dev,
+                                 max_pos=max(prefill_tokens, decode_ctx) + 1)
+        self.pool = pool or PartitionPool(device)
+        self.n = self.pool.n
+        h = model.hidden
+        bf = dict(dtype=torch.bfloat16, device=self.dev)
+        # prefill workload
+        self.px = torch.randn(self.T, h, generator=gen).to(**bf)
+        self.py = torch.empty(self.T, h, **bf)
+        self.psc = PrefillScratch(model, self.T, self.dev)
+        pblocks = -(-self.T // PAGE)
+        self.pcache = KVCache(pblocks, model.num_kv_heads, model.head_dim, self.dev)
+        self.p_cu = torch.tensor([0, self.T], dtype=torch.int32, device=self.dev)
+        self.p_pos = torch.arange(self.T, dtype=torch.int32, device=self.dev)
+        self.p_slots = torch.arange(self.T, dtype=torch.int32, device=self.dev)
+        # decode workload: B sequences of context C over a shuffled block pool
+        pages = -(-self.C // PAGE)
+        nblk = self.B * pages
+        self.dcache = KVCache(nblk, model.num_kv_heads, model.head_dim, self.dev)
+        self.dcache.k.normal_(generator=None)
+        self.dcache.v.normal_(generator=None)
+        perm = torch.randperm(nblk, generator=gen).to(torch.int32)
+        self.block_table = perm.view(self.B, pages).to(self.dev)
+        self.ctx = torch.full((self.B,), self.C, dtype=torch.int32, device=self.dev)
+        self.d_pos, self.d_slots = decode_slots(self.block_table, self.ctx)
+        self.dx = torch.randn(self.B, h, generator=gen).to(**bf)
+        self.dy = torch.empty(self.B, h, **bf)
+        self.dsc = DecodeScratch(model, self.B, pages, self.dev, max_ctas=self.n)
+        self._graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------- launches
+    def prefill_layer(self, ps: PhaseStreams, timers=None) -> int:
+        return self.layer.prefill(self.px, self.py, self.psc, self.p_cu, 1, self.T, self.p_pos,
+                                  self.p_slots, self.pcache, ps.sms, ps.torch_stream, timers)
+
+    def decode_layer(self, ds: PhaseStreams) -> int:
+        return self.layer.decode(self.dx, self.dy, self.dsc, self.ctx, self.d_pos, self.d_slots,
+                                 self.block_table, self.dcache, ds.sms, ds.torch_stream)
+
+    def decode_graph(self, ds: PhaseStreams):
+        """CUDA graph of one decode layer-step captured on the phase's stream."""
+        key = (ds.stream, ds.sms)
+        g = self._graphs.get(key)
+        if g is None:
+            with torch.cuda.stream(ds.torch_stream):
+                self.decode_layer(ds)  # warm (tensor maps, attributes)
+                ds.torch_stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=ds.torch_stream):
+                    self.decode_layer(ds)
+            torch.cuda.synchronize()
+            self._graphs[key] = g
+        return g
+
+    def launches_per_decode_step(self) -> int:
+        splits = 1  # decode attention may add a split-combine launch
+        return 9 + splits
+
+    # --------------------------------------------------------------- timing
+    def isolated(self, phase: int, sms: int, reps: int = 5) -> float:
+        """Median seconds of one layer pass of `phase` alone on `sms` SMs."""
+        st = self.pool.phase(phase, sms)
+        times = []
+        g = self.decode_graph(st) if phase == DECODE else None
+        with torch.cuda.stream(st.torch_stream):
+            for _ in range(reps + 1):
+                torch.cuda._sleep(200_000)
+                a, b = _ev(), _ev()
+                a.record(st.torch_stream)
+                if phase == PREFILL:
+                    self.prefill_layer(st)
+                else:
+                    g.replay()
+                b.record(st.torch_stream)
+                times.append((a, b))
+        torch.cuda.synchronize()
+        ms = sorted(x.elapsed_time(y) for x, y in times[1:])
+        return ms[len(ms) // 2] * 1e-3
+
+    def corun(self, pm: int, dm: int, steps: int, decode_per_step: int, time_upgate: bool = False,
+              copy_in=None, copy_out=None) -> CoRunResult:
+        """`steps` prefill layers on pm SMs co-executed with
+        steps * decode_per_step decode layer-steps on dm SMs."""
+        ps, ds = self.pool.split(pm, dm)
+        g = self.decode_graph(ds)
+        ctrl = torch.cuda.current_stream(self.dev)
+        start, end_p, end_d = _ev(), _ev(), _ev()
+        p_ev = [(_ev(), _ev()) for _ in range(steps)]
+        ug_ev = [{"mlp_up_gate": (_ev(), _ev())} for _ in range(steps)] if time_upgate else None
+        d_ev = [(_ev(), _ev()) for _ in range(steps * decode_per_step)]
+        torch.cuda._sleep(400_000)
+        start.record(ctrl)
+        ps.torch_stream.wait_event(start)
+        ds.torch_stream.wait_event(start)
+        # interleave host enqueue so neither stream starves
+        di = 0
+        for s in range(steps):
+            with torch.cuda.stream(ps.torch_stream):
+                if copy_in is not None:
+                    copy_in(PREFILL, ps.torch_stream)
+                p_ev[s][0].record(ps.torch_stream)
+                self.prefill_layer(ps, ug_ev[s] if ug_ev else None)
+                p_ev[s][1].record(ps.torch_stream)
+                if copy_out is not None:
+                    copy_out(PREFILL, ps.torch_stream)
+            with torch.cuda.stream(ds.torch_stream):
+                for _ in range(decode_per_step):
+                    if copy_in is not None:
+                        copy_in(DECODE, ds.torch_stream)
+                    d_ev[di][0].record(ds.torch_stream)
+                    g.replay()
+                    d_ev[di][1].record(ds.torch_stream)
+                    if copy_out is not None:
+                        copy_out(DECODE, ds.torch_stream)
+                    di += 1
+        end_p.record(ps.torch_stream)
+        end_d.record(ds.torch_stream)
+        torch.cuda.synchronize()
+        span = max(start.elapsed_time(end_p), start.elapsed_time(end_d)) * 1e-3
+        res = CoRunResult(pm, dm, steps, steps * decode_per_step, span, steps * self.T,
+                          steps * decode_per_step * self.B)
+        res.prefill_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in p_ev]
+        res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
+        if ug_ev:
+            res.upgate_s = [a.elapsed_time(b) * 1e-3 for a, b in (e["mlp_up_gate"] for e in ug_ev)]
+        return res
+
+    def time_sliced(self, steps: int, decode_per_step: int) -> CoRunResult:
+        """Same work, one full-GPU stream: prefill layer then its decode steps."""
+        st = self.pool.full(PREFILL)
+        g = self.decode_graph(st)
+        start, end = _ev(), _ev()
+        p_ev = [(_ev(), _ev()) for _ in range(steps)]
+        d_ev = [(_ev(), _ev()) for _ in range(steps * decode_per_step)]
+        with torch.cuda.stream(st.torch_stream):
+            torch.cuda._sleep(400_000)
+            start.record(st.torch_stream)
+            di = 0
+            for s in range(steps):
+                p_ev[s][0].record(st.torch_stream)
+                self.prefill_layer(st)
+                p_ev[s][1].record(st.torch_stream)
+                for _ in range(decode_per_step):
+                    d_ev[di][0].record(st.torch_stream)
+                    g.replay()
+                    d_ev[di][1].record(st.torch_stream)
+                    di += 1
+            end.record(st.torch_stream)
+        torch.cuda.synchronize()
+        res = CoRunResult(self.n, self.n, steps, steps * decode_per_step,
+                          start.elapsed_time(end) * 1e-3, steps * self.T,
+                          steps * decode_per_step * self.B)
+        res.prefill_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in p_ev]
+        res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
+        return res
+
+    # ------------------------------------------------------------ workload
+    def prefill_flops(self) -> float:
+        m = self.model
+        h = m.hidden
+        gemm = 2.0 * self.T * h * (m.qkv_out_dim + h + 3 * m.intermediate)
+        attn = 2.0 * self.T * self.T * h  # causal: 4 T^2 h / 2
+        return gemm + attn
+
+    def upgate_flops(self) -> float:
+        return 4.0 * self.T * self.model.intermediate * self.model.hidden

@@ -21,13 +21,18 @@ DEV = torch.device("cuda", 0)
 
 
 def timeit(fn, iters=20, warmup=3, flush=True, stream=None):
-    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=DEV) if flush else None
+    # L2 flush by READING a buffer larger than L2 (a write-based flush would
+    # leave ~126 MB of dirty lines to be written back inside the timed kernel)
+    flush_buf = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=DEV) if flush else None
     st = stream or torch.cuda.current_stream()
     times = []
     with torch.cuda.stream(st):
         for i in range(warmup + iters):
             if flush_buf is not None:
-                flush_buf.zero_()
+                flush_buf.sum()
+            # keep the GPU busy while the host enqueues the timed launch, so
+            # host-side launch latency never lands between the two events
+            torch.cuda._sleep(100_000)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(st)
@@ -65,9 +70,8 @@ def bench_gemm_swap(T, N, K, epi, sms, results):
     y = torch.empty(T, outN, device=DEV, dtype=torch.bfloat16)
     r = torch.randn(T, outN, device=DEV).to(torch.bfloat16) if epi == lib.EPI_RESID else None
     bn = 32 if T <= 32 else 64 if T <= 64 else 128 if T <= 128 else 256
-    cols = -(-T // bn) * bn
-    ws = torch.zeros(N, cols, device=DEV, dtype=torch.float32)
-    cnt = torch.zeros((N // 128) * (cols // bn), device=DEV, dtype=torch.int32)
+    ws = torch.empty(lib.gemm_swap_ws_bytes(T, N, K, sms) // 4, device=DEV)
+    cnt = torch.zeros((N // 128) * (-(-T // bn)), device=DEV, dtype=torch.int32)
     t = timeit(lambda: lib.gemm_swap(x, w, y, ws, cnt, epi, resid=r, max_ctas=sms))
     gbs = (N * K * 2 + T * K * 2 + T * outN * 2) / t / 1e9
     results.append({"kernel": "gemm_swap", "T": T, "N": N, "K": K, "epi": epi, "sms": sms,
@@ -127,7 +131,7 @@ def main(argv=None):
         bench_gemm(4096, 2 * inter, h, lib.EPI_SILU, sms, res)
     for sms in ([148, 32] if a.quick else [148, 96, 64, 48, 32, 16]):
         bench_decode_attn(32, 2048, 32, 8, sms, res)
-    for sms in (148, 32):
+    for sms in (148, 64, 32):
         bench_gemm_swap(32, qkv, h, lib.EPI_STORE, sms, res)
         bench_gemm_swap(32, h, h, lib.EPI_RESID, sms, res)
         bench_gemm_swap(32, 2 * inter, h, lib.EPI_SILU, sms, res)

@@ -32,8 +32,8 @@ SIGNATURES = {
     "hp_partition_destroy": (_i, [_p]),
     "hp_rmsnorm": (_i, [_p, _i, _p, _p, _i, _i, _i, _f, _i, _p]),
     "hp_gemm": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
-    "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _i, _p]),
-    "hp_gemm_swap_splits": (_i, [_i, _i, _i, _i]),
+    "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
+    "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
@@ -117,14 +117,19 @@ def gemm(x, w, y, epilogue: int = EPI_STORE, resid=None, max_ctas: int = 148, st
                          epilogue, max_ctas, _stream(stream)), "hp_gemm")
 
 
-def gemm_swap(x, w, y, ws, counters, epilogue: int = EPI_STORE, resid=None, k_splits: int = 0,
+def gemm_swap_ws_bytes(T: int, N: int, K: int, max_ctas: int) -> int:
+    return load().hp_gemm_swap_ws_bytes(T, N, K, max_ctas)
+
+
+def gemm_swap(x, w, y, ws, counters, epilogue: int = EPI_STORE, resid=None,
               max_ctas: int = 148, stream=None) -> None:
     T, K = x.shape
     N = w.shape[0]
     check(load().hp_gemm_swap(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
                               _ptr(resid), resid.stride(0) if resid is not None else 0, T, N, K,
-                              epilogue, _ptr(ws), ws.numel() * ws.element_size(), _ptr(counters),
-                              counters.numel(), k_splits, max_ctas, _stream(stream)), "hp_gemm_swap")
+                              epilogue, _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                              _ptr(counters), 0 if counters is None else counters.numel(), max_ctas,
+                              _stream(stream)), "hp_gemm_swap")
 
 
 def rope_kv_write(qkv, Hq: int, Hkv: int, d: int, positions, cos_sin, slots, kcache, vcache,

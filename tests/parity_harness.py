@@ -1,0 +1,247 @@
+"""Device-vs-oracle parity harness (TEST INFRASTRUCTURE; used by the gpu tests
+and by __graft_entry__.smoke()).
+
+Config 1 of BASELINE.json: a tiny Llama-style model (2 layers, hidden 256, 4
+heads of 64, 2 KV heads, intermediate 768, vocab 1024; random init) runs one
+1024-token prefill plus 8 requests with contexts {17, 64, 128, 255, 256,
+511, 512, 1000} (partial last pages) through the B200 kernels, then 16
+greedy decode steps for all 9 sequences, and the same computation in the
+numpy oracle (oracle/numerics.py, bf16 rounding at the kernel boundaries).
+
+Tolerances (stated here, asserted by the callers):
+  hidden states  |dev - ref| <= ATOL + RTOL |ref|  with ATOL = 2e-2, RTOL = 1e-2
+                 (bf16 storage: one ulp at |x| in [4, 8) is 3.1e-2)
+  greedy tokens  identical at every step (teacher-forced on the oracle's
+                 token, so one near-tie cannot cascade); a difference is
+                 tolerated only where the oracle's top-2 logit margin is
+                 within MARGIN_ULPS bf16 ulps of the top logit (a genuine
+                 bf16 tie) and is reported as `tie_flips`.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from oracle import numerics as O  # noqa: E402
+
+ATOL, RTOL = 2e-2, 1e-2
+MARGIN_ULPS = 1
+TINY_CTX = (17, 64, 128, 255, 256, 511, 512, 1000)
+PAGE = 64
+
+
+def _bf(x):
+    return O.bf16_round(np.asarray(x, dtype=np.float32))
+
+
+def tiny_weights(seed: int, vocab: int = 1024):
+    from paper_2504_19516_b200.workload import TINY_MODEL as m
+
+    rng = np.random.default_rng(seed)
+    h, I = m.hidden, m.intermediate
+    layers = []
+    for _ in range(m.num_layers):
+        layers.append(O.LayerWeights(
+            _bf(rng.normal(0, 0.02, (m.qkv_out_dim, h))), _bf(rng.normal(0, 0.02, (h, h))),
+            _bf(rng.normal(0, 0.02, (I, h))), _bf(rng.normal(0, 0.02, (I, h))),
+            _bf(rng.normal(0, 0.02, (h, I))), _bf(1.0 + 0.1 * rng.normal(size=h)),
+            _bf(1.0 + 0.1 * rng.normal(size=h))))
+    embed = _bf(rng.normal(0, 1.0, (vocab, h)))
+    lm_head = _bf(rng.normal(0, 0.08, (vocab, h)))
+    final_norm = _bf(np.ones(h))
+    return m, layers, embed, final_norm, lm_head
+
+
+def _ulp_bf16(x):
+    e = np.floor(np.log2(np.maximum(np.abs(x), 1e-30)))
+    return 2.0 ** (e - 7)
+
+
+def run_tiny(seed: int = 0, decode_steps: int = 16, device: int = 0) -> dict:
+    """Run config 1 on device and oracle; returns comparison statistics."""
+    import torch
+
+    from paper_2504_19516_b200.device.layer import LayerWeights
+    from paper_2504_19516_b200.device.model import DeviceModel
+
+    vocab = 1024
+    m, Wl, embed, final_norm, lm_head = tiny_weights(seed, vocab)
+    dev = torch.device("cuda", device)
+    rng = np.random.default_rng(seed + 1)
+    prompts = [rng.integers(0, vocab, 1024)] + [rng.integers(0, vocab, c) for c in TINY_CTX]
+    lens = [len(p) for p in prompts]
+    nseq = len(prompts)
+    # paged block pool with a shuffled assignment
+    need = [-(-(L + decode_steps + 1) // PAGE) for L in lens]
+    nblk = sum(need) + 5
+    perm = rng.permutation(nblk)
+    max_pages = max(need)
+    bt = np.zeros((nseq, max_pages), dtype=np.int32)
+    k = 0
+    for i, nb in enumerate(need):
+        bt[i, :nb] = perm[k:k + nb]
+        k += nb
+
+    def t(a, dt=torch.bfloat16):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(dev)
+
+    dW = [LayerWeights.from_numpy(dev, w.w_qkv, w.w_o, w.w_gate, w.w_up, w.w_down, w.attn_norm,
+                                  w.mlp_norm) for w in Wl]
+    dm = DeviceModel(m, vocab, nblk, dev, weights=dW, embed=t(embed), final_norm=t(final_norm),
+                     lm_head=t(lm_head), max_prefill_tokens=sum(lens), max_batch=nseq,
+                     max_pages=max_pages)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+
+    # ---------------- device prefill
+    tokens = np.concatenate(prompts).astype(np.int32)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    pos = np.concatenate([np.arange(L) for L in lens]).astype(np.int32)
+    slots = np.concatenate([bt[i, np.arange(L) // PAGE] * PAGE + np.arange(L) % PAGE
+                            for i, L in enumerate(lens)]).astype(np.int32)
+    dev_hidden = []
+    hid = dm.prefill(t(tokens, torch.int32), t(cu, torch.int32), max(lens), t(pos, torch.int32),
+                     t(slots, torch.int32), sms, hidden_out=dev_hidden)
+    last_idx = torch.tensor(cu[1:] - 1, device=dev, dtype=torch.long)
+    dev_logits = dm.logits_of(hid[last_idx].contiguous(), sms).float().cpu().numpy()
+    dev_hidden = [h.float().cpu().numpy() for h in dev_hidden]
+
+    # ---------------- oracle prefill (per sequence) + cache mirror
+    d, Hq, Hkv = m.head_dim, m.num_heads, m.num_kv_heads
+    table = O.rope_table(4096, d)
+    kc = [np.zeros((nblk, Hkv, PAGE, d), np.float32) for _ in range(m.num_layers)]
+    vc = [np.zeros((nblk, Hkv, PAGE, d), np.float32) for _ in range(m.num_layers)]
+    ref_hidden = [np.zeros((len(tokens), m.hidden), np.float32) for _ in range(m.num_layers)]
+    ref_last = np.zeros((nseq, m.hidden), np.float32)
+    for i, p in enumerate(prompts):
+        x = embed[p]
+        L = len(p)
+        for li, W in enumerate(Wl):
+            x, kk, vv = O.layer_prefill(x, W, Hq, Hkv, d, np.arange(L), table, bf16_boundaries=True)
+            ref_hidden[li][cu[i]:cu[i + 1]] = x
+            for j in range(L):
+                b, o = bt[i, j // PAGE], j % PAGE
+                kc[li][b, :, o, :] = kk[j]
+                vc[li][b, :, o, :] = vv[j]
+        ref_last[i] = x[-1]
+
+    out = {"prefill_tokens": int(len(tokens)), "nseq": nseq}
+    errs = []
+    for li in range(m.num_layers):
+        diff = np.abs(dev_hidden[li] - ref_hidden[li])
+        errs.append(float(np.max(diff - RTOL * np.abs(ref_hidden[li]))))
+    out["prefill_max_abs"] = [float(np.max(np.abs(dev_hidden[li] - ref_hidden[li])))
+                              for li in range(m.num_layers)]
+    out["prefill_excess"] = max(errs)  # <= ATOL required
+
+    # ---------------- greedy decode, teacher-forced on the oracle's tokens
+    ref_tok, margin, ref_logits = O.greedy_tokens(ref_last, final_norm, lm_head)
+    dev_tok = dev_logits.argmax(-1)
+    matches, near_ties, mismatches, tie_flips = 0, 0, 0, 0
+
+    def score(ref_tok, dev_tok, margin, logits):
+        nonlocal matches, near_ties, mismatches, tie_flips
+        for r, dv, mg, lg in zip(ref_tok, dev_tok, margin, logits):
+            tie = mg <= MARGIN_ULPS * _ulp_bf16(np.max(lg))
+            near_ties += int(tie)
+            if r == dv:
+                matches += 1
+            elif tie:
+                tie_flips += 1
+            else:
+                mismatches += 1
+
+    score(ref_tok, dev_tok, margin, ref_logits)
+    ctx = np.array(lens, dtype=np.int32)
+    bt_dev = t(bt, torch.int32)
+    cur = ref_tok.astype(np.int32)
+    step_err = []
+    for s in range(decode_steps):
+        ctx = ctx + 1
+        hid = dm.decode(t(cur, torch.int32), t(ctx, torch.int32), bt_dev, sms)
+        dl = dm.logits_of(hid, sms).float().cpu().numpy()
+        dh = hid.float().cpu().numpy()
+        x = embed[cur]
+        for li, W in enumerate(Wl):
+            x = O.layer_decode(x, W, Hq, Hkv, d, ctx, table, kc[li], vc[li], bt, bf16_boundaries=True)
+        step_err.append(float(np.max(np.abs(dh - x) - RTOL * np.abs(x))))
+        rt, mg, lg = O.greedy_tokens(x, final_norm, lm_head)
+        score(rt, dl.argmax(-1), mg, lg)
+        cur = rt.astype(np.int32)
+    out["decode_excess"] = max(step_err)
+    out["tokens_compared"] = matches + mismatches + tie_flips
+    out["token_matches"] = matches
+    out["token_mismatches"] = mismatches
+    out["near_ties"] = near_ties
+    out["tie_flips"] = tie_flips
+    return out
+
+
+def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, device: int = 0) -> dict:
+    """Config-2 numerics at a CPU-affordable size: one Llama-3-8B layer,
+    prefill of T tokens and one decode step for B sequences of context ctx,
+    device vs oracle."""
+    import torch
+
+    from paper_2504_19516_b200.device.layer import (DecodeScratch, DeviceLayer, KVCache,
+                                                    LayerWeights, PrefillScratch, decode_slots)
+    from paper_2504_19516_b200.workload import MODEL_PRESETS
+
+    m = MODEL_PRESETS["llama3-8b"]
+    rng = np.random.default_rng(seed)
+    h, I, d, Hq, Hkv = m.hidden, m.intermediate, m.head_dim, m.num_heads, m.num_kv_heads
+    W = O.LayerWeights(_bf(rng.normal(0, 0.02, (m.qkv_out_dim, h))), _bf(rng.normal(0, 0.02, (h, h))),
+                       _bf(rng.normal(0, 0.02, (I, h))), _bf(rng.normal(0, 0.02, (I, h))),
+                       _bf(rng.normal(0, 0.02, (h, I))), _bf(1 + 0.1 * rng.normal(size=h)),
+                       _bf(1 + 0.1 * rng.normal(size=h)))
+    dev = torch.device("cuda", device)
+    lyr = DeviceLayer(m, LayerWeights.from_numpy(dev, W.w_qkv, W.w_o, W.w_gate, W.w_up, W.w_down,
+                                                 W.attn_norm, W.mlp_norm), dev, max_pos=max(T, ctx) + 2)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    table = O.rope_table(max(T, ctx) + 2, d)
+
+    def t(a, dt=torch.bfloat16):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(dev)
+
+    # prefill
+    x = _bf(rng.normal(size=(T, h)))
+    cache = KVCache(-(-T // PAGE), Hkv, d, dev)
+    y = torch.empty(T, h, dtype=torch.bfloat16, device=dev)
+    lyr.prefill(t(x), y, PrefillScratch(m, T, dev), t(np.array([0, T]), torch.int32), 1, T,
+                t(np.arange(T), torch.int32), t(np.arange(T), torch.int32), cache, sms)
+    ref, _, _ = O.layer_prefill(x, W, Hq, Hkv, d, np.arange(T), table, bf16_boundaries=True)
+    dy = y.float().cpu().numpy()
+    res = {"prefill_max_abs": float(np.max(np.abs(dy - ref))),
+           "prefill_excess": float(np.max(np.abs(dy - ref) - RTOL * np.abs(ref)))}
+    # decode: B sequences with random cache contents, one new token each
+    pages = -(-(ctx) // PAGE)
+    nblk = B * pages + 3
+    kc = _bf(rng.normal(size=(nblk, Hkv, PAGE, d)))
+    vc = _bf(rng.normal(size=(nblk, Hkv, PAGE, d)))
+    bt = rng.permutation(nblk)[: B * pages].reshape(B, pages).astype(np.int32)
+    ctxs = np.array([ctx - 7 * i for i in range(B)], dtype=np.int32)
+    xd = _bf(rng.normal(size=(B, h)))
+    dcache = KVCache(nblk, Hkv, d, dev)
+    dcache.k.copy_(t(kc))
+    dcache.v.copy_(t(vc))
+    ctx_t, bt_t = t(ctxs, torch.int32), t(bt, torch.int32)
+    pos, slots = decode_slots(bt_t, ctx_t)
+    yd = torch.empty(B, h, dtype=torch.bfloat16, device=dev)
+    lyr.decode(t(xd), yd, DecodeScratch(m, B, pages, dev), ctx_t, pos, slots, bt_t, dcache, sms)
+    refd = O.layer_decode(xd, W, Hq, Hkv, d, ctxs, table, kc, vc, bt, bf16_boundaries=True)
+    dyd = yd.float().cpu().numpy()
+    res["decode_max_abs"] = float(np.max(np.abs(dyd - refd)))
+    res["decode_excess"] = float(np.max(np.abs(dyd - refd) - RTOL * np.abs(refd)))
+    # the new tokens' K/V landed in the cache slots
+    kdev = dcache.k.float().cpu().numpy()
+    res["kv_write_max_abs"] = float(max(np.max(np.abs(kdev[bt[b, (c - 1) // PAGE], :, (c - 1) % PAGE] -
+                                                      kc[bt[b, (c - 1) // PAGE], :, (c - 1) % PAGE]))
+                                        for b, c in enumerate(ctxs)))
+    return res

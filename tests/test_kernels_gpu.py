@@ -93,41 +93,43 @@ def test_gemm_silu(T, gen):
     assert rel_err(y, ref) < 2e-2
 
 
-def _ws(N, T):
+def _ws(N, T, K, ctas):
     bn = 32 if T <= 32 else 64 if T <= 64 else 128 if T <= 128 else 256
-    cols = -(-T // bn) * bn
-    ws = torch.zeros(N, cols, device=DEV, dtype=torch.float32)
+    ws = torch.empty(lib.gemm_swap_ws_bytes(T, N, K, ctas) // 4, device=DEV, dtype=torch.float32)
     cnt = torch.zeros((N // 128) * (-(-T // bn)), device=DEV, dtype=torch.int32)
     return ws, cnt
 
 
-@pytest.mark.parametrize("T,N,K,splits", [(1, 128, 256, 1), (8, 6144, 4096, 0), (32, 4096, 4096, 0),
-                                          (33, 1024, 1024, 3), (100, 512, 2048, 0), (256, 256, 512, 2)])
-def test_gemm_swap_store(T, N, K, splits, gen):
+@pytest.mark.parametrize("T,N,K,ctas", [(1, 128, 256, 1), (8, 6144, 4096, 148), (32, 4096, 4096, 64),
+                                        (32, 4096, 4096, 32), (33, 1024, 1024, 7), (100, 512, 2048, 148),
+                                        (256, 256, 512, 3), (32, 28672, 4096, 148)])
+def test_gemm_swap_store(T, N, K, ctas, gen):
     x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
-    ws, cnt = _ws(N, T)
-    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, k_splits=splits, max_ctas=64)
+    ws, cnt = _ws(N, T, K, ctas)
+    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
     assert rel_err(y, x.float() @ w.float().T) < 1e-2
-    # workspace and counters are left clean for the next call
+    # arrival counters are left clean for the next call
     torch.cuda.synchronize()
-    assert ws.abs().max().item() == 0.0 and cnt.abs().max().item() == 0
-    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, k_splits=splits, max_ctas=64)
+    assert cnt.abs().max().item() == 0
+    y.zero_()
+    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
     assert rel_err(y, x.float() @ w.float().T) < 1e-2
 
 
-def test_gemm_swap_resid_silu(gen):
+@pytest.mark.parametrize("ctas", [32, 148])
+def test_gemm_swap_resid_silu(ctas, gen):
     T, K = 32, 1024
     x, r = bf((T, K), gen=gen), bf((T, 4096), gen=gen)
     w = bf((4096, K), 0.05, gen)
-    ws, cnt = _ws(4096, T)
+    ws, cnt = _ws(4096, T, K, ctas)
     y = r.clone()
-    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_RESID, resid=y, max_ctas=32)
+    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_RESID, resid=y, max_ctas=ctas)
     assert rel_err(y, x.float() @ w.float().T + r.float()) < 1e-2
     wi, g, u = interleave_ref(1024, K, gen)
-    ws2, cnt2 = _ws(2048, T)
+    ws2, cnt2 = _ws(2048, T, K, ctas)
     y2 = torch.empty(T, 1024, device=DEV, dtype=torch.bfloat16)
-    lib.gemm_swap(x, wi, y2, ws2, cnt2, lib.EPI_SILU, max_ctas=32)
+    lib.gemm_swap(x, wi, y2, ws2, cnt2, lib.EPI_SILU, max_ctas=ctas)
     ref = silu_ref(x.float() @ g.float().T) * (x.float() @ u.float().T)
     assert rel_err(y2, ref) < 2e-2
 
@@ -190,10 +192,10 @@ def attn_ref(q, k, v, causal, scale):
     return torch.einsum("hqk,khd->qhd", s.softmax(-1), v)
 
 
-@pytest.mark.parametrize("lens,Hq,Hkv", [([128], 4, 1), ([1000], 8, 2), ([64, 130, 7], 4, 4),
-                                         ([2048], 32, 8)])
-def test_prefill_attn(lens, Hq, Hkv, gen):
-    d = 128
+@pytest.mark.parametrize("lens,Hq,Hkv,d", [([128], 4, 1, 128), ([1000], 8, 2, 128),
+                                           ([64, 130, 7], 4, 4, 128), ([2048], 32, 8, 128),
+                                           ([1024], 4, 2, 64), ([5, 300], 4, 2, 64)])
+def test_prefill_attn(lens, Hq, Hkv, d, gen):
     T = sum(lens)
     qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
     q, k, v = qkv[:, : Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
@@ -226,11 +228,13 @@ def make_cache(B, ctx, Hkv, d, page, gen, extra_blocks=3):
     return kc, vc, bt
 
 
-@pytest.mark.parametrize("ctx,Hq,Hkv", [([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2),
-                                        ([2048] * 32, 32, 8), ([1], 8, 1), ([5000, 33], 64, 8)])
+@pytest.mark.parametrize("ctx,Hq,Hkv,d", [([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2, 128),
+                                          ([2048] * 32, 32, 8, 128), ([1], 8, 1, 128),
+                                          ([5000, 33], 64, 8, 128), ([3000] * 3, 32, 8, 128),
+                                          ([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2, 64)])
 @pytest.mark.parametrize("max_ctas", [8, 148])
-def test_decode_attn(ctx, Hq, Hkv, max_ctas, gen):
-    d, page = 128, 64
+def test_decode_attn(ctx, Hq, Hkv, d, max_ctas, gen):
+    page = 64
     B = len(ctx)
     kc, vc, bt = make_cache(B, ctx, Hkv, d, page, gen)
     q = bf((B, Hq * d), gen=gen)
@@ -269,4 +273,25 @@ def test_partition_confinement():
     assert len(outs[1]) <= 16
     assert len(outs[0]) <= n - 16
     assert not (outs[0] & outs[1])
+    part.close()
+
+
+def test_partition_confinement_under_graph_replay():
+    """Kernels replayed from a CUDA graph captured on a green-context stream
+    stay on that partition's SMs (decode steps are graph-replayed)."""
+    n = lib.device_sms(0)
+    part = lib.Partition(24)
+    st = part.stream(1)
+    buf = torch.zeros(4 * n, 3, device=DEV, dtype=torch.int64)
+    with torch.cuda.stream(st):
+        lib.probe(buf, 4 * n, spin_ns=20000, stream=st)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            lib.probe(buf, 4 * n, spin_ns=20000, stream=st)
+        buf.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    sms = set(buf[:, 0].tolist())
+    assert len(sms) <= 24, sorted(sms)
     part.close()

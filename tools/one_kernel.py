@@ -19,7 +19,7 @@ if which.startswith("swap"):
     x = torch.randn(T, K, device=DEV).to(torch.bfloat16)
     w = (torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16)
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
-    ws = torch.zeros(N, 32, device=DEV)
+    ws = torch.empty(lib.gemm_swap_ws_bytes(T, N, K, sms) // 4, device=DEV)
     cnt = torch.zeros(N // 128, device=DEV, dtype=torch.int32)
     for _ in range(reps):
         lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, max_ctas=sms)
