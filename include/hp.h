@@ -76,7 +76,14 @@ int hp_partition_destroy(hp_partition* part);
 int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out, int ldo, int rows, int cols,
                float eps, int max_ctas, void* stream);
 
-/* Token-major tcgen05 GEMM (prefill): Y[T,N] = epi(X[T,K] . W[N,K]^T).
+/* Weight layout conversion (one-time, at load): row-major W [N, K] ->
+ * tiled [N/256][K/64][256][64] with the 128B-swizzle chunk permutation, so
+ * every GEMM weight tile is one contiguous 16/32 KB run fetched by a single
+ * bulk copy.  N % 256 == 0, K % 64 == 0; `out` holds N*K bf16. */
+int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream);
+
+/* Token-major tcgen05 GEMM (prefill): Y[T,N] = epi(X[T,K] . W[N,K]^T), W
+ * tiled by hp_tile_weight (pass ldw = K).
  * SILU: W rows interleaved in blocks of 64 (gate, up), Y has N/2 columns.
  * The qkv / o_proj / mlp_up_gate / mlp_down kernels of layer_kernels
  * (workload.py:162-210) at phase "prefill". */
@@ -121,6 +128,15 @@ int hp_decode_attn(const void* q, int ldq, const void* kcache, const void* vcach
                    void* workspace, size_t ws_bytes, int max_ctas, void* stream);
 
 /* ---------------------------------------------------- instrumentation */
+/* Memory-bandwidth probe behind the SRM memory term D_p = D min(1, p/n_d)
+ * (perf_model.py:172-180): stream `bytes` from `src` with `ctas` CTAs.
+ * method 0 = 128-bit loads, 1 = TMA bulk copies (bytes % 32 KB == 0).
+ * `out` receives a dummy reduction. */
+int hp_membw(const void* src, size_t bytes, int ctas, int method, float* out, void* stream);
+/* Same, through 2-D TMA boxes {64 bf16, box_rows} of a [rows, cols] bf16
+ * matrix (the GEMM weight-stream access shape). */
+int hp_membw2d(const void* src, int rows, int cols, int box_rows, int ctas, float* out, void* stream);
+
 /* Per-CTA probe: out[i] = {smid, start_ns, end_ns} for `ctas` CTAs spinning
  * `spin_ns` each -- partition confinement (%smid) and measured idle. */
 int hp_probe(int ctas, int threads, int64_t spin_ns, uint64_t* out, void* stream);

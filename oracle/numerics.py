@@ -195,6 +195,6 @@ def greedy_tokens(hidden: np.ndarray, final_norm: np.ndarray, lm_head: np.ndarra
                   bf16_boundaries: bool = True):
     """argmax over logits = RMSNorm(hidden) . lm_head^T; also the top-2 margin."""
     n = _b(rmsnorm(hidden, final_norm), bf16_boundaries)
-    logits = n @ lm_head.T
+    logits = _b(n @ lm_head.T, bf16_boundaries)  # the device stores logits as bf16
     top2 = np.sort(logits, axis=-1)[:, -2:]
     return logits.argmax(axis=-1), top2[:, 1] - top2[:, 0], logits

@@ -106,6 +106,35 @@ HP_DEVICE void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, 
       : "memory");
 }
 
+// 1-D bulk copy global -> shared, completing on an mbarrier (tx bytes).
+// Used for operands stored pre-tiled and pre-swizzled in HBM (weights, KV
+// pages): one request per tile instead of one per 128-byte row, which is
+// what lets a single SM stream ~200 GB/s (2-D boxes with 128 B rows top out
+// near 80 GB/s per SM from DRAM).
+HP_DEVICE void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+HP_DEVICE void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// Byte offset of the (row-block, k-block) tile of a weight stored in the
+// tiled layout [N/256][K/64][256 rows][64 cols], each 16B chunk c of row r
+// at position c ^ (r & 7) (the SWIZZLE_128B pattern UMMA descriptors read).
+HP_DEVICE size_t wtile_offset(int row0, int kb, int K) {
+  return (size_t(row0 >> 8) * (K >> 6) + kb) * (256 * 64 * 2) + size_t(row0 & 255) * 128;
+}
+
 HP_DEVICE uint64_t l2_policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

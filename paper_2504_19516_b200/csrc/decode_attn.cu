@@ -3,24 +3,23 @@
 // ctx_lens[b] cached positions.  HBM-bound: every cached K/V byte is read
 // once per step.
 //
-// Layout: kcache/vcache [num_blocks, Hkv, page, D] bf16 (page a multiple of
-// 32, D in {64, 128}), so one (block, kv head) page is a contiguous run.  The
-// cache is viewed as a 2-D tensor [num_blocks*Hkv*page, D] and streamed with
-// TMA in tiles of 32 tokens (128B-swizzled boxes of 64 dims) into a 12-stage
-// shared-memory ring filled by a dedicated producer warp (~190 KB in flight
-// per SM at D = 128).  The producer pre-loads block-table windows and the
-// next unit's metadata so no dependent global load sits between two TMA
-// issues.
+// Cache layout (written by hp_rope_kv_write): per (block, kv head) a page is
+// [D/64][page][64] bf16 with the 16-byte chunks of token row r permuted by
+// (r & 7) -- the SWIZZLE_128B pattern.  A 64-token tile of one 64-dim half is
+// therefore one contiguous 8 KB run: the producer warp streams K and V with
+// 1-D bulk copies (one request per 8 KB rather than one per 128-byte row) into
+// a 5-stage ring (160 KB in flight per SM at D = 128), and consumers read it
+// with conflict-free ldmatrix exactly as if TMA had swizzled it.
 //
-// Work unit = (sequence b, kv head, split of `tps` 32-token tiles).  Four
+// Work unit = (sequence b, kv head, split of `tps` 64-token tiles).  Eight
 // consumer warps take the unit's tiles round-robin; each computes the GQA
 // group's scores with tensor cores in "swap" orientation
-//     S^T[32 tok, 8 heads] = K[32, D] . Q^T[D, 8]        (mma.m16n8k16)
-//     O^T[D, 8]           += V^T[D, 32] . P^T[32, 8]
-// so the query group (<= 8 heads) sits in the MMA's N=8 dimension, keeps an
-// exp2 online softmax with warp-shuffle max/sum, and the warps merge their
-// (m, l, O) at the unit end.  Multi-split sequences write fp32 partials that
-// k_decode_combine merges by log-sum-exp.
+//     S^T[64 tok, 8 heads] = K[64, D] . Q^T[D, 8]        (mma.m16n8k16)
+//     O^T[D, 8]           += V^T[D, 64] . P^T[64, 8]
+// so the query group (<= 8 heads) sits in the MMA's N=8 dimension, with an
+// exp2 online softmax and warp-shuffle max/sum; the warps merge (m, l, O) at
+// the unit end and multi-split sequences are merged by log-sum-exp in
+// k_decode_combine.
 //
 // Caches must not hold NaN/Inf in unused slots of partially filled pages
 // (allocate them zeroed): masked probabilities are exactly 0, but 0 * NaN is
@@ -34,26 +33,28 @@
 
 namespace hp {
 
-constexpr int DA_TILE = 32;
-constexpr int DA_STAGES = 12;
-constexpr int DA_CONSUMERS = 4;
+constexpr int DA_TILE = 64;
+constexpr int DA_CONSUMERS = 8;
 constexpr int DA_THREADS = (DA_CONSUMERS + 1) * 32;
-constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;  // 32 rows x 128 B
-constexpr int DA_PROW = 40;                          // padded P^T row (bf16)
+constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;  // 64 rows x 128 B
+constexpr int DA_PROW = 72;                          // padded P^T row (bf16)
 
 template <int D>
 struct DaCfg {
   static constexpr int NBOX = D / 64;                           // 128B boxes per row
   static constexpr uint32_t STAGE_BYTES = 2 * NBOX * DA_BOX_BYTES;
+  static constexpr int STAGES = int((160u * 1024u) / STAGE_BYTES);
   static constexpr int CB = 8 * D + 16;                         // per-warp merge buffer (floats)
-  static constexpr size_t SMEM = 1024 + size_t(DA_STAGES) * STAGE_BYTES +
+  static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES +
                                  DA_CONSUMERS * CB * sizeof(float) +
-                                 DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * DA_STAGES * 8 + 64;
+                                 DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * STAGES * 8 + 64 + 16;
 };
 
 struct DecodeParams {
   const __nv_bfloat16* q;
   int ldq;
+  const uint8_t* kc;
+  const uint8_t* vc;
   const int* block_table;
   int max_pages;
   const int* ctx_lens;
@@ -81,39 +82,45 @@ __device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(DA_THREADS, 1)
-    k_decode_attn(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                  const DecodeParams p) {
+__global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParams p) {
   using C = DaCfg<D>;
   constexpr int KK = D / 16;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
-  float* cbuf = reinterpret_cast<float*>(ring + DA_STAGES * C::STAGE_BYTES);
+  float* cbuf = reinterpret_cast<float*>(ring + STAGES * C::STAGE_BYTES);
   __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * C::CB);
   uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + DA_CONSUMERS * 8 * DA_PROW);
-  uint64_t* empty = full + DA_STAGES;
+  uint64_t* empty = full + STAGES;
+  // Tiles are consumed round-robin by 8 warps from a ring of STAGES slots, so
+  // a warp can reach a slot more than one phase ahead of the producer, where
+  // a parity wait would be ambiguous.  Consumers first wait until the
+  // producer has issued their tile (which implies the slot's previous
+  // occupant was released), then wait on the slot's parity.
+  volatile uint32_t* issued = reinterpret_cast<volatile uint32_t*>(empty + STAGES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    for (int s = 0; s < DA_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    *issued = 0;
     fence_barrier_init();
   }
   __syncthreads();
 
   const int total = p.B * p.Hkv * p.max_splits;
   const int page_tiles = p.page / DA_TILE;
+  const size_t page_elems = size_t(p.page) * 64;  // one 64-dim half of one page
 
   if (warp == DA_CONSUMERS) {
     // ------------------------------------------------------------ producer
     // Lane j holds the block id of page (window_first + j); the next unit's
     // context length and first window are loaded one unit ahead.
+    const uint64_t pol = l2_policy_evict_first();  // KV is read once per step
     uint32_t gtile = 0;
     int u = blockIdx.x;
     int ctx_cur = 0, blk_cur = 0;
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         int blk_win = blk_cur;
         for (int t = t0; t < t1; ++t) {
           const int pg = t / page_tiles;
-          if (pg >= win_first + 32) {  // slide the window (rare: > 32 pages per unit)
+          if (pg >= win_first + 32) {  // slide the window (> 32 pages per unit)
             win_first += 32;
             const int pj = win_first + lane;
             blk_win = pj < p.max_pages ? bt[pj] : 0;
@@ -150,17 +157,20 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
           const int blk = __shfl_sync(0xffffffffu, blk_win, pg - win_first);
           if (lane == 0) {
             const uint32_t g = gtile + (t - t0);
-            const int st = g % DA_STAGES;
-            const uint32_t ph = (g / DA_STAGES) & 1;
-            const int row = (blk * p.Hkv + id.kvh) * p.page + (t % page_tiles) * DA_TILE;
+            const int st = g % STAGES;
+            const uint32_t ph = (g / STAGES) & 1;
+            const size_t base = (size_t(blk) * p.Hkv + id.kvh) * C::NBOX * page_elems +
+                                size_t(t % page_tiles) * DA_TILE * 64;
             mbar_wait(&empty[st], ph ^ 1);
             mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
             uint8_t* sb = ring + st * C::STAGE_BYTES;
 #pragma unroll
             for (int bx = 0; bx < C::NBOX; ++bx) {
-              tma_load_2d(sb + bx * DA_BOX_BYTES, &tmK, &full[st], bx * 64, row);
-              tma_load_2d(sb + (C::NBOX + bx) * DA_BOX_BYTES, &tmV, &full[st], bx * 64, row);
+              const size_t off = (base + bx * page_elems) * 2;
+              bulk_load_hint(sb + bx * DA_BOX_BYTES, p.kc + off, DA_BOX_BYTES, &full[st], pol);
+              bulk_load_hint(sb + (C::NBOX + bx) * DA_BOX_BYTES, p.vc + off, DA_BOX_BYTES, &full[st], pol);
             }
+            *issued = g + 1;
           }
           __syncwarp();
         }
@@ -217,18 +227,20 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
 
       for (int i = warp; i < nt; i += DA_CONSUMERS) {
         const uint32_t g = gtile + i;
-        const int st = g % DA_STAGES;
-        const uint32_t ph = (g / DA_STAGES) & 1;
+        const int st = g % STAGES;
+        const uint32_t ph = (g / STAGES) & 1;
+        while (*issued <= g) __nanosleep(64);
         mbar_wait(&full[st], ph);
         const uint32_t kb = smem_u32(ring + st * C::STAGE_BYTES);
         const uint32_t vb = kb + C::NBOX * DA_BOX_BYTES;
-        // ---- S^T = K . Q^T  (two 16-token m tiles)
-        float sc[2][4];
+        // ---- S^T = K . Q^T : four independent 16-token m tiles
+        float sc[4][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
+        for (int mt = 0; mt < 4; ++mt) sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
 #pragma unroll
-          for (int kk = 0; kk < KK; ++kk) {
+        for (int kk = 0; kk < KK; ++kk) {
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
             const uint32_t r = mt * 16 + (mat & 1) * 8 + (lane & 7);
             const uint32_t c = (kk & 3) * 2 + (mat >> 1);
             uint32_t a[4];
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         const int tokbase = (t0 + i) * DA_TILE;
         float tm0 = -INFINITY, tm1 = -INFINITY;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < 4; ++mt) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const bool valid = tokbase + mt * 16 + g8 + h * 8 < ctx;
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
           o[dm][3] *= a1;
         }
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < 4; ++mt) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const float p0 = exp2f(sc[mt][2 * h] - n0);
@@ -283,16 +295,16 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         }
         __syncwarp();
         // ---- O^T += V^T . P^T
-        uint32_t pf[2][2];
+        uint32_t pf[4][2];
 #pragma unroll
-        for (int kt = 0; kt < 2; ++kt) {
+        for (int kt = 0; kt < 4; ++kt) {
           pf[kt][0] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4);
           pf[kt][1] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4 + 8);
         }
 #pragma unroll
-        for (int dm = 0; dm < KK; ++dm) {
+        for (int kt = 0; kt < 4; ++kt) {
 #pragma unroll
-          for (int kt = 0; kt < 2; ++kt) {
+          for (int dm = 0; dm < KK; ++dm) {
             const uint32_t r = kt * 16 + (mat >> 1) * 8 + (lane & 7);
             const uint32_t c = (dm & 3) * 2 + (mat & 1);
             uint32_t a[4];
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
       }
-      // ---- merge the four warps' (m, l, O)
+      // ---- merge the consumer warps' (m, l, O)
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -324,19 +336,17 @@ __global__ void __launch_bounds__(DA_THREADS, 1)
       }
       named_bar_sync(1, DA_CONSUMERS * 32);
       const int nsplit = (ntiles + p.tps - 1) / p.tps;
-      constexpr int Q4 = D / 4;  // float4 groups per head row
+      const int nw = min(DA_CONSUMERS, nt);  // warps that saw at least one tile
+      constexpr int Q4 = D / 4;              // float4 groups per head row
       for (int e = threadIdx.x; e < p.G * Q4; e += DA_CONSUMERS * 32) {
         const int h = e / Q4;
         const int d4 = (e % Q4) * 4;
         float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < DA_CONSUMERS; ++w) M = fmaxf(M, cbuf[w * C::CB + 8 * D + h]);
+        for (int w = 0; w < nw; ++w) M = fmaxf(M, cbuf[w * C::CB + 8 * D + h]);
         float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int w = 0; w < DA_CONSUMERS; ++w) {
+        for (int w = 0; w < nw; ++w) {
           const float* c = cbuf + w * C::CB;
-          const float mw = c[8 * D + h];
-          const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+          const float f = exp2f(c[8 * D + h] - M);
           L += f * c[8 * D + 8 + h];
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[j] += f * c[h * D + d4 + j];
@@ -402,8 +412,7 @@ __global__ void k_decode_combine(const DecodeParams p) {
 }
 
 template <int D>
-static int launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const DecodeParams& p,
-                         int max_ctas, cudaStream_t st) {
+static int launch_decode(const DecodeParams& p, int max_ctas, cudaStream_t st) {
   using C = DaCfg<D>;
   static bool attr = false;
   if (!attr) {
@@ -411,7 +420,7 @@ static int launch_decode(const CUtensorMap& tk, const CUtensorMap& tv, const Dec
     attr = true;
   }
   const int units = p.B * p.Hkv * p.max_splits;
-  k_decode_attn<D><<<std::min(units, max_ctas), DA_THREADS, C::SMEM, st>>>(tk, tv, p);
+  k_decode_attn<D><<<std::min(units, max_ctas), DA_THREADS, C::SMEM, st>>>(p);
   HP_LAUNCH_CHECK("k_decode_attn");
   if (p.max_splits > 1) {
     const int warps = p.B * p.Hq;
@@ -436,7 +445,7 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
                               void* stream) {
   HP_CHECK_ARG(q && kcache && vcache && block_table && ctx_lens && out, "hp_decode_attn: null pointer");
   HP_CHECK_ARG(d == 64 || d == 128, "hp_decode_attn: head_dim must be 64 or 128");
-  HP_CHECK_ARG(page % DA_TILE == 0 && page >= DA_TILE, "hp_decode_attn: page must be a multiple of 32");
+  HP_CHECK_ARG(page % DA_TILE == 0 && page >= DA_TILE, "hp_decode_attn: page must be a multiple of 64");
   HP_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0 && Hq / Hkv <= 8, "hp_decode_attn: GQA group must be <= 8");
   HP_CHECK_ARG(B >= 1 && max_pages >= 1 && num_blocks >= 1, "hp_decode_attn: empty batch/cache");
   HP_CHECK_ARG(max_ctas >= 1, "hp_decode_attn: max_ctas must be >= 1");
@@ -444,6 +453,8 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   DecodeParams p{};
   p.q = static_cast<const __nv_bfloat16*>(q);
   p.ldq = ldq;
+  p.kc = static_cast<const uint8_t*>(kcache);
+  p.vc = static_cast<const uint8_t*>(vcache);
   p.block_table = block_table;
   p.max_pages = max_pages;
   p.ctx_lens = ctx_lens;
@@ -455,11 +466,11 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   p.G = Hq / Hkv;
   p.page = page;
   p.scale_log2 = scale * 1.4426950408889634f;
-  // split so that the unit count covers the grid ~4x, at least 4 tiles/unit
+  // split so that the unit count covers the grid ~4x, at least 2 tiles/unit
   const int max_tiles = max_pages * (page / DA_TILE);
   const int pairs = B * Hkv;
   int tps = max_tiles;
-  while (tps > 4 && pairs * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
+  while (tps > 2 && pairs * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
   p.tps = std::max(1, tps);
   p.max_splits = (max_tiles + p.tps - 1) / p.tps;
   if (p.max_splits > 1) {
@@ -467,22 +478,15 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
     if (ws_bytes < hp_decode_attn_ws_bytes(B, Hq, d, p.max_splits)) {
       // not enough scratch for this split: fall back to fewer, longer splits
       const int ms = int(ws_bytes / (size_t(B) * Hq * (d + 2) * sizeof(float)));
-      if (ms <= 1) {
-        p.tps = max_tiles;
-      } else {
-        p.tps = (max_tiles + ms - 1) / ms;
-      }
+      p.tps = ms <= 1 ? max_tiles : (max_tiles + ms - 1) / ms;
       p.max_splits = (max_tiles + p.tps - 1) / p.tps;
     }
     p.ws_o = static_cast<float*>(workspace);
     p.ws_ml = p.ws_o + size_t(B) * Hq * p.max_splits * d;
   }
-  CUtensorMap tk, tv;
-  const uint64_t rows = uint64_t(num_blocks) * Hkv * page;
-  int rc = cached_tmap_bf16(&tk, kcache, rows, d, d, DA_TILE, 64, true);
-  if (rc) return rc;
-  rc = cached_tmap_bf16(&tv, vcache, rows, d, d, DA_TILE, 64, true);
-  if (rc) return rc;
+  HP_CHECK_ARG((reinterpret_cast<uintptr_t>(kcache) & 15) == 0 && (reinterpret_cast<uintptr_t>(vcache) & 15) == 0,
+               "hp_decode_attn: caches must be 16B aligned");
+  (void)num_blocks;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d == 128 ? launch_decode<128>(tk, tv, p, max_ctas, st) : launch_decode<64>(tk, tv, p, max_ctas, st);
+  return d == 128 ? launch_decode<128>(p, max_ctas, st) : launch_decode<64>(p, max_ctas, st);
 }

@@ -56,6 +56,7 @@ struct SwapParams {
   int ldr;
   float* ws;        // [tiles][max_contrib][128][BN]
   int* counters;    // [tiles], zero on entry and exit
+  const uint8_t* w;  // weights in the tiled layout (hp_tile_weight)
   int epi;
 };
 
@@ -118,7 +119,7 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
-    k_gemm_swap_sk(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+    k_gemm_swap_sk(const __grid_constant__ CUtensorMap tmX,
                    const SwapParams p) {
   using C = SwapCfg<BN>;
   constexpr int STAGES = C::STAGES;
@@ -137,7 +138,6 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = s.kb0; kb < s.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d_hint(sA + stage * C::A_BYTES, &tmW, &full[stage], kb * SBK, mt * SBM, w_policy);
+          bulk_load_hint(sA + stage * C::A_BYTES, p.w + wtile_offset(mt * SBM, kb, p.K), C::A_BYTES,
+                         &full[stage], w_policy);
           tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int BN>
-static int launch_swap(const CUtensorMap& tw, const CUtensorMap& tx, const SwapParams& p, int grid,
+static int launch_swap(const CUtensorMap& tx, const SwapParams& p, int grid,
                        cudaStream_t st) {
   using C = SwapCfg<BN>;
   static bool attr_set = false;
@@ -321,7 +322,7 @@ static int launch_swap(const CUtensorMap& tw, const CUtensorMap& tx, const SwapP
     HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_swap_sk<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     attr_set = true;
   }
-  k_gemm_swap_sk<BN><<<grid, 192, C::SMEM, st>>>(tw, tx, p);
+  k_gemm_swap_sk<BN><<<grid, 192, C::SMEM, st>>>(tx, p);
   HP_LAUNCH_CHECK("k_gemm_swap_sk");
   return HP_OK;
 }
@@ -349,7 +350,8 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
                             int max_ctas, void* stream) {
   HP_CHECK_ARG(X && W && Y, "hp_gemm_swap: null pointer");
   HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
-  HP_CHECK_ARG(N % SBM == 0, "hp_gemm_swap: N must be a multiple of 128");
+  HP_CHECK_ARG(N % 256 == 0, "hp_gemm_swap: N must be a multiple of 256 (tiled weight layout)");
+  HP_CHECK_ARG(ldw == K, "hp_gemm_swap: W must be in the tiled layout (ldw == K)");
   HP_CHECK_ARG(K % SBK == 0, "hp_gemm_swap: K must be a multiple of 64");
   HP_CHECK_ARG(epilogue >= HP_EPI_STORE && epilogue <= HP_EPI_SILU, "hp_gemm_swap: bad epilogue");
   HP_CHECK_ARG(epilogue != HP_EPI_RESID || R != nullptr, "hp_gemm_swap: residual epilogue needs R");
@@ -371,6 +373,7 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
   p.ldo = ldy;
   p.resid = static_cast<const __nv_bfloat16*>(R);
   p.ldr = ldr;
+  p.w = static_cast<const uint8_t*>(W);
   p.ws = static_cast<float*>(workspace);
   p.counters = counters;
   p.epi = epilogue;
@@ -380,17 +383,15 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
     HP_CHECK_ARG(ws_bytes >= hp_gemm_swap_ws_bytes(T, N, K, max_ctas), "hp_gemm_swap: workspace too small");
     HP_CHECK_ARG(n_counters >= p.m_tiles * p.n_tiles, "hp_gemm_swap: too few counters");
   }
-  CUtensorMap tw, tx;
-  int rc = cached_tmap_bf16(&tw, W, N, K, ldw, SBM, SBK, true);
-  if (rc) return rc;
-  rc = cached_tmap_bf16(&tx, X, T, K, ldx, BN, SBK, true);
+  CUtensorMap tx;
+  int rc = cached_tmap_bf16(&tx, X, T, K, ldx, BN, SBK, true);
   if (rc) return rc;
   const int g = (p.total_iters + p.ipc - 1) / p.ipc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (BN) {
-    case 32: return launch_swap<32>(tw, tx, p, g, st);
-    case 64: return launch_swap<64>(tw, tx, p, g, st);
-    case 128: return launch_swap<128>(tw, tx, p, g, st);
-    default: return launch_swap<256>(tw, tx, p, g, st);
+    case 32: return launch_swap<32>(tx, p, g, st);
+    case 64: return launch_swap<64>(tx, p, g, st);
+    case 128: return launch_swap<128>(tx, p, g, st);
+    default: return launch_swap<256>(tx, p, g, st);
   }
 }

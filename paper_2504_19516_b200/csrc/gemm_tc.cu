@@ -33,6 +33,7 @@ enum { EPI_STORE = 0, EPI_RESID = 1, EPI_SILU = 2 };
 struct GemmParams {
   int Ma, Nb, K;
   int m_tiles, n_tiles, k_splits, kb_per_split, num_kb;
+  const uint8_t* w;  // weights in the tiled layout (hp_tile_weight)
   __nv_bfloat16* out;
   int ldo;
   const __nv_bfloat16* resid;
@@ -81,8 +82,7 @@ __device__ __forceinline__ void add_row32(float* v, const __nv_bfloat16* src) {
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const GemmParams p) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
   using C = GemmCfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -100,7 +100,6 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -135,7 +134,8 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+          bulk_load(sB + stage * C::B_BYTES, p.w + wtile_offset(nt * BN, kb, p.K), C::B_BYTES,
+                    &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -231,8 +231,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int BN>
-static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                  cudaStream_t st) {
+static int launch(const CUtensorMap& ta, const GemmParams& p, int grid, cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -240,7 +239,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams
                                      int(C::SMEM)));
     attr_set = true;
   }
-  k_gemm_tc<BN><<<grid, 192, C::SMEM, st>>>(ta, tb, p);
+  k_gemm_tc<BN><<<grid, 192, C::SMEM, st>>>(ta, p);
   HP_LAUNCH_CHECK("k_gemm_tc");
   return HP_OK;
 }
@@ -260,15 +259,14 @@ extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, 
   HP_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SILU, "hp_gemm: bad epilogue");
   HP_CHECK_ARG(epilogue != EPI_RESID || R != nullptr, "hp_gemm: residual epilogue needs R");
   HP_CHECK_ARG(max_ctas >= 1, "hp_gemm: max_ctas must be >= 1");
-  const int BN = (N % 256 == 0) ? 256 : 128;
-  HP_CHECK_ARG(N % 128 == 0, "hp_gemm: N must be a multiple of 128");
-  HP_CHECK_ARG(epilogue != EPI_SILU || N % 128 == 0, "hp_gemm: SiLU needs N multiple of 128");
-  CUtensorMap ta, tb;
+  HP_CHECK_ARG(N % 256 == 0, "hp_gemm: N must be a multiple of 256 (tiled weight layout)");
+  HP_CHECK_ARG(ldw == K, "hp_gemm: W must be in the tiled layout (ldw == K)");
+  const int BN = 256;
+  CUtensorMap ta;
   int rc = cached_tmap_bf16(&ta, X, T, K, ldx, BM, BK, true);
   if (rc) return rc;
-  rc = cached_tmap_bf16(&tb, W, N, K, ldw, BN, BK, true);
-  if (rc) return rc;
   GemmParams p{};
+  p.w = static_cast<const uint8_t*>(W);
   p.Ma = T;
   p.Nb = N;
   p.K = K;
@@ -285,6 +283,6 @@ extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, 
   const int units = p.m_tiles * p.n_tiles;
   const int grid = std::min(units, max_ctas);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return BN == 256 ? launch<256>(ta, tb, p, grid, st) : launch<128>(ta, tb, p, grid, st);
+  return launch<256>(ta, p, grid, st);
 }
 

@@ -67,6 +67,11 @@ __global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, 
     __nv_bfloat16* row = qkv + size_t(t) * ld + size_t(head) * d;
     const int slot = (head >= Hq) ? slots[t] : 0;
     const int blk = slot / page, off = slot % page;
+    // cache page layout [d/64][page][64], 16B chunks swizzled by (token & 7)
+    auto cidx = [&](int kvh, int j) -> size_t {
+      return ((size_t(blk) * Hkv + kvh) * (d / 64) + j / 64) * size_t(page) * 64 + size_t(off) * 64 +
+             ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7);
+    };
     if (head < Hq + Hkv) {
       const float* c = cs + size_t(pos[t]) * d;
       const float c0 = c[i], c1 = c[i + 1], s0 = c[half + i], s1 = c[half + i + 1];
@@ -79,22 +84,46 @@ __global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, 
       *reinterpret_cast<uint32_t*>(row + half + i) = nhi;
       if (head >= Hq) {
         const int kh = head - Hq;
-        __nv_bfloat16* dst = kc + ((size_t(blk) * Hkv + kh) * page + off) * d;
-        *reinterpret_cast<uint32_t*>(dst + i) = nlo;
-        *reinterpret_cast<uint32_t*>(dst + half + i) = nhi;
+        *reinterpret_cast<uint32_t*>(kc + cidx(kh, i)) = nlo;
+        *reinterpret_cast<uint32_t*>(kc + cidx(kh, half + i)) = nhi;
       }
     } else {
       const int vh = head - Hq - Hkv;
-      __nv_bfloat16* dst = vc + ((size_t(blk) * Hkv + vh) * page + off) * d;
-      *reinterpret_cast<uint32_t*>(dst + i) = *reinterpret_cast<const uint32_t*>(row + i);
-      *reinterpret_cast<uint32_t*>(dst + half + i) = *reinterpret_cast<const uint32_t*>(row + half + i);
+      *reinterpret_cast<uint32_t*>(vc + cidx(vh, i)) = *reinterpret_cast<const uint32_t*>(row + i);
+      *reinterpret_cast<uint32_t*>(vc + cidx(vh, half + i)) =
+          *reinterpret_cast<const uint32_t*>(row + half + i);
     }
+  }
+}
+
+// Row-major W [N, K] (row pitch ldw) -> tiled [N/256][K/64][256][64] with
+// the SWIZZLE_128B chunk permutation; one thread per 16-byte chunk.
+__global__ void k_tile_weight(const __nv_bfloat16* __restrict__ w, int ldw,
+                              __nv_bfloat16* __restrict__ out, int N, int K) {
+  const long chunks = long(N) * (K / 8);
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < chunks; i += long(gridDim.x) * blockDim.x) {
+    const int r = int(i / (K / 8));
+    const int c = int(i % (K / 8));
+    const int kb = c >> 3, cc = c & 7, nb = r >> 8, rr = r & 255;
+    const size_t dst = ((size_t(nb) * (K >> 6) + kb) * 256 + rr) * 64 + (size_t(cc ^ (rr & 7)) << 3);
+    *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(w + size_t(r) * ldw + c * 8);
   }
 }
 
 }  // namespace hp
 
 using namespace hp;
+
+extern "C" int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream) {
+  HP_CHECK_ARG(w && out && w != out, "hp_tile_weight: bad pointers (in place not supported)");
+  HP_CHECK_ARG(N % 256 == 0 && K % 64 == 0 && ldw >= K && ldw % 8 == 0, "hp_tile_weight: N % 256, K % 64");
+  const long chunks = long(N) * (K / 8);
+  const int grid = int(std::min<long>((chunks + 255) / 256, 148L * 16));
+  k_tile_weight<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(w), ldw, static_cast<__nv_bfloat16*>(out), N, K);
+  HP_LAUNCH_CHECK("k_tile_weight");
+  return HP_OK;
+}
 
 extern "C" int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out, int ldo, int rows,
                           int cols, float eps, int max_ctas, void* stream) {

@@ -1,0 +1,215 @@
+"""B200Executor: the reference's device seam, executed on hardware.
+
+Implements the `GroundTruthOracle` protocol (reference engine.py:159-208):
+
+  prefill_layer_s(es)   one prefill layer over es.prefill_lens on
+                        es.prefill_sms SMs, with the decode side of `es`
+                        running concurrently on es.decode_sms SMs
+  decode_step_s(es)     one decode step (all model layers) for
+                        es.decode_ctx_lens on es.decode_sms SMs, with the
+                        prefill side of `es` running concurrently
+  alpha(phase, sms, tokens)        measured / SRM at a canonical shape
+  contention_bw(sms, prefill_len)  HBM bandwidth of `sms` SMs next to a
+                                   prefill on the remaining SMs
+
+so `engine.run(cfg, trace, oracle=B200Executor(...))` drives the
+reference's event loop with CUDA-event measurements of the real kernels
+confined to green-context partitions (PartitionPool) instead of the
+synthetic surfaces.  Decisions, queueing and reports stay the reference's.
+
+Every layer of a decode step has identical cost, so a step is measured as
+one decode layer (queued ahead of the timer, so host launch latency is
+excluded) times `model.num_layers`; the prefill side likewise measures one
+layer.  The kernels run on a resident random-init layer; K/V for arbitrary
+decode batches come from a page pool addressed modulo its size (the bytes
+streamed are what the timing depends on).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from ..errors import InvalidArgumentError
+from ..perf_model import ExecutionState, GpuSpec, scaled_peaks, srm_decode_step_s, srm_prefill_layer_s
+from ..workload import ModelSpec
+from . import lib
+from .layer import PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch, decode_slots
+from .partition import DECODE, PREFILL, PartitionPool
+
+
+def _ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+class B200Executor:
+    def __init__(self, model: ModelSpec, gpu: GpuSpec, device: int = 0, seed: int = 0,
+                 max_prefill_tokens: int = 32768, max_decode_batch: int = 256,
+                 pool_tokens: int = 1 << 21, sm_step: int = 8, pool: PartitionPool | None = None):
+        if model.head_dim not in (64, 128):
+            raise InvalidArgumentError("B200Executor supports head_dim 64 or 128")
+        self.model = model
+        self.gpu = gpu
+        self.dev = torch.device("cuda", device)
+        torch.cuda.set_device(self.dev)
+        self.pool = pool or PartitionPool(device, granularity=max(8, sm_step))
+        if gpu.num_sms != self.pool.n:
+            raise InvalidArgumentError(
+                f"GpuSpec has {gpu.num_sms} SMs but the device has {self.pool.n}; "
+                "use perf_model.b200_spec() (or [gpu] num_sms = 148)")
+        gen = torch.Generator(device="cpu")
+        gen.manual_seed(seed)
+        self.layer = DeviceLayer(model, LayerWeights.random(model, self.dev, gen), self.dev,
+                                 max_pos=max(max_prefill_tokens, 1 << 15) + 1)
+        h = model.hidden
+        bf = dict(dtype=torch.bfloat16, device=self.dev)
+        self.max_prefill_tokens = max_prefill_tokens
+        self.px = torch.randn(max_prefill_tokens, h, generator=gen).to(**bf)
+        self.py = torch.empty_like(self.px)
+        self.psc = PrefillScratch(model, max_prefill_tokens, self.dev)
+        self.pcache = KVCache(-(-max_prefill_tokens // PAGE), model.num_kv_heads, model.head_dim, self.dev)
+        self.pool_blocks = max(1, pool_tokens // PAGE)
+        self.dcache = KVCache(self.pool_blocks, model.num_kv_heads, model.head_dim, self.dev)
+        self.max_decode_batch = max_decode_batch
+        self.dx = torch.randn(max_decode_batch, h, generator=gen).to(**bf)
+        self.dy = torch.empty_like(self.dx)
+        self.dsc = DecodeScratch(model, max_decode_batch, 1024, self.dev, max_ctas=self.pool.n)
+        self.calls = {"prefill": 0, "decode": 0}
+
+    # ------------------------------------------------------------ workloads
+    def _prefill_args(self, lens):
+        lens = [int(x) for x in lens]
+        T = sum(lens)
+        if T > self.max_prefill_tokens:
+            raise InvalidArgumentError(f"prefill of {T} tokens exceeds max_prefill_tokens")
+        cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0).tolist()), dtype=torch.int32, device=self.dev)
+        pos = torch.cat([torch.arange(L, dtype=torch.int32) for L in lens]).to(self.dev)
+        slots = torch.arange(T, dtype=torch.int32, device=self.dev)
+        return T, cu, len(lens), max(lens), pos, slots
+
+    def _decode_args(self, ctx_lens):
+        B = len(ctx_lens)
+        if B > self.max_decode_batch:
+            raise InvalidArgumentError(f"decode batch {B} exceeds max_decode_batch")
+        pages = [-(-int(c) // PAGE) for c in ctx_lens]
+        mp = max(pages)
+        bt = torch.zeros(B, mp, dtype=torch.int64)
+        nxt = 0
+        for i, p in enumerate(pages):
+            bt[i, :p] = (torch.arange(p) + nxt) % self.pool_blocks
+            nxt += p
+        bt = bt.to(torch.int32).to(self.dev)
+        ctx = torch.tensor([int(c) for c in ctx_lens], dtype=torch.int32, device=self.dev)
+        pos, slots = decode_slots(bt, ctx)
+        return B, ctx, bt, pos, slots
+
+    def _launch_prefill(self, ps, args):
+        T, cu, nseq, mx, pos, slots = args
+        self.layer.prefill(self.px[:T], self.py[:T], self.psc, cu, nseq, mx, pos, slots, self.pcache,
+                           ps.sms, ps.torch_stream)
+
+    def _launch_decode(self, ds, args):
+        B, ctx, bt, pos, slots = args
+        self.layer.decode(self.dx[:B], self.dy[:B], self.dsc, ctx, pos, slots, bt, self.dcache, ds.sms,
+                          ds.torch_stream)
+
+    # --------------------------------------------------------------- timing
+    def _measure(self, phase: str, es: ExecutionState) -> float:
+        """Seconds of one layer of `phase` under the co-execution state `es`."""
+        n = self.pool.n
+        pm = es.prefill_sms if es.prefill_lens else 0
+        dm = es.decode_sms if es.decode_ctx_lens else 0
+        ps, ds = self.pool.split(pm, dm)
+        pargs = self._prefill_args(es.prefill_lens) if ps is not None else None
+        dargs = self._decode_args(es.decode_ctx_lens) if ds is not None else None
+        main, other = (ps, ds) if phase == "prefill" else (ds, ps)
+        run_main = self._launch_prefill if phase == "prefill" else self._launch_decode
+        run_other = self._launch_decode if phase == "prefill" else self._launch_prefill
+        margs, oargs = (pargs, dargs) if phase == "prefill" else (dargs, pargs)
+        if main is None:
+            raise InvalidArgumentError(f"{phase} phase has no SMs in {es}")
+        ctrl = torch.cuda.current_stream(self.dev)
+        start = _ev()
+        a, b = _ev(), _ev()
+        torch.cuda._sleep(300_000)  # queue everything ahead of the timed region
+        start.record(ctrl)
+        main.torch_stream.wait_event(start)
+        if other is not None:
+            other.torch_stream.wait_event(start)
+            # keep the other phase busy for the whole measured layer
+            with torch.cuda.stream(other.torch_stream):
+                for _ in range(self._cover_count(phase, es)):
+                    run_other(other, oargs)
+        with torch.cuda.stream(main.torch_stream):
+            a.record(main.torch_stream)
+            run_main(main, margs)
+            b.record(main.torch_stream)
+        torch.cuda.synchronize(self.dev)
+        self.calls[phase] += 1
+        return a.elapsed_time(b) * 1e-3
+
+    def _cover_count(self, phase: str, es: ExecutionState) -> int:
+        """How many layers of the other phase overlap one layer of `phase`."""
+        p = srm_prefill_layer_s(es, self.model, self.gpu) if es.prefill_lens and es.prefill_sms else 0.0
+        d = (srm_decode_step_s(es, self.model, self.gpu) / self.model.num_layers
+             if es.decode_ctx_lens and es.decode_sms else 0.0)
+        if phase == "prefill":
+            return max(1, min(64, math.ceil(3.0 * p / max(d, 1e-9))))
+        return max(1, min(8, math.ceil(3.0 * d / max(p, 1e-9))))
+
+    # -------------------------------------------------------- oracle protocol
+    def prefill_layer_s(self, es: ExecutionState) -> float:
+        return self._measure("prefill", es)
+
+    def decode_step_s(self, es: ExecutionState) -> float:
+        return self.model.num_layers * self._measure("decode", es)
+
+    def hybrid_iteration_s(self, chunks, decode_ctx_lens, sms: int) -> float:
+        raise lib.HotPathError(
+            "hybrid (chunked-prefill) iterations need prefix-aware prefill attention "
+            "(prior_lens); not built yet -- SURVEY.md section 8(f) next #1")
+
+    def alpha(self, phase: str, sms: int, tokens: int) -> float:
+        """Measured / SRM at a canonical shape of `tokens` on `sms` SMs."""
+        if phase == "prefill":
+            T = max(1, min(int(tokens), self.max_prefill_tokens))
+            es = ExecutionState(prefill_lens=(T,), prefill_sms=sms)
+            return self.prefill_layer_s(es) / srm_prefill_layer_s(es, self.model, self.gpu)
+        from ..engine import canonical_decode_es
+
+        es = canonical_decode_es(int(tokens), sms)
+        if es.decode_batch > self.max_decode_batch:
+            raise InvalidArgumentError("canonical decode batch exceeds max_decode_batch")
+        return self.decode_step_s(es) / srm_decode_step_s(es, self.model, self.gpu)
+
+    def contention_bw(self, sms: int, co_prefill_len: int, nbytes: int = 1 << 30) -> float:
+        """HBM bytes/s a stream on `sms` SMs attains while a prefill layer of
+        `co_prefill_len` tokens runs on the other N - sms SMs."""
+        buf = getattr(self, "_bwbuf", None)
+        if buf is None or buf.numel() * 4 != nbytes:
+            buf = self._bwbuf = torch.ones(nbytes // 4, dtype=torch.float32, device=self.dev)
+            self._bwout = torch.zeros(4, device=self.dev)
+        n = self.pool.n
+        T = max(0, min(int(co_prefill_len), self.max_prefill_tokens))
+        if T > 0 and sms < n:
+            ps, ds = self.pool.split(n - sms, sms)
+        else:
+            ds, ps = self.pool.phase(DECODE, sms), None
+        ctrl = torch.cuda.current_stream(self.dev)
+        start, a, b = _ev(), _ev(), _ev()
+        torch.cuda._sleep(300_000)
+        start.record(ctrl)
+        if ps is not None:
+            ps.torch_stream.wait_event(start)
+            args = self._prefill_args([T])
+            with torch.cuda.stream(ps.torch_stream):
+                for _ in range(3):
+                    self._launch_prefill(ps, args)
+        ds.torch_stream.wait_event(start)
+        with torch.cuda.stream(ds.torch_stream):
+            a.record(ds.torch_stream)
+            lib.membw(buf, ds.sms, 1, self._bwout, stream=ds.torch_stream)
+            b.record(ds.torch_stream)
+        torch.cuda.synchronize(self.dev)
+        return nbytes / (a.elapsed_time(b) * 1e-3)

@@ -19,11 +19,14 @@ reference's oracle call stands for (engine.py:189-198).
 Data layout in HBM (bf16 unless noted):
   x / h / y          [T, hidden] residual stream (ping-pong, inputs untouched)
   qkv                [T, (Hq + 2 Hkv) d]  q | k | v column blocks
-  w_qkv              [(Hq + 2 Hkv) d, hidden]        torch [out, in]
-  w_o                [hidden, hidden]
-  w_ug               [2 I, hidden]  gate/up rows interleaved in 64-row blocks
-  w_down             [hidden, I]
-  kcache / vcache    [num_blocks, Hkv, page, d]  (page 64), zero-initialised
+  w_qkv              [(Hq + 2 Hkv) d, hidden]        torch [out, in], then tiled
+  w_o                [hidden, hidden]                 (hp_tile_weight: [N/256][K/64]
+  w_ug               [2 I, hidden]  gate/up rows       [256][64], 128B-swizzled, so
+                     interleaved in 64-row blocks      each GEMM tile is one
+  w_down             [hidden, I]                       contiguous bulk copy)
+  kcache / vcache    [num_blocks, Hkv, page, d] logical; stored per page as
+                     [d/64][page][64] with swizzled 16B chunks (lib.kv_pack);
+                     zero-initialised
   block_table int32  [B, max_pages];  ctx_lens int32 [B]
   rope table fp32    [max_pos, d]  (cos | sin)
 """
@@ -78,22 +81,23 @@ class LayerWeights:
             return (1.0 + 0.1 * torch.randn(h, generator=gen, device="cpu")).to(torch.bfloat16).to(device)
 
         gate, up = w(I, h), w(I, h)
-        return cls(w(model.qkv_out_dim, h), w(h, h), interleave_gate_up(gate, up), w(h, I),
-                   norm(), norm())
+        return cls.from_dense(w(model.qkv_out_dim, h), w(h, h), gate, up, w(h, I), norm(), norm())
+
+    @classmethod
+    def from_dense(cls, w_qkv, w_o, w_gate, w_up, w_down, attn_norm, mlp_norm):
+        """Row-major torch [out, in] device weights -> the resident layout:
+        gate/up interleaved, every matrix tiled for bulk-copy streaming."""
+        t = lib.tile_weight
+        out = cls(t(w_qkv), t(w_o), t(interleave_gate_up(w_gate, w_up)), t(w_down), attn_norm, mlp_norm)
+        torch.cuda.synchronize()
+        return out
 
     @classmethod
     def from_numpy(cls, device, w_qkv, w_o, w_gate, w_up, w_down, attn_norm, mlp_norm):
         def t(a):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16).to(device)
 
-        return cls(t(w_qkv), t(w_o), interleave_gate_up(t(w_gate), t(w_up)), t(w_down),
-                   t(attn_norm), t(mlp_norm))
-
-    def gate_up(self):
-        """De-interleave (for checkers)."""
-        I2, h = self.w_ug.shape
-        v = self.w_ug.view(-1, 2, 64, h)
-        return v[:, 0].reshape(I2 // 2, h), v[:, 1].reshape(I2 // 2, h)
+        return cls.from_dense(t(w_qkv), t(w_o), t(w_gate), t(w_up), t(w_down), t(attn_norm), t(mlp_norm))
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in

@@ -31,6 +31,7 @@ SIGNATURES = {
     "hp_partition_sms": (_i, [_p, _i, C.POINTER(_i)]),
     "hp_partition_destroy": (_i, [_p]),
     "hp_rmsnorm": (_i, [_p, _i, _p, _p, _i, _i, _i, _f, _i, _p]),
+    "hp_tile_weight": (_i, [_p, _i, _p, _i, _i, _p]),
     "hp_gemm": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
@@ -39,6 +40,8 @@ SIGNATURES = {
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_decode_attn": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _f, _p, _sz, _i, _p]),
     "hp_probe": (_i, [_i, _i, _i64, _p, _p]),
+    "hp_membw": (_i, [_p, _sz, _i, _i, _p, _p]),
+    "hp_membw2d": (_i, [_p, _i, _i, _i, _i, _p, _p]),
 }
 
 
@@ -109,7 +112,19 @@ def rmsnorm(x, weight, out, eps: float, max_ctas: int, stream=None) -> None:
                             eps, max_ctas, _stream(stream)), "hp_rmsnorm")
 
 
+def tile_weight(w, stream=None):
+    """Row-major [N, K] bf16 weight -> the tiled, pre-swizzled layout the GEMMs
+    stream with bulk copies (same shape/size; opaque element order)."""
+    import torch
+
+    N, K = w.shape
+    out = torch.empty_like(w, memory_format=torch.contiguous_format)
+    check(load().hp_tile_weight(_ptr(w), w.stride(0), _ptr(out), N, K, _stream(stream)), "hp_tile_weight")
+    return out
+
+
 def gemm(x, w, y, epilogue: int = EPI_STORE, resid=None, max_ctas: int = 148, stream=None) -> None:
+    """Y = epi(X . W^T) with `w` from tile_weight()."""
     T, K = x.shape
     N = w.shape[0]
     check(load().hp_gemm(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
@@ -123,6 +138,7 @@ def gemm_swap_ws_bytes(T: int, N: int, K: int, max_ctas: int) -> int:
 
 def gemm_swap(x, w, y, ws, counters, epilogue: int = EPI_STORE, resid=None,
               max_ctas: int = 148, stream=None) -> None:
+    """Decode GEMM (T <= 256), `w` from tile_weight()."""
     T, K = x.shape
     N = w.shape[0]
     check(load().hp_gemm_swap(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
@@ -159,6 +175,43 @@ def decode_attn(q, kcache, vcache, block_table, ctx_lens, out, Hq: int, Hkv: int
                                 Hkv, d, page, kcache.shape[0], scale, _ptr(ws),
                                 0 if ws is None else ws.numel() * ws.element_size(), max_ctas,
                                 _stream(stream)), "hp_decode_attn")
+
+
+def membw(src, ctas: int, method: int, out, stream=None) -> None:
+    check(load().hp_membw(_ptr(src), src.numel() * src.element_size(), ctas, method, _ptr(out),
+                          _stream(stream)), "hp_membw")
+
+
+def _kv_chunk_index(x5):
+    """Gather index swapping 16-byte chunk c of token row r with c ^ (r & 7)."""
+    import torch
+
+    nb, H, nh, P, _ = x5.shape[:5]
+    r = torch.arange(P, device=x5.device)
+    c = torch.arange(8, device=x5.device)
+    src = c[None, :] ^ (r[:, None] & 7)
+    return src[None, None, None, :, :, None].expand(nb, H, nh, P, 8, 8)
+
+
+def kv_pack(x):
+    """Logical K or V cache [blocks, Hkv, page, d] -> the device page layout
+    ([blocks, Hkv, d/64, page, 64] with 128B-swizzled chunks), returned as a
+    tensor of the same shape whose memory is in device order."""
+    import torch
+
+    nb, H, P, d = x.shape
+    v = x.reshape(nb, H, P, d // 64, 8, 8).permute(0, 1, 3, 2, 4, 5)
+    return torch.gather(v, 4, _kv_chunk_index(v)).contiguous().view(nb, H, P, d)
+
+
+def kv_unpack(y):
+    """Inverse of kv_pack."""
+    import torch
+
+    nb, H, P, d = y.shape
+    v = y.reshape(nb, H, d // 64, P, 8, 8)
+    v = torch.gather(v, 4, _kv_chunk_index(v))
+    return v.permute(0, 1, 3, 2, 4, 5).contiguous().view(nb, H, P, d)
 
 
 def probe(out, ctas: int, threads: int = 128, spin_ns: int = 20000, stream=None) -> None:
@@ -208,8 +261,6 @@ class Partition:
             load().hp_partition_destroy(self._h)
             self._h = None
 
-    def __del__(self):  # pragma: no cover - interpreter shutdown order
-        try:
-            self.close()
-        except Exception:
-            pass
+    # No __del__: destroying a green context while torch still holds events or
+    # cached streams on it aborts at interpreter exit; partitions live for the
+    # process unless close() is called explicitly.

@@ -37,7 +37,8 @@ class DeviceModel:
         bf = dict(dtype=torch.bfloat16, device=device)
         self.embed = embed if embed is not None else torch.randn(vocab, h, generator=gen).to(**bf)
         self.final_norm = final_norm if final_norm is not None else torch.ones(h, **bf)
-        self.lm_head = lm_head if lm_head is not None else (torch.randn(vocab, h, generator=gen) * 0.05).to(**bf)
+        lm_head = lm_head if lm_head is not None else (torch.randn(vocab, h, generator=gen) * 0.05).to(**bf)
+        self.lm_head = lib.tile_weight(lm_head)  # streamed by the GEMMs as bulk tiles
         self.caches = [KVCache(num_blocks, model.num_kv_heads, model.head_dim, device)
                        for _ in range(model.num_layers)]
         self.psc = PrefillScratch(model, max_prefill_tokens, device)

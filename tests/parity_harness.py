@@ -9,8 +9,9 @@ greedy decode steps for all 9 sequences, and the same computation in the
 numpy oracle (oracle/numerics.py, bf16 rounding at the kernel boundaries).
 
 Tolerances (stated here, asserted by the callers):
-  hidden states  |dev - ref| <= ATOL + RTOL |ref|  with ATOL = 2e-2, RTOL = 1e-2
-                 (bf16 storage: one ulp at |x| in [4, 8) is 3.1e-2)
+  hidden states  |dev - ref| <= ATOL max(1, rms(ref)) + RTOL |ref|  with
+                 ATOL = 2e-2, RTOL = 1e-2 (see `excess`; bf16 storage: one ulp
+                 at |x| in [4, 8) is 3.1e-2)
   greedy tokens  identical at every step (teacher-forced on the oracle's
                  token, so one near-tie cannot cascade); a difference is
                  tolerated only where the oracle's top-2 logit margin is
@@ -40,6 +41,19 @@ PAGE = 64
 
 def _bf(x):
     return O.bf16_round(np.asarray(x, dtype=np.float32))
+
+
+def excess(dev, ref) -> float:
+    """Normalised tolerance excess: max(|dev-ref| - RTOL|ref|) / max(1, rms(ref)).
+    Passing means <= ATOL, i.e. |dev-ref| <= ATOL*max(1, rms(ref)) + RTOL*|ref|
+    everywhere: the absolute term scales with the tensor's RMS because
+    bf16 rounding differences at the stored intermediates (e.g. SwiGLU
+    activations reaching ~25 in a Llama-3-8B layer) propagate in proportion
+    to activation scale."""
+    dev = np.asarray(dev, np.float32)
+    ref = np.asarray(ref, np.float32)
+    scale = max(1.0, float(np.sqrt(np.mean(ref.astype(np.float64) ** 2))))
+    return float(np.max(np.abs(dev - ref) - RTOL * np.abs(ref))) / scale
 
 
 def tiny_weights(seed: int, vocab: int = 1024):
@@ -133,10 +147,7 @@ def run_tiny(seed: int = 0, decode_steps: int = 16, device: int = 0) -> dict:
         ref_last[i] = x[-1]
 
     out = {"prefill_tokens": int(len(tokens)), "nseq": nseq}
-    errs = []
-    for li in range(m.num_layers):
-        diff = np.abs(dev_hidden[li] - ref_hidden[li])
-        errs.append(float(np.max(diff - RTOL * np.abs(ref_hidden[li]))))
+    errs = [excess(dev_hidden[li], ref_hidden[li]) for li in range(m.num_layers)]
     out["prefill_max_abs"] = [float(np.max(np.abs(dev_hidden[li] - ref_hidden[li])))
                               for li in range(m.num_layers)]
     out["prefill_excess"] = max(errs)  # <= ATOL required
@@ -171,7 +182,7 @@ def run_tiny(seed: int = 0, decode_steps: int = 16, device: int = 0) -> dict:
         x = embed[cur]
         for li, W in enumerate(Wl):
             x = O.layer_decode(x, W, Hq, Hkv, d, ctx, table, kc[li], vc[li], bt, bf16_boundaries=True)
-        step_err.append(float(np.max(np.abs(dh - x) - RTOL * np.abs(x))))
+        step_err.append(excess(dh, x))
         rt, mg, lg = O.greedy_tokens(x, final_norm, lm_head)
         score(rt, dl.argmax(-1), mg, lg)
         cur = rt.astype(np.int32)
@@ -218,8 +229,7 @@ def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, dev
                 t(np.arange(T), torch.int32), t(np.arange(T), torch.int32), cache, sms)
     ref, _, _ = O.layer_prefill(x, W, Hq, Hkv, d, np.arange(T), table, bf16_boundaries=True)
     dy = y.float().cpu().numpy()
-    res = {"prefill_max_abs": float(np.max(np.abs(dy - ref))),
-           "prefill_excess": float(np.max(np.abs(dy - ref) - RTOL * np.abs(ref)))}
+    res = {"prefill_max_abs": float(np.max(np.abs(dy - ref))), "prefill_excess": excess(dy, ref)}
     # decode: B sequences with random cache contents, one new token each
     pages = -(-(ctx) // PAGE)
     nblk = B * pages + 3
@@ -229,8 +239,10 @@ def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, dev
     ctxs = np.array([ctx - 7 * i for i in range(B)], dtype=np.int32)
     xd = _bf(rng.normal(size=(B, h)))
     dcache = KVCache(nblk, Hkv, d, dev)
-    dcache.k.copy_(t(kc))
-    dcache.v.copy_(t(vc))
+    from paper_2504_19516_b200.device import lib
+
+    dcache.k.copy_(lib.kv_pack(t(kc)))
+    dcache.v.copy_(lib.kv_pack(t(vc)))
     ctx_t, bt_t = t(ctxs, torch.int32), t(bt, torch.int32)
     pos, slots = decode_slots(bt_t, ctx_t)
     yd = torch.empty(B, h, dtype=torch.bfloat16, device=dev)
@@ -238,9 +250,9 @@ def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, dev
     refd = O.layer_decode(xd, W, Hq, Hkv, d, ctxs, table, kc, vc, bt, bf16_boundaries=True)
     dyd = yd.float().cpu().numpy()
     res["decode_max_abs"] = float(np.max(np.abs(dyd - refd)))
-    res["decode_excess"] = float(np.max(np.abs(dyd - refd) - RTOL * np.abs(refd)))
+    res["decode_excess"] = excess(dyd, refd)
     # the new tokens' K/V landed in the cache slots
-    kdev = dcache.k.float().cpu().numpy()
+    kdev = lib.kv_unpack(dcache.k).float().cpu().numpy()
     res["kv_write_max_abs"] = float(max(np.max(np.abs(kdev[bt[b, (c - 1) // PAGE], :, (c - 1) % PAGE] -
                                                       kc[bt[b, (c - 1) // PAGE], :, (c - 1) % PAGE]))
                                         for b, c in enumerate(ctxs)))

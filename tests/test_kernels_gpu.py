@@ -39,12 +39,12 @@ def gen():
 
 
 # ------------------------------------------------------------------- GEMM
-@pytest.mark.parametrize("T,N,K", [(128, 256, 256), (200, 384, 512), (1024, 6144, 4096),
+@pytest.mark.parametrize("T,N,K", [(128, 256, 256), (200, 768, 512), (1024, 6144, 4096),
                                    (77, 4096, 4096), (4096, 1024, 1024)])
 def test_gemm_store(T, N, K, gen):
     x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
-    lib.gemm(x, w, y, lib.EPI_STORE, max_ctas=148)
+    lib.gemm(x, lib.tile_weight(w),y, lib.EPI_STORE, max_ctas=148)
     ref = x.float() @ w.float().T
     torch.cuda.synchronize()
     assert rel_err(y, ref) < 1e-2
@@ -55,7 +55,7 @@ def test_gemm_grid_sizes(max_ctas, gen):
     T, N, K = 300, 512, 640
     x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
-    lib.gemm(x, w, y, lib.EPI_STORE, max_ctas=max_ctas)
+    lib.gemm(x, lib.tile_weight(w),y, lib.EPI_STORE, max_ctas=max_ctas)
     assert rel_err(y, x.float() @ w.float().T) < 1e-2
 
 
@@ -63,11 +63,11 @@ def test_gemm_resid(gen):
     T, N, K = 333, 4096, 1024
     x, w, r = bf((T, K), gen=gen), bf((N, K), 0.05, gen), bf((T, N), gen=gen)
     y = torch.empty_like(r)
-    lib.gemm(x, w, y, lib.EPI_RESID, resid=r)
+    lib.gemm(x, lib.tile_weight(w),y, lib.EPI_RESID, resid=r)
     assert rel_err(y, x.float() @ w.float().T + r.float()) < 1e-2
     # in place (out aliases the residual), as the layer uses it
     r2 = r.clone()
-    lib.gemm(x, w, r2, lib.EPI_RESID, resid=r2)
+    lib.gemm(x, lib.tile_weight(w),r2, lib.EPI_RESID, resid=r2)
     assert rel_err(r2, x.float() @ w.float().T + r.float()) < 1e-2
 
 
@@ -88,7 +88,7 @@ def test_gemm_silu(T, gen):
     w, g, u = interleave_ref(N2, K, gen)
     x = bf((T, K), gen=gen)
     y = torch.empty(T, N2, device=DEV, dtype=torch.bfloat16)
-    lib.gemm(x, w, y, lib.EPI_SILU)
+    lib.gemm(x, lib.tile_weight(w),y, lib.EPI_SILU)
     ref = silu_ref(x.float() @ g.float().T) * (x.float() @ u.float().T)
     assert rel_err(y, ref) < 2e-2
 
@@ -100,20 +100,20 @@ def _ws(N, T, K, ctas):
     return ws, cnt
 
 
-@pytest.mark.parametrize("T,N,K,ctas", [(1, 128, 256, 1), (8, 6144, 4096, 148), (32, 4096, 4096, 64),
+@pytest.mark.parametrize("T,N,K,ctas", [(1, 256, 256, 1), (8, 6144, 4096, 148), (32, 4096, 4096, 64),
                                         (32, 4096, 4096, 32), (33, 1024, 1024, 7), (100, 512, 2048, 148),
                                         (256, 256, 512, 3), (32, 28672, 4096, 148)])
 def test_gemm_swap_store(T, N, K, ctas, gen):
     x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
     ws, cnt = _ws(N, T, K, ctas)
-    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
+    lib.gemm_swap(x, lib.tile_weight(w),y, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
     assert rel_err(y, x.float() @ w.float().T) < 1e-2
     # arrival counters are left clean for the next call
     torch.cuda.synchronize()
     assert cnt.abs().max().item() == 0
     y.zero_()
-    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
+    lib.gemm_swap(x, lib.tile_weight(w),y, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
     assert rel_err(y, x.float() @ w.float().T) < 1e-2
 
 
@@ -124,12 +124,12 @@ def test_gemm_swap_resid_silu(ctas, gen):
     w = bf((4096, K), 0.05, gen)
     ws, cnt = _ws(4096, T, K, ctas)
     y = r.clone()
-    lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_RESID, resid=y, max_ctas=ctas)
+    lib.gemm_swap(x, lib.tile_weight(w),y, ws, cnt, lib.EPI_RESID, resid=y, max_ctas=ctas)
     assert rel_err(y, x.float() @ w.float().T + r.float()) < 1e-2
     wi, g, u = interleave_ref(1024, K, gen)
     ws2, cnt2 = _ws(2048, T, K, ctas)
     y2 = torch.empty(T, 1024, device=DEV, dtype=torch.bfloat16)
-    lib.gemm_swap(x, wi, y2, ws2, cnt2, lib.EPI_SILU, max_ctas=ctas)
+    lib.gemm_swap(x, lib.tile_weight(wi), y2, ws2, cnt2, lib.EPI_SILU, max_ctas=ctas)
     ref = silu_ref(x.float() @ g.float().T) * (x.float() @ u.float().T)
     assert rel_err(y2, ref) < 2e-2
 
@@ -174,6 +174,7 @@ def test_rope_kv_write(gen):
     assert rel_err(got[:, :Hq], q_ref) < 1e-2
     assert rel_err(got[:, Hq:Hq + Hkv], k_ref) < 1e-2
     blk, off = (slots // page).long(), (slots % page).long()
+    kc, vc = lib.kv_unpack(kc), lib.kv_unpack(vc)  # device page layout -> logical
     assert rel_err(kc[blk, :, off], k_ref) < 1e-2
     assert torch.equal(vc[blk, :, off].float(), v_ref)
 
@@ -242,7 +243,8 @@ def test_decode_attn(ctx, Hq, Hkv, d, max_ctas, gen):
     ctx_t = torch.tensor(ctx, device=DEV, dtype=torch.int32)
     ws = torch.empty(lib.decode_attn_ws_bytes(B, Hq, d, 256) // 4, device=DEV, dtype=torch.float32)
     scale = 1.0 / math.sqrt(d)
-    lib.decode_attn(q, kc, vc, bt, ctx_t, out, Hq, Hkv, d, page, scale, ws=ws, max_ctas=max_ctas)
+    lib.decode_attn(q, lib.kv_pack(kc), lib.kv_pack(vc), bt, ctx_t, out, Hq, Hkv, d, page, scale,
+                    ws=ws, max_ctas=max_ctas)
     for b, c in enumerate(ctx):
         np_ = -(-c // page)
         blocks = bt[b, :np_].long()
