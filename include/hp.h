@@ -89,6 +89,14 @@ int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream
  * (workload.py:162-210) at phase "prefill". */
 int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
             int ldr, int T, int N, int K, int epilogue, int max_ctas, void* stream);
+/* Same, recording per-CTA {smid, start_ns, end_ns} into cta_times[grid][3]
+ * (config-3 wave measurement: measured idle = 1 - sum(busy) / (n * span),
+ * against wave_stats(hp_gemm_tiles(T, N), 1, n), perf_model.py:157-169). */
+int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
+                   int ldr, int T, int N, int K, int epilogue, int max_ctas, uint64_t* cta_times,
+                   void* stream);
+/* Output tiles (persistent-grid work units) of hp_gemm for T tokens, N features. */
+int hp_gemm_tiles(int T, int N);
 
 /* Swap-AB stream-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
  * hp_gemm; W streams through UMMA-M and the (tile, k-block) space is split

@@ -38,6 +38,7 @@ constexpr int DA_CONSUMERS = 8;
 constexpr int DA_THREADS = (DA_CONSUMERS + 1) * 32;
 constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;  // 64 rows x 128 B
 constexpr int DA_PROW = 72;                          // padded P^T row (bf16)
+constexpr int DA_WIN = 256;                          // block-table window (pages per unit)
 
 template <int D>
 struct DaCfg {
@@ -47,7 +48,8 @@ struct DaCfg {
   static constexpr int CB = 8 * D + 16;                         // per-warp merge buffer (floats)
   static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES +
                                  DA_CONSUMERS * CB * sizeof(float) +
-                                 DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * STAGES * 8 + 64 + 16;
+                                 DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * STAGES * 8 + 64 + 64 +
+                                 2 * DA_WIN * sizeof(int);
 };
 
 struct DecodeParams {
@@ -95,19 +97,21 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   uint64_t* empty = full + STAGES;
   // Tiles are consumed round-robin by 8 warps from a ring of STAGES slots, so
   // a warp can reach a slot more than one phase ahead of the producer, where
-  // a parity wait would be ambiguous.  Consumers first wait until the
-  // producer has issued their tile (which implies the slot's previous
-  // occupant was released), then wait on the slot's parity.
-  volatile uint32_t* issued = reinterpret_cast<volatile uint32_t*>(empty + STAGES);
+  // a parity wait would be ambiguous.  Consumers first wait until the slot's
+  // tag names their tile (set once the producer passed the slot's empty
+  // barrier for it, i.e. the previous occupant was released), then wait on
+  // the slot's parity.
+  volatile uint32_t* tag = reinterpret_cast<volatile uint32_t*>(empty + STAGES);
+  int* win = reinterpret_cast<int*>(const_cast<uint32_t*>(tag) + 16);  // [2][DA_WIN] page ids
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2 * C::NBOX);  // one arrive per K/V box (issued by separate lanes)
       mbar_init(&empty[s], 1);
+      tag[s] = 0xffffffffu;
     }
-    *issued = 0;
     fence_barrier_init();
   }
   __syncthreads();
@@ -118,66 +122,57 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
 
   if (warp == DA_CONSUMERS) {
     // ------------------------------------------------------------ producer
-    // Lane j holds the block id of page (window_first + j); the next unit's
-    // context length and first window are loaded one unit ahead.
+    // One thread's async-copy stream is serialised at ~one DRAM latency per
+    // copy, so every 8 KB box of a tile is issued by its own lane: lane =
+    // slot * PARTS + part, where `slot` takes every SLOTS-th tile of the
+    // unit (SLOTS <= STAGES keeps every parity wait unambiguous) and `part`
+    // is one K or V box.  The unit's block-table pages are staged in a
+    // double-buffered smem window, loaded one unit ahead.
+    constexpr int PARTS = 2 * C::NBOX;
+    constexpr int SLOTS = (32 / PARTS) < STAGES ? (32 / PARTS) : STAGES;
+    const int slot = lane / PARTS, part = lane % PARTS;
+    const bool issuer = slot < SLOTS;
     const uint64_t pol = l2_policy_evict_first();  // KV is read once per step
     uint32_t gtile = 0;
-    int u = blockIdx.x;
-    int ctx_cur = 0, blk_cur = 0;
-    if (u < total) {
+    int wb = 0;
+    auto load_window = [&](int u, int buf) -> int {  // returns ctx of unit u
       const UnitId id = unit_of(p, u);
-      ctx_cur = p.ctx_lens[id.b];
-      const int pg = (id.s * p.tps) / page_tiles + lane;
-      blk_cur = pg < p.max_pages ? p.block_table[size_t(id.b) * p.max_pages + pg] : 0;
-    }
+      const int ctx = p.ctx_lens[id.b];
+      const int first = (id.s * p.tps) / page_tiles;
+      const int last = min(p.max_pages, ((id.s + 1) * p.tps + page_tiles - 1) / page_tiles);
+      for (int j = lane; j < last - first; j += 32)
+        win[buf * DA_WIN + j] = p.block_table[size_t(id.b) * p.max_pages + first + j];
+      return ctx;
+    };
+    int u = blockIdx.x;
+    int ctx_cur = u < total ? load_window(u, 0) : 0;
     for (; u < total; u += gridDim.x) {
       const UnitId id = unit_of(p, u);
-      const int un = u + gridDim.x;
-      int ctx_nxt = 0, blk_nxt = 0;
-      if (un < total) {  // prefetch: consumed only at the next iteration
-        const UnitId nid = unit_of(p, un);
-        ctx_nxt = p.ctx_lens[nid.b];
-        const int pg = (nid.s * p.tps) / page_tiles + lane;
-        blk_nxt = pg < p.max_pages ? p.block_table[size_t(nid.b) * p.max_pages + pg] : 0;
-      }
+      __syncwarp();
+      const int ctx_nxt = (u + int(gridDim.x) < total) ? load_window(u + gridDim.x, wb ^ 1) : 0;
       const int ntiles = (ctx_cur + DA_TILE - 1) / DA_TILE;
       const int t0 = id.s * p.tps;
       const int t1 = min(ntiles, t0 + p.tps);
-      if (t0 < t1) {
-        const int* bt = p.block_table + size_t(id.b) * p.max_pages;
-        int win_first = t0 / page_tiles;  // first page covered by blk_cur
-        int blk_win = blk_cur;
-        for (int t = t0; t < t1; ++t) {
-          const int pg = t / page_tiles;
-          if (pg >= win_first + 32) {  // slide the window (> 32 pages per unit)
-            win_first += 32;
-            const int pj = win_first + lane;
-            blk_win = pj < p.max_pages ? bt[pj] : 0;
-          }
-          const int blk = __shfl_sync(0xffffffffu, blk_win, pg - win_first);
-          if (lane == 0) {
-            const uint32_t g = gtile + (t - t0);
-            const int st = g % STAGES;
-            const uint32_t ph = (g / STAGES) & 1;
-            const size_t base = (size_t(blk) * p.Hkv + id.kvh) * C::NBOX * page_elems +
-                                size_t(t % page_tiles) * DA_TILE * 64;
-            mbar_wait(&empty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
-            uint8_t* sb = ring + st * C::STAGE_BYTES;
-#pragma unroll
-            for (int bx = 0; bx < C::NBOX; ++bx) {
-              const size_t off = (base + bx * page_elems) * 2;
-              bulk_load_hint(sb + bx * DA_BOX_BYTES, p.kc + off, DA_BOX_BYTES, &full[st], pol);
-              bulk_load_hint(sb + (C::NBOX + bx) * DA_BOX_BYTES, p.vc + off, DA_BOX_BYTES, &full[st], pol);
-            }
-            *issued = g + 1;
-          }
-          __syncwarp();
+      if (issuer && t0 < t1) {
+        const int first = t0 / page_tiles;
+        for (int t = t0 + slot; t < t1; t += SLOTS) {
+          const int blk = win[wb * DA_WIN + t / page_tiles - first];
+          const uint32_t g = gtile + (t - t0);
+          const int st = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          const size_t base = (size_t(blk) * p.Hkv + id.kvh) * C::NBOX * page_elems +
+                              size_t(t % page_tiles) * DA_TILE * 64;
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&full[st], DA_BOX_BYTES);
+          const int bx = part % C::NBOX;
+          const uint8_t* src = (part < C::NBOX ? p.kc : p.vc) + (base + bx * page_elems) * 2;
+          bulk_load_hint(ring + st * C::STAGE_BYTES + part * DA_BOX_BYTES, src, DA_BOX_BYTES, &full[st], pol);
+          if (part == 0) tag[st] = g;
         }
-        gtile += t1 - t0;
       }
+      gtile += max(0, t1 - t0);
       ctx_cur = ctx_nxt;
-      blk_cur = blk_nxt;
+      wb ^= 1;
     }
     return;
   }
@@ -229,7 +224,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
         const uint32_t g = gtile + i;
         const int st = g % STAGES;
         const uint32_t ph = (g / STAGES) & 1;
-        while (*issued <= g) __nanosleep(64);
+        while (tag[st] != g) __nanosleep(32);
         mbar_wait(&full[st], ph);
         const uint32_t kb = smem_u32(ring + st * C::STAGE_BYTES);
         const uint32_t vb = kb + C::NBOX * DA_BOX_BYTES;
@@ -471,7 +466,7 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   const int pairs = B * Hkv;
   int tps = max_tiles;
   while (tps > 2 && pairs * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
-  p.tps = std::max(1, tps);
+  p.tps = std::max(1, std::min(tps, (DA_WIN - 1) * (page / DA_TILE)));  // unit pages fit the window
   p.max_splits = (max_tiles + p.tps - 1) / p.tps;
   if (p.max_splits > 1) {
     HP_CHECK_ARG(workspace != nullptr, "hp_decode_attn: workspace required for split contexts");
@@ -479,6 +474,8 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
       // not enough scratch for this split: fall back to fewer, longer splits
       const int ms = int(ws_bytes / (size_t(B) * Hq * (d + 2) * sizeof(float)));
       p.tps = ms <= 1 ? max_tiles : (max_tiles + ms - 1) / ms;
+      HP_CHECK_ARG(p.tps <= (DA_WIN - 1) * (page / DA_TILE),
+                   "hp_decode_attn: workspace too small to split this context");
       p.max_splits = (max_tiles + p.tps - 1) / p.tps;
     }
     p.ws_o = static_cast<float*>(workspace);

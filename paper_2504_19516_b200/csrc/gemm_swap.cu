@@ -162,21 +162,26 @@ __global__ void __launch_bounds__(192, 1)
   const int end = min(begin + p.ipc, p.total_iters);
 
   if (warp == 0) {
-    if (lane == 0) {
+    // Producer: the async-copy stream of a single issuing thread is
+    // effectively serialised (~one DRAM latency per copy), so PL lanes each
+    // own every PL-th stage -- PL copies in flight from independent threads.
+    constexpr int PL = STAGES < 8 ? STAGES : 8;
+    if (lane < PL) {
       const uint64_t w_policy = l2_policy_evict_first();  // weights: read once per step
-      int stage = 0;
-      uint32_t phase = 0;
+      uint32_t g = 0;
       int it = begin;
       Seg s;
       while (next_seg(p, it, end, s)) {
         const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
-        for (int kb = s.kb0; kb < s.kb1; ++kb) {
+        for (int kb = s.kb0; kb < s.kb1; ++kb, ++g) {
+          if (int(g % PL) != lane) continue;
+          const int stage = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           bulk_load_hint(sA + stage * C::A_BYTES, p.w + wtile_offset(mt * SBM, kb, p.K), C::A_BYTES,
                          &full[stage], w_policy);
           tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }

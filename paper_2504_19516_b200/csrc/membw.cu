@@ -115,20 +115,28 @@ __global__ void __launch_bounds__(128) k_membw_tma2d(const __grid_constant__ CUt
 // method 10+k: single-thread bulk-copy stream with chunk = (4 KB << k) and
 // as many stages as fit in 192 KB -- isolates the copy engine's per-SM
 // throughput from any consumer work.
-__global__ void __launch_bounds__(32) k_membw_bulk(const uint8_t* __restrict__ src, size_t bytes,
-                                                   uint32_t chunk, float* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_membw_bulk(const uint8_t* __restrict__ src, size_t bytes,
+                                                    uint32_t chunk, int spin, float* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  const int nst = int((192u * 1024u) / chunk);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 192 * 1024);
-  if (threadIdx.x != 0) return;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // spin >= 2: lanes 0..spin-1 of ONE warp issue independent rings (is the
+  // copy stream serialised per thread or per warp?)
+  const bool lanes_mode = spin >= 2;
+  const int nw = lanes_mode ? spin : int(blockDim.x / 32);
+  const int w = lanes_mode ? int(threadIdx.x) : int(threadIdx.x / 32);
+  if (lanes_mode ? threadIdx.x >= unsigned(spin) : (threadIdx.x & 31) != 0) return;
+  if (lanes_mode) spin = 0;
+  const int nst = int((192u * 1024u) / chunk) / nw;  // stages per issuing thread
+  uint8_t* smem = base + size_t(w) * nst * chunk;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + 192 * 1024) + w * 64;
   for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
   fence_barrier_init();
   const size_t nchunks = bytes / chunk;
-  const size_t my = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const size_t gw = size_t(gridDim.x) * nw, me = size_t(blockIdx.x) * nw + w;
+  const size_t my = nchunks > me ? (nchunks - me + gw - 1) / gw : 0;
   auto issue = [&](size_t k) {
     const int s = int(k % nst);
-    const size_t c = blockIdx.x + k * gridDim.x;
+    const size_t c = me + k * gw;
     mbar_arrive_expect_tx(&full[s], chunk);
     bulk_load(smem + size_t(s) * chunk, src + c * chunk, chunk, &full[s]);
   };
@@ -136,7 +144,20 @@ __global__ void __launch_bounds__(32) k_membw_bulk(const uint8_t* __restrict__ s
   uint32_t acc = 0;
   for (size_t k = 0; k < my; ++k) {
     const int s = int(k % nst);
-    mbar_wait(&full[s], uint32_t((k / nst) & 1));
+    if (spin) {
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}\n"
+            : "=r"(done)
+            : "r"(smem_u32(&full[s])), "r"(uint32_t((k / nst) & 1))
+            : "memory");
+      }
+    } else {
+      mbar_wait(&full[s], uint32_t((k / nst) & 1));
+    }
     acc ^= *reinterpret_cast<const uint32_t*>(smem + size_t(s) * chunk);
     if (k + nst < my) issue(k + nst);
   }
@@ -171,15 +192,21 @@ extern "C" int hp_membw(const void* src, size_t bytes, int ctas, int method, flo
   if (method == 0) {
     k_membw_ldg<<<ctas, 512, 0, st>>>(static_cast<const uint4*>(src), bytes / 16, out);
   } else if (method >= 10) {
-    const uint32_t chunk = 4096u << (method - 10);
-    HP_CHECK_ARG(chunk <= 64 * 1024 && bytes % chunk == 0, "hp_membw: bad bulk chunk");
-    const size_t smem = 192 * 1024 + 128 + 8 * 64;
+    // method = 10 + log2(chunk / 4 KB) + 8 * log2(issuing warps) + 64 * spin
+    // (spin 0: try_wait, 1: test_wait spin, k >= 2: k issuing lanes of one warp)
+    const int spin = (method - 10) / 64;
+    const int m = (method - 10) % 64;
+    const uint32_t chunk = 4096u << (m % 8);
+    const int warps = spin >= 2 ? 1 : 1 << (m / 8);
+    HP_CHECK_ARG(chunk <= 64 * 1024 && bytes % chunk == 0 && warps <= 8 &&
+                     (192u * 1024u) / chunk >= uint32_t(warps), "hp_membw: bad bulk config");
+    const size_t smem = 192 * 1024 + 128 + 8 * 64 * 8;
     static bool attr2 = false;
     if (!attr2) {
       HP_CUDA_TRY(cudaFuncSetAttribute(k_membw_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       attr2 = true;
     }
-    k_membw_bulk<<<ctas, 32, smem, st>>>(static_cast<const uint8_t*>(src), bytes, chunk, out);
+    k_membw_bulk<<<ctas, 32 * warps, smem, st>>>(static_cast<const uint8_t*>(src), bytes, chunk, spin, out);
   } else {
     HP_CHECK_ARG(bytes % MB_CHUNK == 0, "hp_membw: TMA path needs a multiple of 32 KB");
     const size_t smem = MB_STAGES * MB_CHUNK + 256;

@@ -33,6 +33,8 @@ SIGNATURES = {
     "hp_rmsnorm": (_i, [_p, _i, _p, _p, _i, _i, _i, _f, _i, _p]),
     "hp_tile_weight": (_i, [_p, _i, _p, _i, _i, _p]),
     "hp_gemm": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
+    "hp_gemm_traced": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
+    "hp_gemm_tiles": (_i, [_i, _i]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
@@ -130,6 +132,20 @@ def gemm(x, w, y, epilogue: int = EPI_STORE, resid=None, max_ctas: int = 148, st
     check(load().hp_gemm(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
                          _ptr(resid), resid.stride(0) if resid is not None else 0, T, N, K,
                          epilogue, max_ctas, _stream(stream)), "hp_gemm")
+
+
+def gemm_traced(x, w, y, cta_times, epilogue: int = EPI_STORE, resid=None, max_ctas: int = 148,
+                stream=None) -> None:
+    """hp_gemm that also records per-CTA {smid, start_ns, end_ns} (int64 [grid, 3])."""
+    T, K = x.shape
+    N = w.shape[0]
+    check(load().hp_gemm_traced(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0),
+                                _ptr(resid), resid.stride(0) if resid is not None else 0, T, N, K,
+                                epilogue, max_ctas, _ptr(cta_times), _stream(stream)), "hp_gemm_traced")
+
+
+def gemm_tiles(T: int, N: int) -> int:
+    return load().hp_gemm_tiles(T, N)
 
 
 def gemm_swap_ws_bytes(T: int, N: int, K: int, max_ctas: int) -> int:

@@ -1,4 +1,3 @@
-"""Per-SM bulk-copy throughput vs chunk size, issuing warps, wait mode."""
 import os
 import sys
 
@@ -29,13 +28,18 @@ def bw(st, method):
     return nbytes / t / 1e9 / st.sms
 
 
-for sms in (8, 32):
-    st = pool.phase(DECODE, sms)
-    for spin in (0, 1):
-        for wl in (0, 2):
-            line = f"sms {st.sms:3d} spin {spin} warps {1 << wl}:"
-            for k in (0, 1, 2, 3, 4):
-                if (192 * 1024) // (4096 << k) < (1 << wl):
-                    continue
-                line += f"  {4 << k:2d}KB {bw(st, 10 + k + 8 * wl + 64 * spin):6.1f}"
-            print(line, flush=True)
+st = pool.phase(DECODE, 16)
+for lanes in (2, 4, 8):
+    line = f"sms 16 lanes-in-one-warp {lanes}:"
+    for k in (0, 1, 2, 3):
+        if (192 * 1024) // (4096 << k) < lanes:
+            continue
+        line += f"  {4 << k:2d}KB {bw(st, 10 + k + 64 * lanes):6.1f}"
+    print(line, flush=True)
+for wl in (1, 3):
+    line = f"sms 16 warps {1 << wl}:"
+    for k in (0, 1, 2, 3):
+        if (192 * 1024) // (4096 << k) < (1 << wl):
+            continue
+        line += f"  {4 << k:2d}KB {bw(st, 10 + k + 8 * wl):6.1f}"
+    print(line, flush=True)

@@ -17,7 +17,7 @@ if which.startswith("swap"):
     if which == "swap_qkv":
         N = 6144
     x = torch.randn(T, K, device=DEV).to(torch.bfloat16)
-    w = (torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16)
+    w = lib.tile_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
     ws = torch.empty(lib.gemm_swap_ws_bytes(T, N, K, sms) // 4, device=DEV)
     cnt = torch.zeros(N // 128, device=DEV, dtype=torch.int32)
@@ -38,7 +38,7 @@ elif which == "decode_attn":
 elif which.startswith("gemm"):
     T = int(which[4:] or 4096)
     x = torch.randn(T, 4096, device=DEV).to(torch.bfloat16)
-    w = (torch.randn(28672, 4096, device=DEV) * 0.02).to(torch.bfloat16)
+    w = lib.tile_weight((torch.randn(28672, 4096, device=DEV) * 0.02).to(torch.bfloat16))
     y = torch.empty(T, 14336, device=DEV, dtype=torch.bfloat16)
     for _ in range(reps):
         lib.gemm(x, w, y, lib.EPI_SILU, max_ctas=sms)
