@@ -77,9 +77,9 @@ int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out, int ldo, i
                float eps, int max_ctas, void* stream);
 
 /* Weight layout conversion (one-time, at load): row-major W [N, K] ->
- * tiled [N/256][K/64][256][64] with the 128B-swizzle chunk permutation, so
- * every GEMM weight tile is one contiguous 16/32 KB run fetched by a single
- * bulk copy.  N % 256 == 0, K % 64 == 0; `out` holds N*K bf16. */
+ * tiled [N/128][K/128][2][128][64] with the 128B-swizzle chunk permutation,
+ * so every [128 x 128] weight tile is one contiguous 32 KB run fetched by a
+ * single bulk copy.  N % 128 == 0, K % 128 == 0; `out` holds N*K bf16. */
 int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream);
 
 /* Token-major tcgen05 GEMM (prefill): Y[T,N] = epi(X[T,K] . W[N,K]^T), W
@@ -144,6 +144,13 @@ int hp_membw(const void* src, size_t bytes, int ctas, int method, float* out, vo
 /* Same, through 2-D TMA boxes {64 bf16, box_rows} of a [rows, cols] bf16
  * matrix (the GEMM weight-stream access shape). */
 int hp_membw2d(const void* src, int rows, int cols, int box_rows, int ctas, float* out, void* stream);
+/* Producer/consumer copy pipeline (a GEMM mainloop without the MMA):
+ * `producers` issuing warps, one in-order consumer, chunk_kb KB stages. */
+int hp_membw_pipe(const void* src, size_t bytes, int ctas, int chunk_kb, int producers, float* out,
+                  void* stream);
+/* tcgen05.mma issue/completion rate: n MMAs (M=128, N=bn, K=16, smem
+ * operands) over `chains` accumulators; out[cta] = {issue cycles, done cycles}. */
+int hp_umma_rate(int n, int bn, int chains, int ctas, long long* out, void* stream);
 
 /* Per-CTA probe: out[i] = {smid, start_ns, end_ns} for `ctas` CTAs spinning
  * `spin_ns` each -- partition confinement (%smid) and measured idle. */

@@ -71,8 +71,13 @@ HP_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifndef HP_WAIT_MODE
+#define HP_WAIT_MODE 0
+#endif
+
 HP_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#if HP_WAIT_MODE == 0
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -82,6 +87,27 @@ HP_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       "DONE_%=:\n\t}\n" ::"r"(addr),
       "r"(parity)
       : "memory");
+#elif HP_WAIT_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
@@ -128,11 +154,13 @@ HP_DEVICE void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64
       : "memory");
 }
 
-// Byte offset of the (row-block, k-block) tile of a weight stored in the
-// tiled layout [N/256][K/64][256 rows][64 cols], each 16B chunk c of row r
-// at position c ^ (r & 7) (the SWIZZLE_128B pattern UMMA descriptors read).
+// Byte offset of the [128 rows x 64 k] sub-tile (rows row0.., k-block kb of
+// 64) of a weight stored in the tiled layout [N/128][K/128][2][128][64]:
+// each 16B chunk c of row r sits at position c ^ (r & 7) (the SWIZZLE_128B
+// pattern UMMA descriptors read), and the two 64-k halves of a 128 x 128
+// block are adjacent, so a decode GEMM stage is one contiguous 32 KB copy.
 HP_DEVICE size_t wtile_offset(int row0, int kb, int K) {
-  return (size_t(row0 >> 8) * (K >> 6) + kb) * (256 * 64 * 2) + size_t(row0 & 255) * 128;
+  return ((size_t(row0 >> 7) * (K >> 7) + (kb >> 1)) * 2 + (kb & 1)) * (128 * 64 * 2);
 }
 
 HP_DEVICE uint64_t l2_policy_evict_first() {

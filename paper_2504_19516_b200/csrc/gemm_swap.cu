@@ -17,8 +17,10 @@
 // blocks, so a 128-row tile yields 64 outputs).  Outputs are written through
 // a padded shared-memory transpose so stores along the feature dim coalesce.
 //
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM alloc + UMMA
-// issuer, warps 2..5 epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (288 threads): warps 0..3 copy producers (each owns every 4th
+// pipeline stage: one thread's async-copy stream is serialised at roughly one
+// memory latency per copy), warp 4 TMEM alloc + UMMA issuer, warps 5..8
+// epilogue (TMEM lane quarter = warp % 4).
 #include "common.cuh"
 #include "runtime.h"
 #include "../../include/hp.h"
@@ -30,16 +32,25 @@ namespace hp {
 namespace {
 
 constexpr int SBM = 128;
-constexpr int SBK = 64;
+constexpr int SBK = 128;  // k per pipeline stage: one contiguous 32 KB weight tile
 constexpr int VLD = 33;  // padded fp32 row of the epilogue transpose buffer
+constexpr int SW_PRODUCERS = 4;
+constexpr int SW_MMA = SW_PRODUCERS;
+constexpr int SW_THREADS = (SW_PRODUCERS + 5) * 32;
 
 template <int BN>
 struct SwapCfg {
   static constexpr uint32_t A_BYTES = SBM * SBK * 2;
   static constexpr uint32_t B_BYTES = BN * SBK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : (BN >= 64 ? 8 : 10));
-  static constexpr uint32_t TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
+  static constexpr int STAGES = BN >= 256 ? 2 : (BN >= 128 ? 3 : (BN >= 64 ? 4 : 5));
+  static constexpr int PL = STAGES < SW_PRODUCERS ? STAGES : SW_PRODUCERS;  // issuing warps
+  // independent accumulation chains: consecutive UMMAs into one TMEM
+  // accumulator serialise on its latency (~150 cycles at N=32), so k-steps
+  // rotate over NCH accumulators that the epilogue sums
+  static constexpr int NCH = BN <= 64 ? 4 : (BN == 128 ? 2 : 1);
+  static constexpr uint32_t ACC_COLS = NCH * BN;
+  static constexpr uint32_t TMEM_COLS = (2 * ACC_COLS <= 64) ? 64 : (2 * ACC_COLS <= 128 ? 128 : (2 * ACC_COLS <= 256 ? 256 : 512));
   static constexpr size_t VBUF = size_t(SBM) * VLD * 4;
   static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + VBUF + 256;
 };
@@ -74,6 +85,24 @@ __device__ __forceinline__ bool next_seg(const SwapParams& p, int& it, int end, 
 }
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+// Sum of the NCH accumulation chains (columns ch*BN apart) for 32 columns.
+template <int BN, int NCH>
+__device__ __forceinline__ void load_acc(uint32_t taddr, float* v) {
+  tmem_ld32(taddr, v);
+  if constexpr (NCH > 1) {
+    float w[32];
+#pragma unroll
+    for (int ch = 1; ch < NCH; ++ch) {
+      tmem_ld_wait();
+      tmem_ld32(taddr + ch * BN, w);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += w[j];
+    }
+  }
+  tmem_ld_wait();
+}
 
 // Epilogue-warp barrier (128 threads, named barrier 1).
 __device__ __forceinline__ void epi_sync() { named_bar_sync(1, 128); }
@@ -118,7 +147,7 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
 }  // namespace
 
 template <int BN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(SW_THREADS, 1)
     k_gemm_swap_sk(const __grid_constant__ CUtensorMap tmX,
                    const SwapParams p) {
   using C = SwapCfg<BN>;
@@ -149,7 +178,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) {
+  if (warp == SW_MMA) {
     tmem_alloc(tmem_slot, C::TMEM_COLS);
     tmem_relinquish();
   }
@@ -161,12 +190,10 @@ __global__ void __launch_bounds__(192, 1)
   const int begin = blockIdx.x * p.ipc;
   const int end = min(begin + p.ipc, p.total_iters);
 
-  if (warp == 0) {
-    // Producer: the async-copy stream of a single issuing thread is
-    // effectively serialised (~one DRAM latency per copy), so PL lanes each
-    // own every PL-th stage -- PL copies in flight from independent threads.
-    constexpr int PL = STAGES < 8 ? STAGES : 8;
-    if (lane < PL) {
+  if (warp < SW_PRODUCERS) {
+    constexpr int PL = C::PL;  // <= STAGES keeps parity waits unambiguous; extra warps idle
+    // warp-converged walk (uniform registers), one elected lane issues
+    {
       const uint64_t w_policy = l2_policy_evict_first();  // weights: read once per step
       uint32_t g = 0;
       int it = begin;
@@ -174,51 +201,66 @@ __global__ void __launch_bounds__(192, 1)
       while (next_seg(p, it, end, s)) {
         const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
         for (int kb = s.kb0; kb < s.kb1; ++kb, ++g) {
-          if (int(g % PL) != lane) continue;
+          if (int(g % PL) != warp) continue;
           const int stage = g % STAGES;
           const uint32_t phase = (g / STAGES) & 1;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          bulk_load_hint(sA + stage * C::A_BYTES, p.w + wtile_offset(mt * SBM, kb, p.K), C::A_BYTES,
-                         &full[stage], w_policy);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            // 128 rows x 128 k of W: one contiguous 32 KB run (two swizzled 64-k halves)
+            bulk_load_hint(sA + stage * C::A_BYTES, p.w + wtile_offset(mt * SBM, 2 * kb, p.K), C::A_BYTES,
+                           &full[stage], w_policy);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
+            tma_load_2d(sB + stage * C::B_BYTES + BN * 128, &tmX, &full[stage], kb * SBK + 64, nt * BN);
+          }
+          __syncwarp();
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(SBM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      int it = begin;
-      Seg s;
-      while (next_seg(p, it, end, s)) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+  } else if (warp == SW_MMA) {
+    // The whole warp walks the (warp-uniform) schedule so descriptors live in
+    // uniform registers; one elected lane issues.  A divergent single-lane
+    // issuer paid ~150 cycles of register shuffling per tcgen05.mma, which
+    // capped a 16 KB stage of four N=32 MMAs at ~55 GB/s per SM.
+    constexpr uint32_t idesc = umma_idesc_bf16(SBM, BN);
+    const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
+    const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sB));
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = begin;
+    Seg s;
+    while (next_seg(p, it, end, s)) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+      for (int kb = s.kb0; kb < s.kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = s.kb0; kb < s.kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+        const uint64_t ad = adesc0 + uint64_t((stage * C::A_BYTES) >> 4);
+        const uint64_t bd = bdesc0 + uint64_t((stage * C::B_BYTES) >> 4);
+        const bool first = kb == s.kb0;
+        if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < SBK / 16; ++k)
-            umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                      (kb > s.kb0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < SBK / 16; ++k)  // k-steps of 16: 4 per 64-k swizzled half
+            umma_bf16(d_tmem + (k % C::NCH) * BN, ad + (k >> 2) * (128 * 128 >> 4) + 2 * (k & 3),
+                      bd + (k >> 2) * (BN * 128 >> 4) + 2 * (k & 3), idesc,
+                      (!first || k >= C::NCH) ? 1u : 0u);
           umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int et = (warp - 2) * 32 + lane;
+    const int et = (warp - SW_MMA - 1) * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = begin;
@@ -230,13 +272,12 @@ __global__ void __launch_bounds__(192, 1)
       const bool single = first == last;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * C::ACC_COLS;
       if (single) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
-          tmem_ld32(taddr + c * 32, v);
-          tmem_ld_wait();
+          load_acc<BN, C::NCH>(taddr + c * 32, v);
           if (c == BN / 32 - 1) {
             tc_fence_before();
             __syncwarp();
@@ -254,8 +295,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
-          tmem_ld32(taddr + c * 32, v);
-          tmem_ld_wait();
+          load_acc<BN, C::NCH>(taddr + c * 32, v);
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4*>(mine + c * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -312,7 +352,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == SW_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
@@ -327,7 +367,7 @@ static int launch_swap(const CUtensorMap& tx, const SwapParams& p, int grid,
     HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_swap_sk<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     attr_set = true;
   }
-  k_gemm_swap_sk<BN><<<grid, 192, C::SMEM, st>>>(tx, p);
+  k_gemm_swap_sk<BN><<<grid, SW_THREADS, C::SMEM, st>>>(tx, p);
   HP_LAUNCH_CHECK("k_gemm_swap_sk");
   return HP_OK;
 }
@@ -355,9 +395,9 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
                             int max_ctas, void* stream) {
   HP_CHECK_ARG(X && W && Y, "hp_gemm_swap: null pointer");
   HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
-  HP_CHECK_ARG(N % 256 == 0, "hp_gemm_swap: N must be a multiple of 256 (tiled weight layout)");
+  HP_CHECK_ARG(N % 128 == 0, "hp_gemm_swap: N must be a multiple of 128 (tiled weight layout)");
   HP_CHECK_ARG(ldw == K, "hp_gemm_swap: W must be in the tiled layout (ldw == K)");
-  HP_CHECK_ARG(K % SBK == 0, "hp_gemm_swap: K must be a multiple of 64");
+  HP_CHECK_ARG(K % SBK == 0, "hp_gemm_swap: K must be a multiple of 128");
   HP_CHECK_ARG(epilogue >= HP_EPI_STORE && epilogue <= HP_EPI_SILU, "hp_gemm_swap: bad epilogue");
   HP_CHECK_ARG(epilogue != HP_EPI_RESID || R != nullptr, "hp_gemm_swap: residual epilogue needs R");
   HP_CHECK_ARG(max_ctas >= 1, "hp_gemm_swap: max_ctas must be >= 1");
@@ -389,7 +429,7 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
     HP_CHECK_ARG(n_counters >= p.m_tiles * p.n_tiles, "hp_gemm_swap: too few counters");
   }
   CUtensorMap tx;
-  int rc = cached_tmap_bf16(&tx, X, T, K, ldx, BN, SBK, true);
+  int rc = cached_tmap_bf16(&tx, X, T, K, ldx, BN, 64, true);  // two 64-k boxes per stage
   if (rc) return rc;
   const int g = (p.total_iters + p.ipc - 1) / p.ipc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

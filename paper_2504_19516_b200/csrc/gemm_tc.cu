@@ -125,60 +125,66 @@ __global__ void __launch_bounds__(192, 1)
   const int total = p.m_tiles * p.n_tiles * p.k_splits;
 
   if (warp == 0) {
-    // One issuing lane: operands are L2-resident here (activation tiles are
-    // re-read by every N tile, weights by every M tile), and a single
-    // in-order issue stream measured fastest (multi-lane issue cost ~5%).
-    constexpr int PL = 1;
-    if (lane < PL) {
-      uint32_t g = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const int tile = u / p.k_splits, ks = u % p.k_splits;
-        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
-        const int kb0 = ks * p.kb_per_split;
-        const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb, ++g) {
-          if (int(g % PL) != lane) continue;
-          const int stage = g % STAGES;
-          const uint32_t phase = (g / STAGES) & 1;
-          mbar_wait(&empty[stage], phase ^ 1);
+    // One in-order issue stream (operands are mostly L2-resident here:
+    // activation tiles are re-read by every N tile, weights by every M tile);
+    // the warp walks the schedule converged and one elected lane issues.
+    uint32_t g = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      const int tile = u / p.k_splits, ks = u % p.k_splits;
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int kb0 = ks * p.kb_per_split;
+      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        const int stage = g % STAGES;
+        const uint32_t phase = (g / STAGES) & 1;
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mt * BM);
-          bulk_load(sB + stage * C::B_BYTES, p.w + wtile_offset(nt * BN, kb, p.K), C::B_BYTES,
-                    &full[stage]);
+#pragma unroll
+          for (int h = 0; h < BN / 128; ++h)  // BN rows = BN/128 tiled 128-row blocks
+            bulk_load(sB + stage * C::B_BYTES + h * (128 * BK * 2),
+                      p.w + wtile_offset(nt * BN + h * 128, kb, p.K), 128 * BK * 2, &full[stage]);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        const int ks = u % p.k_splits;
-        const int kb0 = ks * p.kb_per_split;
-        const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // warp-converged schedule walk (descriptors in uniform registers); one
+    // elected lane issues the UMMAs
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
+    const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sB));
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      const int ks = u % p.k_splits;
+      const int kb0 = ks * p.kb_per_split;
+      const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+        const uint64_t ad = adesc0 + uint64_t((stage * C::A_BYTES) >> 4);
+        const uint64_t bd = bdesc0 + uint64_t((stage * C::B_BYTES) >> 4);
+        const bool first = kb == kb0;
+        if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (!first || k > 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -280,7 +286,7 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
                               uint64_t* cta_times, void* stream) {
   HP_CHECK_ARG(X && W && Y, "hp_gemm: null pointer");
   HP_CHECK_ARG(T >= 1 && N >= 1 && K >= 1, "hp_gemm: empty problem");
-  HP_CHECK_ARG(K % BK == 0, "hp_gemm: K must be a multiple of 64");
+  HP_CHECK_ARG(K % 128 == 0, "hp_gemm: K must be a multiple of 128 (tiled weight layout)");
   HP_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SILU, "hp_gemm: bad epilogue");
   HP_CHECK_ARG(epilogue != EPI_RESID || R != nullptr, "hp_gemm: residual epilogue needs R");
   HP_CHECK_ARG(max_ctas >= 1, "hp_gemm: max_ctas must be >= 1");

@@ -96,7 +96,7 @@ __global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, 
   }
 }
 
-// Row-major W [N, K] (row pitch ldw) -> tiled [N/256][K/64][256][64] with
+// Row-major W [N, K] (row pitch ldw) -> tiled [N/128][K/128][2][128][64] with
 // the SWIZZLE_128B chunk permutation; one thread per 16-byte chunk.
 __global__ void k_tile_weight(const __nv_bfloat16* __restrict__ w, int ldw,
                               __nv_bfloat16* __restrict__ out, int N, int K) {
@@ -104,8 +104,9 @@ __global__ void k_tile_weight(const __nv_bfloat16* __restrict__ w, int ldw,
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < chunks; i += long(gridDim.x) * blockDim.x) {
     const int r = int(i / (K / 8));
     const int c = int(i % (K / 8));
-    const int kb = c >> 3, cc = c & 7, nb = r >> 8, rr = r & 255;
-    const size_t dst = ((size_t(nb) * (K >> 6) + kb) * 256 + rr) * 64 + (size_t(cc ^ (rr & 7)) << 3);
+    const int kb = c >> 3, cc = c & 7, mb = r >> 7, rr = r & 127;
+    const size_t dst = (((size_t(mb) * (K >> 7) + (kb >> 1)) * 2 + (kb & 1)) * 128 + rr) * 64 +
+                       (size_t(cc ^ (rr & 7)) << 3);
     *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(w + size_t(r) * ldw + c * 8);
   }
 }
@@ -116,7 +117,7 @@ using namespace hp;
 
 extern "C" int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream) {
   HP_CHECK_ARG(w && out && w != out, "hp_tile_weight: bad pointers (in place not supported)");
-  HP_CHECK_ARG(N % 256 == 0 && K % 64 == 0 && ldw >= K && ldw % 8 == 0, "hp_tile_weight: N % 256, K % 64");
+  HP_CHECK_ARG(N % 128 == 0 && K % 128 == 0 && ldw >= K && ldw % 8 == 0, "hp_tile_weight: N % 128, K % 128");
   const long chunks = long(N) * (K / 8);
   const int grid = int(std::min<long>((chunks + 255) / 256, 148L * 16));
   k_tile_weight<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(

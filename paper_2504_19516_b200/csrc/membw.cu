@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(128) k_membw_tma2d(const __grid_constant__ CUt
 // as many stages as fit in 192 KB -- isolates the copy engine's per-SM
 // throughput from any consumer work.
 __global__ void __launch_bounds__(256) k_membw_bulk(const uint8_t* __restrict__ src, size_t bytes,
-                                                    uint32_t chunk, int spin, float* __restrict__ out) {
+                                                    uint32_t chunk, int spin, int blocked,
+                                                    float* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   // spin >= 2: lanes 0..spin-1 of ONE warp issue independent rings (is the
@@ -133,10 +134,15 @@ __global__ void __launch_bounds__(256) k_membw_bulk(const uint8_t* __restrict__ 
   fence_barrier_init();
   const size_t nchunks = bytes / chunk;
   const size_t gw = size_t(gridDim.x) * nw, me = size_t(blockIdx.x) * nw + w;
-  const size_t my = nchunks > me ? (nchunks - me + gw - 1) / gw : 0;
+  size_t my = nchunks > me ? (nchunks - me + gw - 1) / gw : 0;
+  if (blocked) {
+    const size_t per = (nchunks + gw - 1) / gw;
+    my = me * per >= nchunks ? 0 : std::min(per, nchunks - me * per);
+  }
   auto issue = [&](size_t k) {
     const int s = int(k % nst);
-    const size_t c = me + k * gw;
+    // interleaved (chunk me + k * gw) or blocked (each issuer a contiguous range)
+    const size_t c = blocked ? me * ((nchunks + gw - 1) / gw) + k : me + k * gw;
     mbar_arrive_expect_tx(&full[s], chunk);
     bulk_load(smem + size_t(s) * chunk, src + c * chunk, chunk, &full[s]);
   };
@@ -164,9 +170,135 @@ __global__ void __launch_bounds__(256) k_membw_bulk(const uint8_t* __restrict__ 
   if (acc == 0x12345678u) out[0] = 1.f;
 }
 
+// Producer/consumer pipeline probe (the GEMM mainloop minus the MMA):
+// warps 0..np-1 issue bulk copies for stages g = w (mod np) after waiting the
+// stage's empty barrier; warp np consumes stages strictly in order (wait full,
+// arrive empty).  Blocked per-CTA ranges like the stream-K GEMM.
+__global__ void __launch_bounds__(288) k_membw_pipe(const uint8_t* __restrict__ src, size_t bytes,
+                                                    uint32_t chunk, int np, float* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int nst = int((192u * 1024u) / chunk);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + 192 * 1024);
+  uint64_t* empty = full + 64;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const size_t nchunks = bytes / chunk;
+  const size_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = blockIdx.x * per;
+  const size_t my = c0 >= nchunks ? 0 : std::min(per, nchunks - c0);
+  if (lane != 0) return;
+  if (warp < np) {
+    for (size_t g = warp; g < my; g += np) {
+      const int s = int(g % nst);
+      mbar_wait(&empty[s], uint32_t(((g / nst) & 1) ^ 1));
+      mbar_arrive_expect_tx(&full[s], chunk);
+      bulk_load(base + size_t(s) * chunk, src + (c0 + g) * chunk, chunk, &full[s]);
+    }
+  } else if (warp == np) {
+    uint32_t acc = 0;
+    for (size_t g = 0; g < my; ++g) {
+      const int s = int(g % nst);
+      mbar_wait(&full[s], uint32_t((g / nst) & 1));
+      acc ^= *reinterpret_cast<const uint32_t*>(base + size_t(s) * chunk);
+      mbar_arrive(&empty[s]);
+    }
+    if (acc == 0x12345678u) out[0] = 1.f;
+  }
+}
+
+// UMMA issue-rate probe: one thread issues `n` tcgen05.mma (M=128, N=BN,
+// K=16, both operands from 128B-swizzled smem) into `chains` accumulators,
+// commits once, and records the cycles until completion.
+template <int BN>
+__global__ void __launch_bounds__(128) k_umma_rate(int n, int chains, long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc(&slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 16384);
+    const long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      const int k = i & 3;
+      umma_bf16(tmem + (i % chains) * BN, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                i >= chains ? 1u : 0u);
+    }
+    const long long t1 = clock64();
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    out[blockIdx.x * 2] = t1 - t0;
+    out[blockIdx.x * 2 + 1] = t2 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace hp
 
 using namespace hp;
+
+extern "C" int hp_umma_rate(int n, int bn, int chains, int ctas, long long* out, void* stream) {
+  HP_CHECK_ARG(out && n >= 1 && chains >= 1 && chains * bn <= 512 && ctas >= 1, "hp_umma_rate: bad args");
+  const size_t smem = 1024 + 16384 + 32768;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (bn == 32) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma_rate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma_rate<32><<<ctas, 128, smem, st>>>(n, chains, out);
+  } else if (bn == 128) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma_rate<128><<<ctas, 128, smem, st>>>(n, chains, out);
+  } else {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma_rate<256><<<ctas, 128, smem, st>>>(n, chains, out);
+  }
+  HP_LAUNCH_CHECK("k_umma_rate");
+  return HP_OK;
+}
+
+extern "C" int hp_membw_pipe(const void* src, size_t bytes, int ctas, int chunk_kb, int producers,
+                             float* out, void* stream) {
+  const uint32_t chunk = uint32_t(chunk_kb) * 1024;
+  HP_CHECK_ARG(src && out && ctas >= 1 && chunk >= 4096 && bytes % chunk == 0 && producers >= 1 &&
+                   producers <= 8 && int((192u * 1024u) / chunk) >= producers,
+               "hp_membw_pipe: bad arguments");
+  const size_t smem = 192 * 1024 + 128 + 2 * 64 * 8;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_membw_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  k_membw_pipe<<<ctas, 32 * (producers + 1), smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), bytes, chunk, producers, out);
+  HP_LAUNCH_CHECK("k_membw_pipe");
+  return HP_OK;
+}
 
 extern "C" int hp_membw2d(const void* src, int rows, int cols, int box_rows, int ctas, float* out,
                           void* stream) {
@@ -194,7 +326,8 @@ extern "C" int hp_membw(const void* src, size_t bytes, int ctas, int method, flo
   } else if (method >= 10) {
     // method = 10 + log2(chunk / 4 KB) + 8 * log2(issuing warps) + 64 * spin
     // (spin 0: try_wait, 1: test_wait spin, k >= 2: k issuing lanes of one warp)
-    const int spin = (method - 10) / 64;
+    const int blocked = (method - 10) / 1024;  // + 1024: each issuer streams a contiguous range
+    const int spin = ((method - 10) % 1024) / 64;
     const int m = (method - 10) % 64;
     const uint32_t chunk = 4096u << (m % 8);
     const int warps = spin >= 2 ? 1 : 1 << (m / 8);
@@ -206,7 +339,8 @@ extern "C" int hp_membw(const void* src, size_t bytes, int ctas, int method, flo
       HP_CUDA_TRY(cudaFuncSetAttribute(k_membw_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       attr2 = true;
     }
-    k_membw_bulk<<<ctas, 32 * warps, smem, st>>>(static_cast<const uint8_t*>(src), bytes, chunk, spin, out);
+    k_membw_bulk<<<ctas, 32 * warps, smem, st>>>(static_cast<const uint8_t*>(src), bytes, chunk, spin,
+                                                 blocked, out);
   } else {
     HP_CHECK_ARG(bytes % MB_CHUNK == 0, "hp_membw: TMA path needs a multiple of 32 KB");
     const size_t smem = MB_STAGES * MB_CHUNK + 256;

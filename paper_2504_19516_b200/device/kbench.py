@@ -47,7 +47,7 @@ def timeit(fn, iters=20, warmup=3, flush=True, stream=None):
 
 def bench_gemm(T, N, K, epi, sms, results):
     x = torch.randn(T, K, device=DEV).to(torch.bfloat16)
-    w = (torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16)
+    w = lib.tile_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
     outN = N // 2 if epi == lib.EPI_SILU else N
     y = torch.empty(T, outN, device=DEV, dtype=torch.bfloat16)
     r = torch.randn(T, outN, device=DEV).to(torch.bfloat16) if epi == lib.EPI_RESID else None
@@ -65,7 +65,7 @@ def bench_gemm(T, N, K, epi, sms, results):
 
 def bench_gemm_swap(T, N, K, epi, sms, results):
     x = torch.randn(T, K, device=DEV).to(torch.bfloat16)
-    w = (torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16)
+    w = lib.tile_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
     outN = N // 2 if epi == lib.EPI_SILU else N
     y = torch.empty(T, outN, device=DEV, dtype=torch.bfloat16)
     r = torch.randn(T, outN, device=DEV).to(torch.bfloat16) if epi == lib.EPI_RESID else None

@@ -44,6 +44,8 @@ SIGNATURES = {
     "hp_probe": (_i, [_i, _i, _i64, _p, _p]),
     "hp_membw": (_i, [_p, _sz, _i, _i, _p, _p]),
     "hp_membw2d": (_i, [_p, _i, _i, _i, _i, _p, _p]),
+    "hp_membw_pipe": (_i, [_p, _sz, _i, _i, _i, _p, _p]),
+    "hp_umma_rate": (_i, [_i, _i, _i, _i, _p, _p]),
 }
 
 

@@ -29,15 +29,17 @@ def test_kv_pack_matches_kernel_index_and_roundtrips(d):
 
 def tile_ref(w):
     N, K = w.shape
-    t = w.view(N // 256, 256, K // 64, 8, 8).permute(0, 2, 1, 3, 4)  # [nb, kb, r, c, e]
-    r = torch.arange(256, device=w.device)
+    # [N/128][K/128][2][128][64] == [N/128][K/64][128][64]: 128-row x 64-col
+    # SW128 boxes, two per contiguous 32 KB [128 x 128] tile
+    t = w.view(N // 128, 128, K // 64, 8, 8).permute(0, 2, 1, 3, 4)  # [nb, kb, r, c, e]
+    r = torch.arange(128, device=w.device)
     c = torch.arange(8, device=w.device)
-    src = (c[None, :] ^ (r[:, None] & 7))[None, None, :, :, None].expand(N // 256, K // 64, 256, 8, 8)
+    src = (c[None, :] ^ (r[:, None] & 7))[None, None, :, :, None].expand(N // 128, K // 64, 128, 8, 8)
     return torch.gather(t, 3, src).contiguous().view(N, K)
 
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
 def test_tile_weight_kernel_matches_reference_permutation():
-    w = torch.randn(512, 320, device="cuda").to(torch.bfloat16)
+    w = torch.randn(384, 640, device="cuda").to(torch.bfloat16)
     assert torch.equal(lib.tile_weight(w), tile_ref(w))
