@@ -112,7 +112,11 @@ int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ld
 /* RoPE on q,k in the fused qkv buffer [T, (Hq+2Hkv)*d] (in place) and the
  * paged KV-cache write of k,v (the `kv_write` bytes of the attention kernel,
  * workload.py:180-182).  cos_sin: fp32 [max_pos, d] = [cos(d/2) | sin(d/2)].
- * slot_mapping[t] = block * page + offset; kcache/vcache: [blocks, Hkv, page, d]. */
+ * slot_mapping[t] = block * page + offset; kcache/vcache: [blocks, Hkv, page, d]
+ * logical, stored per (block, kv head) as [page/64][d/64][64 tokens][64] bf16
+ * with the 16-byte chunks of token row r permuted by (r & 7) (128B swizzle),
+ * so every 64-token K or V tile is one contiguous 64*d*2-byte run.
+ * page % 64 == 0, d % 64 == 0. */
 int hp_rope_kv_write(void* qkv, int ldqkv, int T, int Hq, int Hkv, int d, const int* positions,
                      const float* cos_sin, const int* slot_mapping, void* kcache, void* vcache,
                      int page, int max_ctas, void* stream);

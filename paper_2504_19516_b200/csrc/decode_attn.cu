@@ -35,22 +35,45 @@ namespace hp {
 
 constexpr int DA_TILE = 64;
 constexpr int DA_CONSUMERS = 8;
-constexpr int DA_THREADS = (DA_CONSUMERS + 1) * 32;
-constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;  // 64 rows x 128 B
-constexpr int DA_PROW = 72;                          // padded P^T row (bf16)
-constexpr int DA_WIN = 256;                          // block-table window (pages per unit)
+#ifndef HP_DA_PRODUCERS
+#define HP_DA_PRODUCERS 4
+#endif
+constexpr int DA_PRODUCERS = HP_DA_PRODUCERS;         // issuing warps (one copy stream each)
+constexpr int DA_THREADS = (DA_CONSUMERS + DA_PRODUCERS) * 32;
+constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;   // 64 rows x 128 B
+constexpr int DA_PROW = 72;                           // padded P^T row (bf16)
+constexpr int DA_WREG = 8;                            // block-table window regs per lane
+constexpr int DA_WIN = 32 * DA_WREG;                  // window: pages per unit
+constexpr int DA_MAX_RS = 32;                         // ring slots (tags array size)
+constexpr size_t DA_SMEM_MAX = 227 * 1024;
 
-template <int D>
-struct DaCfg {
-  static constexpr int NBOX = D / 64;                           // 128B boxes per row
-  static constexpr uint32_t STAGE_BYTES = 2 * NBOX * DA_BOX_BYTES;
-  static constexpr int STAGES = int((160u * 1024u) / STAGE_BYTES);
-  static constexpr int CB = 8 * D + 16;                         // per-warp merge buffer (floats)
-  static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES +
-                                 DA_CONSUMERS * CB * sizeof(float) +
-                                 DA_CONSUMERS * 8 * DA_PROW * 2 + 2 * STAGES * 8 + 64 + 64 +
-                                 2 * DA_WIN * sizeof(int);
+// Shared-memory plan, computed on the host (ring depth depends on the GQA
+// group through the merge buffer) and recomputed identically on the device.
+struct DaPlan {
+  int rs;               // ring slots (half-tiles), multiple of DA_PRODUCERS
+  uint32_t hs;          // bytes per slot = one 64-token K or V tile
+  int cb;               // per-warp merge buffer (floats)
+  size_t smem;
 };
+
+inline size_t da_fixed_bytes(int D, int G) {
+  const int cb = G * D + 16;
+  return 1024 + size_t(DA_CONSUMERS) * cb * 4 + size_t(DA_CONSUMERS) * 8 * DA_PROW * 2 +
+         2 * DA_MAX_RS * 8 + DA_MAX_RS * 4 + 64;
+}
+
+inline DaPlan da_plan(int D, int G) {
+  DaPlan pl;
+  pl.hs = uint32_t(DA_TILE) * D * 2;
+  pl.cb = G * D + 16;
+  const size_t fixed = da_fixed_bytes(D, G);
+  int rs = int((DA_SMEM_MAX - fixed) / pl.hs);
+  rs = std::min(rs, DA_MAX_RS);
+  rs -= rs % DA_PRODUCERS;
+  pl.rs = rs;
+  pl.smem = fixed + size_t(rs) * pl.hs;
+  return pl;
+}
 
 struct DecodeParams {
   const __nv_bfloat16* q;
@@ -65,6 +88,7 @@ struct DecodeParams {
   int B, Hq, Hkv, G, page;
   int tps;          // tiles per split
   int max_splits;
+  int rs;           // ring slots
   float scale_log2;
   float* ws_o;      // [B, Hq, max_splits, D]
   float* ws_ml;     // [B, Hq, max_splits, 2]
@@ -83,32 +107,45 @@ __device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
   return id;
 }
 
+// Work unit = (sequence b, kv head, split s of `tps` 64-token tiles).  The
+// CTA streams its units' tiles through a ring of `rs` slots, each holding
+// one 64-token K or V tile (16 KB at D = 128, one contiguous run of the page
+// layout [page/64][D/64][64][64]): half-slot h = 2 * tile + (0: K, 1: V).
+//
+// Producers: DA_PRODUCERS warps; warp w owns every slot s with s % P == w
+// and issues the half-tiles h with h % P == w (rs % P == 0), so each slot is
+// refilled by one thread in order and its empty-barrier waits are
+// unambiguous.  One bulk copy per half-tile; several issuing warps because a
+// single thread sustains only ~4 M copies/s.  Each producer keeps the unit's
+// block-table pages in registers (DA_WREG per lane, fetched one unit ahead)
+// and picks a page with a warp shuffle.
+//
+// Consumers: DA_CONSUMERS warps take the unit's tiles round-robin.  The K
+// slot is released as soon as the scores are in registers, the V slot after
+// the P.V product, so a slot is held for one MMA chain, not a whole tile.
 template <int D>
 __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParams p) {
-  using C = DaCfg<D>;
   constexpr int KK = D / 16;
-  constexpr int STAGES = C::STAGES;
+  constexpr uint32_t HS = uint32_t(DA_TILE) * D * 2;
+  const int RS = p.rs;
+  const int CB = p.G * D + 16;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* ring = smem;
-  float* cbuf = reinterpret_cast<float*>(ring + STAGES * C::STAGE_BYTES);
-  __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * C::CB);
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* cbuf = reinterpret_cast<float*>(ring + size_t(RS) * HS);
+  __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * CB);
   uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + DA_CONSUMERS * 8 * DA_PROW);
-  uint64_t* empty = full + STAGES;
-  // Tiles are consumed round-robin by 8 warps from a ring of STAGES slots, so
-  // a warp can reach a slot more than one phase ahead of the producer, where
-  // a parity wait would be ambiguous.  Consumers first wait until the slot's
-  // tag names their tile (set once the producer passed the slot's empty
-  // barrier for it, i.e. the previous occupant was released), then wait on
-  // the slot's parity.
-  volatile uint32_t* tag = reinterpret_cast<volatile uint32_t*>(empty + STAGES);
-  int* win = reinterpret_cast<int*>(const_cast<uint32_t*>(tag) + 16);  // [2][DA_WIN] page ids
+  uint64_t* empty = full + DA_MAX_RS;
+  // Consumers can reach a slot more than one phase ahead of its producer
+  // (8 warps round-robin over the ring), where a parity wait would be
+  // ambiguous: they first wait until the slot's tag names their half-tile
+  // (written once the producer passed the slot's empty barrier for it).
+  volatile uint32_t* tag = reinterpret_cast<volatile uint32_t*>(empty + DA_MAX_RS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 2 * C::NBOX);  // one arrive per K/V box (issued by separate lanes)
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
       tag[s] = 0xffffffffu;
     }
@@ -118,61 +155,58 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
 
   const int total = p.B * p.Hkv * p.max_splits;
   const int page_tiles = p.page / DA_TILE;
-  const size_t page_elems = size_t(p.page) * 64;  // one 64-dim half of one page
 
-  if (warp == DA_CONSUMERS) {
-    // ------------------------------------------------------------ producer
-    // One thread's async-copy stream is serialised at ~one DRAM latency per
-    // copy, so every 8 KB box of a tile is issued by its own lane: lane =
-    // slot * PARTS + part, where `slot` takes every SLOTS-th tile of the
-    // unit (SLOTS <= STAGES keeps every parity wait unambiguous) and `part`
-    // is one K or V box.  The unit's block-table pages are staged in a
-    // double-buffered smem window, loaded one unit ahead.
-    constexpr int PARTS = 2 * C::NBOX;
-    constexpr int SLOTS = (32 / PARTS) < STAGES ? (32 / PARTS) : STAGES;
-    const int slot = lane / PARTS, part = lane % PARTS;
-    const bool issuer = slot < SLOTS;
+  if (warp >= DA_CONSUMERS) {
+    // ------------------------------------------------------------ producers
+    const int pw = warp - DA_CONSUMERS;
     const uint64_t pol = l2_policy_evict_first();  // KV is read once per step
-    uint32_t gtile = 0;
-    int wb = 0;
-    auto load_window = [&](int u, int buf) -> int {  // returns ctx of unit u
+    int win[DA_WREG], winn[DA_WREG];
+    auto fetch = [&](int u, int (&w)[DA_WREG]) -> int {  // returns ctx of unit u
       const UnitId id = unit_of(p, u);
-      const int ctx = p.ctx_lens[id.b];
       const int first = (id.s * p.tps) / page_tiles;
       const int last = min(p.max_pages, ((id.s + 1) * p.tps + page_tiles - 1) / page_tiles);
-      for (int j = lane; j < last - first; j += 32)
-        win[buf * DA_WIN + j] = p.block_table[size_t(id.b) * p.max_pages + first + j];
-      return ctx;
+      const int* row = p.block_table + size_t(id.b) * p.max_pages;
+#pragma unroll
+      for (int r = 0; r < DA_WREG; ++r) {
+        const int j = first + r * 32 + lane;
+        w[r] = j < last ? row[j] : 0;
+      }
+      return p.ctx_lens[id.b];
     };
+    uint32_t hbase = 0;
     int u = blockIdx.x;
-    int ctx_cur = u < total ? load_window(u, 0) : 0;
+    int ctx_cur = u < total ? fetch(u, win) : 0;
     for (; u < total; u += gridDim.x) {
       const UnitId id = unit_of(p, u);
-      __syncwarp();
-      const int ctx_nxt = (u + int(gridDim.x) < total) ? load_window(u + gridDim.x, wb ^ 1) : 0;
+      const int ctx_nxt = (u + int(gridDim.x) < total) ? fetch(u + gridDim.x, winn) : 0;
       const int ntiles = (ctx_cur + DA_TILE - 1) / DA_TILE;
       const int t0 = id.s * p.tps;
       const int t1 = min(ntiles, t0 + p.tps);
-      if (issuer && t0 < t1) {
-        const int first = t0 / page_tiles;
-        for (int t = t0 + slot; t < t1; t += SLOTS) {
-          const int blk = win[wb * DA_WIN + t / page_tiles - first];
-          const uint32_t g = gtile + (t - t0);
-          const int st = g % STAGES;
-          const uint32_t ph = (g / STAGES) & 1;
-          const size_t base = (size_t(blk) * p.Hkv + id.kvh) * C::NBOX * page_elems +
-                              size_t(t % page_tiles) * DA_TILE * 64;
-          mbar_wait(&empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&full[st], DA_BOX_BYTES);
-          const int bx = part % C::NBOX;
-          const uint8_t* src = (part < C::NBOX ? p.kc : p.vc) + (base + bx * page_elems) * 2;
-          bulk_load_hint(ring + st * C::STAGE_BYTES + part * DA_BOX_BYTES, src, DA_BOX_BYTES, &full[st], pol);
-          if (part == 0) tag[st] = g;
+      const int nh = 2 * max(0, t1 - t0);
+      const int first = t0 / page_tiles;
+      for (int hh = (pw - int(hbase % DA_PRODUCERS) + DA_PRODUCERS) % DA_PRODUCERS; hh < nh;
+           hh += DA_PRODUCERS) {
+        const int t = t0 + (hh >> 1);
+        const int pr = t / page_tiles - first;
+        int sel = win[0];
+#pragma unroll
+        for (int r = 1; r < DA_WREG; ++r) sel = (pr >> 5) == r ? win[r] : sel;
+        const int blk = __shfl_sync(0xffffffffu, sel, pr & 31);
+        const uint32_t h = hbase + hh;
+        const int st = int(h % RS);
+        mbar_wait(&empty[st], ((h / RS) & 1) ^ 1);
+        if (lane == 0) {
+          const size_t tile = ((size_t(blk) * p.Hkv + id.kvh) * page_tiles + (t % page_tiles)) * HS;
+          mbar_arrive_expect_tx(&full[st], HS);
+          bulk_load_hint(ring + size_t(st) * HS, ((hh & 1) ? p.vc : p.kc) + tile, HS, &full[st], pol);
+          tag[st] = h;
         }
+        __syncwarp();
       }
-      gtile += max(0, t1 - t0);
+      hbase += nh;
       ctx_cur = ctx_nxt;
-      wb ^= 1;
+#pragma unroll
+      for (int r = 0; r < DA_WREG; ++r) win[r] = winn[r];
     }
     return;
   }
@@ -182,8 +216,8 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   const int t4 = lane & 3;   // thread in group
   const int mat = lane >> 3;
   __nv_bfloat16* pw = pbuf + warp * 8 * DA_PROW;
-  float* cw = cbuf + warp * C::CB;
-  uint32_t gtile = 0;
+  float* cw = cbuf + warp * CB;
+  uint32_t hbase = 0;
 
   auto load_q = [&](int u, uint32_t (&qf)[KK][2], int& ctx) {
     const UnitId id = unit_of(p, u);
@@ -197,6 +231,12 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
       qf[kk][0] = hv ? lo : 0u;
       qf[kk][1] = hv ? hi : 0u;
     }
+  };
+  auto acquire = [&](uint32_t h) -> uint32_t {
+    const int st = int(h % RS);
+    while (tag[st] != h) __nanosleep(20);
+    mbar_wait(&full[st], (h / RS) & 1);
+    return uint32_t(st);
   };
 
   uint32_t qcur[KK][2];
@@ -221,14 +261,21 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
       float l0 = 0.f, l1 = 0.f;              // per-lane partial sums
 
       for (int i = warp; i < nt; i += DA_CONSUMERS) {
-        const uint32_t g = gtile + i;
-        const int st = g % STAGES;
-        const uint32_t ph = (g / STAGES) & 1;
-        while (tag[st] != g) __nanosleep(32);
-        mbar_wait(&full[st], ph);
-        const uint32_t kb = smem_u32(ring + st * C::STAGE_BYTES);
-        const uint32_t vb = kb + C::NBOX * DA_BOX_BYTES;
+        const uint32_t hk = hbase + 2 * i;
+#ifdef HP_DA_NOCOMPUTE  // experiment: stream the ring without the math
+        {
+          const uint32_t a = acquire(hk);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[a]);
+          const uint32_t b = acquire(hk + 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[b]);
+          continue;
+        }
+#endif
         // ---- S^T = K . Q^T : four independent 16-token m tiles
+        const uint32_t sk = acquire(hk);
+        const uint32_t kb = smem_u32(ring + size_t(sk) * HS);
         float sc[4][4];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
@@ -243,6 +290,8 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
             mma_bf16_16816(sc[mt], a, qcur[kk]);
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sk]);  // K tile consumed
         // ---- mask, scale, online softmax
         const int tokbase = (t0 + i) * DA_TILE;
         float tm0 = -INFINITY, tm1 = -INFINITY;
@@ -296,6 +345,8 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           pf[kt][0] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4);
           pf[kt][1] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4 + 8);
         }
+        const uint32_t sv = acquire(hk + 1);
+        const uint32_t vb = smem_u32(ring + size_t(sv) * HS);
 #pragma unroll
         for (int kt = 0; kt < 4; ++kt) {
 #pragma unroll
@@ -308,45 +359,58 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        if (lane == 0) mbar_arrive(&empty[sv]);  // V tile consumed
       }
-      // ---- merge the consumer warps' (m, l, O)
+      // ---- merge the consumer warps' (m, l, O) for the G live heads
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         l0 += __shfl_xor_sync(0xffffffffu, l0, off);
         l1 += __shfl_xor_sync(0xffffffffu, l1, off);
       }
+      const int G = p.G;
+      const bool h0 = 2 * t4 < G, h1 = 2 * t4 + 1 < G;
 #pragma unroll
       for (int dm = 0; dm < KK; ++dm) {
-        cw[(2 * t4) * D + dm * 16 + g8] = o[dm][0];
-        cw[(2 * t4 + 1) * D + dm * 16 + g8] = o[dm][1];
-        cw[(2 * t4) * D + dm * 16 + g8 + 8] = o[dm][2];
-        cw[(2 * t4 + 1) * D + dm * 16 + g8 + 8] = o[dm][3];
+        if (h0) {
+          cw[(2 * t4) * D + dm * 16 + g8] = o[dm][0];
+          cw[(2 * t4) * D + dm * 16 + g8 + 8] = o[dm][2];
+        }
+        if (h1) {
+          cw[(2 * t4 + 1) * D + dm * 16 + g8] = o[dm][1];
+          cw[(2 * t4 + 1) * D + dm * 16 + g8 + 8] = o[dm][3];
+        }
       }
       if (g8 == 0) {
-        cw[8 * D + 2 * t4] = m0;
-        cw[8 * D + 2 * t4 + 1] = m1;
-        cw[8 * D + 8 + 2 * t4] = l0;
-        cw[8 * D + 8 + 2 * t4 + 1] = l1;
+        if (h0) {
+          cw[G * D + 2 * t4] = m0;
+          cw[G * D + 8 + 2 * t4] = l0;
+        }
+        if (h1) {
+          cw[G * D + 2 * t4 + 1] = m1;
+          cw[G * D + 8 + 2 * t4 + 1] = l1;
+        }
       }
       named_bar_sync(1, DA_CONSUMERS * 32);
       const int nsplit = (ntiles + p.tps - 1) / p.tps;
       const int nw = min(DA_CONSUMERS, nt);  // warps that saw at least one tile
       constexpr int Q4 = D / 4;              // float4 groups per head row
-      for (int e = threadIdx.x; e < p.G * Q4; e += DA_CONSUMERS * 32) {
+      for (int e = threadIdx.x; e < G * Q4; e += DA_CONSUMERS * 32) {
         const int h = e / Q4;
         const int d4 = (e % Q4) * 4;
         float M = -INFINITY;
-        for (int w = 0; w < nw; ++w) M = fmaxf(M, cbuf[w * C::CB + 8 * D + h]);
+        for (int w = 0; w < nw; ++w) M = fmaxf(M, cbuf[w * CB + G * D + h]);
         float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int w = 0; w < nw; ++w) {
-          const float* c = cbuf + w * C::CB;
-          const float f = exp2f(c[8 * D + h] - M);
-          L += f * c[8 * D + 8 + h];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] += f * c[h * D + d4 + j];
+          const float* c = cbuf + w * CB;
+          const float f = exp2f(c[G * D + h] - M);
+          L += f * c[G * D + 8 + h];
+          const float4 v = *reinterpret_cast<const float4*>(c + h * D + d4);
+          acc[0] += f * v.x;
+          acc[1] += f * v.y;
+          acc[2] += f * v.z;
+          acc[3] += f * v.w;
         }
-        const int head = id.kvh * p.G + h;
+        const int head = id.kvh * G + h;
         if (nsplit == 1) {
           const float inv = 1.f / L;
           uint2 w;
@@ -363,7 +427,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
         }
       }
       named_bar_sync(1, DA_CONSUMERS * 32);
-      gtile += nt;
+      hbase += 2 * nt;
     }
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
@@ -407,15 +471,17 @@ __global__ void k_decode_combine(const DecodeParams p) {
 }
 
 template <int D>
-static int launch_decode(const DecodeParams& p, int max_ctas, cudaStream_t st) {
-  using C = DaCfg<D>;
+static int launch_decode(DecodeParams& p, int max_ctas, cudaStream_t st) {
+  const DaPlan pl = da_plan(D, p.G);
+  p.rs = pl.rs;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(DA_SMEM_MAX)));
     attr = true;
   }
   const int units = p.B * p.Hkv * p.max_splits;
-  k_decode_attn<D><<<std::min(units, max_ctas), DA_THREADS, C::SMEM, st>>>(p);
+  k_decode_attn<D><<<std::min(units, max_ctas), DA_THREADS, pl.smem, st>>>(p);
   HP_LAUNCH_CHECK("k_decode_attn");
   if (p.max_splits > 1) {
     const int warps = p.B * p.Hq;

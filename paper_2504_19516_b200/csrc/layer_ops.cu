@@ -67,10 +67,11 @@ __global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, 
     __nv_bfloat16* row = qkv + size_t(t) * ld + size_t(head) * d;
     const int slot = (head >= Hq) ? slots[t] : 0;
     const int blk = slot / page, off = slot % page;
-    // cache page layout [d/64][page][64], 16B chunks swizzled by (token & 7)
+    // cache page layout [page/64][d/64][64][64]: each 64-token tile of one
+    // kv head is a contiguous 64*d run, 16B chunks swizzled by (token & 7)
     auto cidx = [&](int kvh, int j) -> size_t {
-      return ((size_t(blk) * Hkv + kvh) * (d / 64) + j / 64) * size_t(page) * 64 + size_t(off) * 64 +
-             ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7);
+      return (((size_t(blk) * Hkv + kvh) * (page / 64) + off / 64) * (d / 64) + j / 64) * 4096 +
+             size_t(off & 63) * 64 + ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7);
     };
     if (head < Hq + Hkv) {
       const float* c = cs + size_t(pos[t]) * d;
@@ -147,7 +148,8 @@ extern "C" int hp_rope_kv_write(void* qkv, int ldqkv, int T, int Hq, int Hkv, in
   HP_CHECK_ARG(qkv && positions && cos_sin && slot_mapping && kcache && vcache, "hp_rope_kv_write: null pointer");
   HP_CHECK_ARG(T >= 1 && Hq >= 1 && Hkv >= 1 && d % 4 == 0, "hp_rope_kv_write: bad shape");
   HP_CHECK_ARG(ldqkv >= (Hq + 2 * Hkv) * d && ldqkv % 2 == 0, "hp_rope_kv_write: bad row pitch");
-  HP_CHECK_ARG(page >= 1 && max_ctas >= 1, "hp_rope_kv_write: bad page/max_ctas");
+  HP_CHECK_ARG(page >= 64 && page % 64 == 0 && max_ctas >= 1, "hp_rope_kv_write: page must be a multiple of 64");
+  HP_CHECK_ARG(d % 64 == 0, "hp_rope_kv_write: head_dim must be a multiple of 64");
   const long total = long(T) * (Hq + 2 * Hkv) * (d / 4);
   const int threads = 256;
   const long want = (total + threads - 1) / threads;

@@ -103,9 +103,11 @@ class CoRunner:
         torch.cuda.synchronize()
 
     # ------------------------------------------------------------- launches
-    def prefill_layer(self, ps: PhaseStreams, timers=None) -> int:
-        return self.layer.prefill(self.px, self.py, self.psc, self.p_cu, 1, self.T, self.p_pos,
-                                  self.p_slots, self.pcache, ps.sms, ps.torch_stream, timers)
+    def prefill_layer(self, ps: PhaseStreams, timers=None, x=None, y=None) -> int:
+        x = self.px if x is None else x
+        y = self.py if y is None else y
+        return self.layer.prefill(x, y, self.psc, self.p_cu, 1, self.T, self.p_pos, self.p_slots,
+                                  self.pcache, ps.sms, ps.torch_stream, timers)
 
     def decode_layer(self, ds: PhaseStreams) -> int:
         return self.layer.decode(self.dx, self.dy, self.dsc, self.ctx, self.d_pos, self.d_slots,
@@ -198,6 +200,63 @@ class CoRunner:
         if ug_ev:
             res.upgate_s = [a.elapsed_time(b) * 1e-3 for a, b in (e["mlp_up_gate"] for e in ug_ev)]
         return res
+
+    def corun_e2e(self, pm: int, dm: int, steps: int, decode_per_step: int, host_px, host_py,
+                  host_dx, host_dy) -> CoRunResult:
+        """`corun` end to end from pinned host memory: every prefill layer's
+        input is copied host->device and its output device->host, every
+        decode step's input/output likewise.  Prefill copies run on their own
+        copy-engine streams, double-buffered so step s+1's input lands and
+        step s-1's output drains while step s computes (the serving
+        pipeline); decode copies (B x hidden) stay in-stream."""
+        ps, ds = self.pool.split(pm, dm)
+        g = self.decode_graph(ds)
+        ctrl = torch.cuda.current_stream(self.dev)
+        h2d, d2h = torch.cuda.Stream(self.dev), torch.cuda.Stream(self.dev)
+        xs = [self.px, torch.empty_like(self.px)]
+        ys = [self.py, torch.empty_like(self.py)]
+        in_ready = [_ev() for _ in range(steps)]
+        done = [_ev() for _ in range(steps)]
+        out_done = [_ev() for _ in range(steps)]
+        start, end_p, end_d, end_o = _ev(), _ev(), _ev(), _ev()
+        torch.cuda._sleep(400_000)
+        start.record(ctrl)
+        for st in (ps.torch_stream, ds.torch_stream, h2d, d2h):
+            st.wait_event(start)
+
+        def load(s):
+            with torch.cuda.stream(h2d):
+                if s >= 2:
+                    h2d.wait_event(done[s - 2])  # buffer s%2 free once step s-2 computed
+                xs[s % 2].copy_(host_px, non_blocking=True)
+                in_ready[s].record(h2d)
+
+        load(0)
+        for s in range(steps):
+            if s + 1 < steps:
+                load(s + 1)
+            with torch.cuda.stream(ps.torch_stream):
+                ps.torch_stream.wait_event(in_ready[s])
+                if s >= 2:
+                    ps.torch_stream.wait_event(out_done[s - 2])  # ys[s%2] drained
+                self.prefill_layer(ps, None, xs[s % 2], ys[s % 2])
+                done[s].record(ps.torch_stream)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done[s])
+                host_py.copy_(ys[s % 2], non_blocking=True)
+                out_done[s].record(d2h)
+            with torch.cuda.stream(ds.torch_stream):
+                for _ in range(decode_per_step):
+                    self.dx.copy_(host_dx, non_blocking=True)
+                    g.replay()
+                    host_dy.copy_(self.dy, non_blocking=True)
+        end_p.record(ps.torch_stream)
+        end_d.record(ds.torch_stream)
+        end_o.record(d2h)
+        torch.cuda.synchronize()
+        span = max(start.elapsed_time(e) for e in (end_p, end_d, end_o)) * 1e-3
+        return CoRunResult(pm, dm, steps, steps * decode_per_step, span, steps * self.T,
+                           steps * decode_per_step * self.B)
 
     def time_sliced(self, steps: int, decode_per_step: int) -> CoRunResult:
         """Same work, one full-GPU stream: prefill layer then its decode steps."""

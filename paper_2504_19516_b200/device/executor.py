@@ -76,6 +76,7 @@ class B200Executor:
         self.dy = torch.empty_like(self.dx)
         self.dsc = DecodeScratch(model, max_decode_batch, 1024, self.dev, max_ctas=self.pool.n)
         self.calls = {"prefill": 0, "decode": 0}
+        self._warm: set = set()
 
     # ------------------------------------------------------------ workloads
     def _prefill_args(self, lens):
@@ -129,17 +130,29 @@ class B200Executor:
         margs, oargs = (pargs, dargs) if phase == "prefill" else (dargs, pargs)
         if main is None:
             raise InvalidArgumentError(f"{phase} phase has no SMs in {es}")
+        cover = self._cover_count(phase, es) if other is not None else 0
+        key = (phase, pm, dm, es.prefill_lens, es.decode_ctx_lens)
+        if key not in self._warm:  # first launch of a shape: tensor maps, module load
+            with torch.cuda.stream(main.torch_stream):
+                run_main(main, margs)
+            if other is not None:
+                with torch.cuda.stream(other.torch_stream):
+                    run_other(other, oargs)
+            torch.cuda.synchronize(self.dev)
+            self._warm.add(key)
         ctrl = torch.cuda.current_stream(self.dev)
         start = _ev()
         a, b = _ev(), _ev()
-        torch.cuda._sleep(300_000)  # queue everything ahead of the timed region
+        # hold the GPU while the host queues everything (~10 launches per
+        # layer, tens of us each through ctypes), so host latency stays out
+        torch.cuda._sleep(400_000 + 300_000 * (1 + cover))
         start.record(ctrl)
         main.torch_stream.wait_event(start)
         if other is not None:
             other.torch_stream.wait_event(start)
             # keep the other phase busy for the whole measured layer
             with torch.cuda.stream(other.torch_stream):
-                for _ in range(self._cover_count(phase, es)):
+                for _ in range(cover):
                     run_other(other, oargs)
         with torch.cuda.stream(main.torch_stream):
             a.record(main.torch_stream)
@@ -178,9 +191,9 @@ class B200Executor:
             return self.prefill_layer_s(es) / srm_prefill_layer_s(es, self.model, self.gpu)
         from ..engine import canonical_decode_es
 
-        es = canonical_decode_es(int(tokens), sms)
-        if es.decode_batch > self.max_decode_batch:
-            raise InvalidArgumentError("canonical decode batch exceeds max_decode_batch")
+        # alpha is a ratio, so a canonical batch beyond the resident scratch is
+        # measured at the largest batch of the same per-sequence context
+        es = canonical_decode_es(min(int(tokens), self.max_decode_batch * 1024), sms)
         return self.decode_step_s(es) / srm_decode_step_s(es, self.model, self.gpu)
 
     def contention_bw(self, sms: int, co_prefill_len: int, nbytes: int = 1 << 30) -> float:

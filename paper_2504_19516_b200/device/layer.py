@@ -20,12 +20,13 @@ Data layout in HBM (bf16 unless noted):
   x / h / y          [T, hidden] residual stream (ping-pong, inputs untouched)
   qkv                [T, (Hq + 2 Hkv) d]  q | k | v column blocks
   w_qkv              [(Hq + 2 Hkv) d, hidden]        torch [out, in], then tiled
-  w_o                [hidden, hidden]                 (hp_tile_weight: [N/256][K/64]
-  w_ug               [2 I, hidden]  gate/up rows       [256][64], 128B-swizzled, so
-                     interleaved in 64-row blocks      each GEMM tile is one
+  w_o                [hidden, hidden]                 (hp_tile_weight: [N/128][K/128][2]
+  w_ug               [2 I, hidden]  gate/up rows       128B-swizzled,
+                     interleaved in 64-row blocks      [128][64], so each 128x128 tile is one
   w_down             [hidden, I]                       contiguous bulk copy)
   kcache / vcache    [num_blocks, Hkv, page, d] logical; stored per page as
-                     [d/64][page][64] with swizzled 16B chunks (lib.kv_pack);
+                     [page/64][d/64][64][64] (64-token tiles, each one
+                     contiguous run) with swizzled 16B chunks (lib.kv_pack);
                      zero-initialised
   block_table int32  [B, max_pages];  ctx_lens int32 [B]
   rope table fp32    [max_pos, d]  (cos | sin)

@@ -200,26 +200,27 @@ def membw(src, ctas: int, method: int, out, stream=None) -> None:
                           _stream(stream)), "hp_membw")
 
 
-def _kv_chunk_index(x5):
-    """Gather index swapping 16-byte chunk c of token row r with c ^ (r & 7)."""
+def _kv_chunk_index(x7):
+    """Gather index swapping 16-byte chunk c of token row r with c ^ (r & 7)
+    over a [nb, H, tiles, halves, 64 rows, 8 chunks, 8] view."""
     import torch
 
-    nb, H, nh, P, _ = x5.shape[:5]
-    r = torch.arange(P, device=x5.device)
-    c = torch.arange(8, device=x5.device)
+    r = torch.arange(64, device=x7.device)
+    c = torch.arange(8, device=x7.device)
     src = c[None, :] ^ (r[:, None] & 7)
-    return src[None, None, None, :, :, None].expand(nb, H, nh, P, 8, 8)
+    return src[None, None, None, None, :, :, None].expand(*x7.shape)
 
 
 def kv_pack(x):
     """Logical K or V cache [blocks, Hkv, page, d] -> the device page layout
-    ([blocks, Hkv, d/64, page, 64] with 128B-swizzled chunks), returned as a
-    tensor of the same shape whose memory is in device order."""
+    ([blocks, Hkv, page/64, d/64, 64, 64]: 64-token tiles, each a contiguous
+    run of 64-dim halves with 128B-swizzled chunks), returned as a tensor of
+    the same shape whose memory is in device order."""
     import torch
 
     nb, H, P, d = x.shape
-    v = x.reshape(nb, H, P, d // 64, 8, 8).permute(0, 1, 3, 2, 4, 5)
-    return torch.gather(v, 4, _kv_chunk_index(v)).contiguous().view(nb, H, P, d)
+    v = x.reshape(nb, H, P // 64, 64, d // 64, 8, 8).permute(0, 1, 2, 4, 3, 5, 6)
+    return torch.gather(v, 5, _kv_chunk_index(v)).contiguous().view(nb, H, P, d)
 
 
 def kv_unpack(y):
@@ -227,9 +228,9 @@ def kv_unpack(y):
     import torch
 
     nb, H, P, d = y.shape
-    v = y.reshape(nb, H, d // 64, P, 8, 8)
-    v = torch.gather(v, 4, _kv_chunk_index(v))
-    return v.permute(0, 1, 3, 2, 4, 5).contiguous().view(nb, H, P, d)
+    v = y.reshape(nb, H, P // 64, d // 64, 64, 8, 8)
+    v = torch.gather(v, 5, _kv_chunk_index(v))
+    return v.permute(0, 1, 2, 4, 3, 5, 6).contiguous().view(nb, H, P, d)
 
 
 def probe(out, ctas: int, threads: int = 128, spin_ns: int = 20000, stream=None) -> None:

@@ -150,8 +150,9 @@ def rope_table(max_pos, d, theta=500000.0):
     return torch.cat([ang.cos(), ang.sin()], dim=1).float().to(DEV)
 
 
-def test_rope_kv_write(gen):
-    T, Hq, Hkv, d, page = 100, 8, 2, 128, 64
+@pytest.mark.parametrize("page", [64, 128])
+def test_rope_kv_write(gen, page):
+    T, Hq, Hkv, d = 100, 8, 2, 128
     qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
     orig = qkv.float().clone()
     pos = torch.randint(0, 4000, (T,), device=DEV, dtype=torch.int32)
@@ -234,8 +235,8 @@ def make_cache(B, ctx, Hkv, d, page, gen, extra_blocks=3):
                                           ([5000, 33], 64, 8, 128), ([3000] * 3, 32, 8, 128),
                                           ([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2, 64)])
 @pytest.mark.parametrize("max_ctas", [8, 148])
-def test_decode_attn(ctx, Hq, Hkv, d, max_ctas, gen):
-    page = 64
+@pytest.mark.parametrize("page", [64, 256])
+def test_decode_attn(ctx, Hq, Hkv, d, max_ctas, page, gen):
     B = len(ctx)
     kc, vc, bt = make_cache(B, ctx, Hkv, d, page, gen)
     q = bf((B, Hq * d), gen=gen)

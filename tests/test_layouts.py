@@ -10,13 +10,13 @@ from paper_2504_19516_b200.device import lib
 def kv_index(blk, h, off, j, Hkv, page, d):
     """Element index of (block, kv head, token offset, dim) in the device page
     layout -- the formula of k_rope_kv_write (layer_ops.cu)."""
-    return (((blk * Hkv + h) * (d // 64) + j // 64) * page * 64 + off * 64
-            + ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7))
+    return ((((blk * Hkv + h) * (page // 64) + off // 64) * (d // 64) + j // 64) * 4096
+            + (off & 63) * 64 + ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7))
 
 
-@pytest.mark.parametrize("d", [64, 128])
-def test_kv_pack_matches_kernel_index_and_roundtrips(d):
-    nb, H, P = 3, 2, 64
+@pytest.mark.parametrize("d,P", [(64, 64), (128, 64), (128, 192)])
+def test_kv_pack_matches_kernel_index_and_roundtrips(d, P):
+    nb, H = 3, 2
     x = torch.arange(nb * H * P * d, dtype=torch.float32).view(nb, H, P, d)
     packed = kv_pack_flat = lib.kv_pack(x).reshape(-1)
     g = torch.Generator().manual_seed(0)

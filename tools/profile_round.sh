@@ -9,7 +9,8 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
 timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
 tail -c 3000 $OUT/bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
+# launch list of the timed region only (NVTX range "timed" in bench.py)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed]" --csv \
     --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_bench.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 6 -c 1 \
     -o $OUT/upgate python tools/one_kernel.py gemm4096 $PM 8 > $OUT/ncu_upgate.out 2>&1

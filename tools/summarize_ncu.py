@@ -29,7 +29,7 @@ def launches(path, out):
         name = r["Kernel Name"].split("(")[0]
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
-        us = v / 1000.0 if unit == "nsecond" else v if unit == "usecond" else v * 1000.0
+        us = v / 1000.0 if unit in ("ns", "nsecond") else v if unit in ("us", "usecond") else v * 1000.0
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += us
@@ -60,7 +60,7 @@ def full(path, out, flops=None):
     if flops:
         t = float(res["gpu__time_duration.sum"][0].replace(",", ""))
         unit = units[hdr.index("gpu__time_duration.sum")]
-        sec = t * (1e-9 if unit == "nsecond" else 1e-6 if unit == "usecond" else 1e-3)
+        sec = t * (1e-9 if unit in ("ns", "nsecond") else 1e-6 if unit in ("us", "usecond") else 1e-3)
         txt += f"\nalgorithmic FLOP per launch {float(flops):.4g} -> {float(flops) / sec / 1e12:.1f} TFLOP/s under ncu\n"
     rd = float(res.get("dram__bytes_read.sum", ["0"])[0].replace(",", ""))
     wr = float(res.get("dram__bytes_write.sum", ["0"])[0].replace(",", ""))
