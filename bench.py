@@ -200,6 +200,7 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split", default=None, help="pm,dm,n: skip the warm-up split sweep (profiling)")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
 
@@ -237,14 +238,15 @@ def main(argv=None) -> int:
     ts_ttft = ts_tpot = t_p_full + t_d_full  # alternating: every decode step waits one prefill layer
     ts_alt = cr.time_sliced(args.warmup, 1)
     candidates = []
-    for dm in range(8, 72, 8):
+    fixed = [int(v) for v in args.split.split(",")] if args.split else None
+    for dm in ([fixed[1]] if fixed else range(8, 72, 8)):
         pm = N - dm
         t_d = cr.isolated(DECODE, dm, reps=3)
         t_p = cr.isolated(PREFILL, pm, reps=3)
         # decode steps per prefill layer: the counts either side of t_p / t_d
         # (fit inside the prefill layer, or overrun it by one step)
         nf = max(1, math.floor(t_p / t_d))
-        for n in sorted({nf, nf + 1}):
+        for n in ([fixed[2]] if fixed else sorted({nf, nf + 1})):
             r = cr.corun(pm, dm, 2, n)
             ok = r.p50(r.decode_layer_s) <= ts_tpot and r.p50(r.prefill_layer_s) <= ts_ttft
             candidates.append({"pm": pm, "dm": dm, "n": n, "tokens_per_s": r.tokens_per_s,

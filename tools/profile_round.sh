@@ -1,20 +1,26 @@
 #!/bin/bash
 # Round profile capture (run under gpurun): bench line, ncu launch list of the
-# same bench command, and one full ncu capture of the dominant kernel.
-# Usage: bash tools/profile_round.sh <tag> [pm_sms]
+# same bench command, and one full ncu capture of each dominant kernel.
+# Usage: bash tools/profile_round.sh <tag> [pm_sms] [split pm,dm,n]
 TAG=${1:-r01}
 PM=${2:-140}
+SPLIT=${3:-}
 OUT=gpurun_out/prof_$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
+nproc > $OUT/nproc.txt; lscpu | head -20 >> $OUT/nproc.txt
 timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
 tail -c 3000 $OUT/bench.err
-# launch list of the timed region only (NVTX range "timed" in bench.py)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed]" --csv \
-    --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_bench.out 2>&1
+cat $OUT/bench.json
+if [ -z "$SPLIT" ]; then
+  SPLIT=$(python -c "import json;d=json.loads(open('$OUT/bench.json').read().strip().splitlines()[-1]);c=d['config'];print(f\"{c['pm']},{c['dm']},{c['decode_steps_per_prefill_layer']}\")")
+fi
+echo "split $SPLIT"
+# launch list of the same bench command (fixed split, no sweep): every launch
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 3000 \
+    --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --split $SPLIT > $OUT/ncu_bench.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 6 -c 1 \
     -o $OUT/upgate python tools/one_kernel.py gemm4096 $PM 8 > $OUT/ncu_upgate.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_decode_attn -s 2 -c 1 \
     -o $OUT/decode_attn python tools/one_kernel.py decode_attn 148 4 > $OUT/ncu_dattn.out 2>&1
 ls -la $OUT
-cat $OUT/bench.json
