@@ -130,6 +130,21 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
                     int max_seqlen, int Hq, int Hkv, int d, float scale, int max_ctas,
                     void* stream);
 
+/* Prefix-aware (chunked) prefill attention over the paged cache
+ * (workload.py:176-183 with prior_lens > 0; the attention of a hybrid batch,
+ * hybrid_kernels workload.py:213-257, as issued by _ChunkedSim engine.py:
+ * 741-800 through GroundTruthOracle.hybrid_iteration_s engine.py:200-208).
+ * Sequence s has cu_seqlens[s+1]-cu_seqlens[s] new tokens (rows of q) at
+ * positions prior_lens[s].. ; their K/V must already be in the cache
+ * (hp_rope_kv_write).  Query i attends cache positions [0, prior_lens[s]+i].
+ * Caches as for hp_rope_kv_write; block_table: int [nseq, max_pages].
+ * Cache blocks must hold finite values (zero-initialised pools). */
+int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache, const void* vcache,
+                          const int* block_table, int max_pages, const int* cu_seqlens,
+                          const int* prior_lens, int nseq, int total_tokens, int max_seqlen,
+                          void* o, int ldo, int Hq, int Hkv, int d, int page, int num_blocks,
+                          float scale, int max_ctas, void* stream);
+
 /* Paged decode attention (workload.py:184-188): one query token per
  * sequence over ctx_lens[b] cached positions.  q: [B, Hq*d]; out: [B, Hq*d];
  * block_table: int [B, max_pages]; workspace: fp32, hp_decode_attn_ws_bytes. */

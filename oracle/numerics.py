@@ -191,6 +191,46 @@ def layer_decode(x: np.ndarray, W: LayerWeights, Hq: int, Hkv: int, d: int, ctx_
     return _b(h + act @ W.w_down.T, rb)
 
 
+def layer_hybrid(x: np.ndarray, W: LayerWeights, Hq: int, Hkv: int, d: int, seqs, table: np.ndarray,
+                 kcache: np.ndarray, vcache: np.ndarray, block_table: np.ndarray,
+                 bf16_boundaries: bool = True) -> np.ndarray:
+    """One layer over a hybrid (chunked-prefill) batch -- reference
+    hybrid_kernels (workload.py:213-257): linear kernels over the
+    concatenated token stream, attention per sequence over its cached prefix
+    plus its new span (workload.py:176-183).
+
+    seqs[i] = (new_len, prior) in row order of x; sequence i's pages are
+    block_table[i].  A decode token is (1, ctx - 1).  The new tokens' K/V are
+    written into the (mutated) caches before attention."""
+    rb = bf16_boundaries
+    T = x.shape[0]
+    page = kcache.shape[2]
+    pos = np.concatenate([np.arange(p, p + n) for n, p in seqs]).astype(np.int64)
+    assert len(pos) == T
+    qkv = _b(_b(rmsnorm(x, W.attn_norm), rb) @ W.w_qkv.T, rb)
+    q = _b(apply_rope(qkv[:, : Hq * d].reshape(T, Hq, d), pos, table), rb)
+    k = _b(apply_rope(qkv[:, Hq * d:(Hq + Hkv) * d].reshape(T, Hkv, d), pos, table), rb)
+    v = qkv[:, (Hq + Hkv) * d:].reshape(T, Hkv, d)
+    a = np.empty((T, Hq, d), np.float32)
+    r0 = 0
+    for i, (n, p) in enumerate(seqs):
+        for j in range(n):
+            blk = block_table[i, (p + j) // page]
+            kcache[blk, :, (p + j) % page, :] = k[r0 + j]
+            vcache[blk, :, (p + j) % page, :] = v[r0 + j]
+        L = p + n
+        pages = block_table[i, : -(-L // page)]
+        kk = kcache[pages].transpose(0, 2, 1, 3).reshape(-1, Hkv, d)[:L]
+        vv = vcache[pages].transpose(0, 2, 1, 3).reshape(-1, Hkv, d)[:L]
+        a[r0:r0 + n] = causal_attention(q[r0:r0 + n], kk, vv, 1.0 / math.sqrt(d), prior=p)
+        r0 += n
+    a = _b(a.reshape(T, Hq * d), rb)
+    h = _b(x + a @ W.w_o.T, rb)
+    n2 = _b(rmsnorm(h, W.mlp_norm), rb)
+    act = _b(silu(n2 @ W.w_gate.T) * (n2 @ W.w_up.T), rb)
+    return _b(h + act @ W.w_down.T, rb)
+
+
 def greedy_tokens(hidden: np.ndarray, final_norm: np.ndarray, lm_head: np.ndarray,
                   bf16_boundaries: bool = True):
     """argmax over logits = RMSNorm(hidden) . lm_head^T; also the top-2 margin."""

@@ -1,5 +1,15 @@
 // Causal GQA prefill attention on the 5th-gen tensor cores (reference kernel
-// group "attn", phase prefill with prior_lens = 0; workload.py:176-183).
+// group "attn", phase prefill; workload.py:176-183).  Two operand sources:
+//   dense   (prior_lens = 0): K/V are the new span's columns of the fused qkv
+//           buffer, fetched as 128B-swizzled TMA boxes;
+//   paged   (prior_lens >= 0, chunked prefill / hybrid batches, workload.py:
+//           177-183, 213-257): K/V are read from the paged cache, which holds
+//           the cached prefix plus the new span (hp_rope_kv_write ran first).
+//           A cache page stores each 64-token tile as [d/64][64][64] with the
+//           same 128B swizzle, so every (tile, 64-dim half) is ONE 8 KB bulk
+//           copy landing exactly where the TMA box would have put it.
+//           Query i of a sequence sits at position prior + i and attends keys
+//           [0, prior + i].
 //
 // One CTA owns one (sequence, 128-query tile, q head) unit at a time
 // (persistent grid = partition SMs, units longest-first).  Warp roles:
@@ -49,6 +59,12 @@ struct FaParams {
   __nv_bfloat16* out;
   int ldo;
   float scale_log2;
+  // paged operand source (PAGED kernels only)
+  const __nv_bfloat16* kc;
+  const __nv_bfloat16* vc;
+  const int* block_table;
+  const int* prior_lens;
+  int max_pages, page, Hkv;
 };
 
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo_bytes) {
@@ -84,8 +100,10 @@ __device__ __forceinline__ float ex2(float x) {
 
 struct Unit {
   int head, seq, qt, s0, len, nkv;
+  int prior, kvlen;  // cached prefix length; keys visible to the last query
 };
 
+template <bool PAGED>
 __device__ __forceinline__ bool unit_of(const FaParams& p, int u, Unit& x) {
   x.head = u % p.Hq;
   const int rest = u / p.Hq;
@@ -94,14 +112,28 @@ __device__ __forceinline__ bool unit_of(const FaParams& p, int u, Unit& x) {
   x.s0 = p.cu_seqlens[x.seq];
   x.len = p.cu_seqlens[x.seq + 1] - x.s0;
   if (x.qt * FQ >= x.len) return false;
+  x.prior = PAGED ? p.prior_lens[x.seq] : 0;
+  x.kvlen = x.prior + x.len;
   const int q0 = x.qt * FQ;
-  x.nkv = min((q0 + FQ + FK - 1) / FK, (x.len + FK - 1) / FK);
+  x.nkv = min((x.prior + q0 + FQ + FK - 1) / FK, (x.kvlen + FK - 1) / FK);
   return true;
+}
+
+// Address of the 64-token tile holding cache position `pos` of sequence
+// `seq`, kv head `kvh` (positions past the sequence map to its first page:
+// finite data whose scores the causal mask removes).
+template <int D>
+__device__ __forceinline__ const __nv_bfloat16* page_tile(const FaParams& p, const __nv_bfloat16* base,
+                                                          int seq, int kvh, int pos, int kvlen) {
+  if (pos >= kvlen) pos = 0;
+  const int blk = __ldg(p.block_table + size_t(seq) * p.max_pages + pos / p.page);
+  const int sub = (pos % p.page) >> 6;
+  return base + (size_t(blk) * p.Hkv + kvh) * size_t(p.page) * D + size_t(sub) * 64 * D;
 }
 
 }  // namespace
 
-template <int D>
+template <int D, bool PAGED>
 __global__ void __launch_bounds__(192, 1)
     k_fa_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const FaParams p) {
@@ -160,7 +192,7 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t un = 0, kt = 0, vt = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         Unit x;
-        if (!unit_of(p, u, x)) continue;
+        if (!unit_of<PAGED>(p, u, x)) continue;
         const int kvh = x.head / p.G;
         mbar_wait(q_empty, (un & 1) ^ 1);
         mbar_arrive_expect_tx(q_full, C::QB);
@@ -170,12 +202,34 @@ __global__ void __launch_bounds__(192, 1)
           const int ks = kt % KST, vs = vt % VST;
           mbar_wait(&k_empty[ks], ((kt / KST) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], C::KB);
-          for (int b = 0; b < C::NB; ++b)
-            tma_load_2d(sK + ks * C::KB + b * BOX, &tmK, &k_full[ks], kvh * D + b * 64, x.s0 + j * FK);
+          if constexpr (PAGED) {
+            // 128 keys = two 64-token cache tiles; each 64-dim half is one
+            // contiguous, already-swizzled 8 KB run -> rows t*64.. of box b
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const __nv_bfloat16* src = page_tile<D>(p, p.kc, x.seq, kvh, j * FK + t * 64, x.kvlen);
+#pragma unroll
+              for (int b = 0; b < C::NB; ++b)
+                bulk_load(sK + ks * C::KB + b * BOX + t * (BOX / 2), src + b * 64 * 64, BOX / 2, &k_full[ks]);
+            }
+          } else {
+            for (int b = 0; b < C::NB; ++b)
+              tma_load_2d(sK + ks * C::KB + b * BOX, &tmK, &k_full[ks], kvh * D + b * 64, x.s0 + j * FK);
+          }
           mbar_wait(&v_empty[vs], ((vt / VST) & 1) ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], C::KB);
-          for (int b = 0; b < C::NB; ++b)
-            tma_load_2d(sV + vs * C::KB + b * BOX, &tmV, &v_full[vs], kvh * D + b * 64, x.s0 + j * FK);
+          if constexpr (PAGED) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const __nv_bfloat16* src = page_tile<D>(p, p.vc, x.seq, kvh, j * FK + t * 64, x.kvlen);
+#pragma unroll
+              for (int b = 0; b < C::NB; ++b)
+                bulk_load(sV + vs * C::KB + b * BOX + t * (BOX / 2), src + b * 64 * 64, BOX / 2, &v_full[vs]);
+            }
+          } else {
+            for (int b = 0; b < C::NB; ++b)
+              tma_load_2d(sV + vs * C::KB + b * BOX, &tmV, &v_full[vs], kvh * D + b * 64, x.s0 + j * FK);
+          }
         }
         ++un;
       }
@@ -203,7 +257,7 @@ __global__ void __launch_bounds__(192, 1)
       };
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         Unit x;
-        if (!unit_of(p, u, x)) continue;
+        if (!unit_of<PAGED>(p, u, x)) continue;
         mbar_wait(q_full, un & 1);
         for (int j = 0; j < x.nkv; ++j, ++kt, ++gt) {
           const int sb = gt & 1;
@@ -234,9 +288,10 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t un = 0, gt = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
       Unit x;
-      if (!unit_of(p, u, x)) continue;
+      if (!unit_of<PAGED>(p, u, x)) continue;
       const int q0 = x.qt * FQ;
-      const int qi = q0 + row;  // query position of this thread's row
+      const int qi = q0 + row;      // row of this thread within the new span
+      const int qpos = x.prior + qi;  // its key-space position
       float m_run = -INFINITY, l = 0.f;
       for (int j = 0; j < x.nkv; ++j, ++gt) {
         const int sb = gt & 1;
@@ -250,12 +305,12 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[sb]);
         const int kbase = j * FK;
-        const bool need_mask = (kbase + FK - 1 > q0) || (kbase + FK > x.len);
+        const bool need_mask = (kbase + FK - 1 > x.prior + q0) || (kbase + FK > x.kvlen);
         float mx = -INFINITY;
 #pragma unroll
         for (int c = 0; c < 128; ++c) {
           float v = s[c] * p.scale_log2;
-          if (need_mask && (kbase + c > qi || kbase + c >= x.len)) v = -INFINITY;
+          if (need_mask && (kbase + c > qpos || kbase + c >= x.kvlen)) v = -INFINITY;
           s[c] = v;
           mx = fmaxf(mx, v);
         }
@@ -334,16 +389,16 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <int D>
+template <int D, bool PAGED>
 static int launch_fa(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const FaParams& p, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_fa_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_fa_tc<D, PAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(FaCfg<D>::SMEM)));
     attr = true;
   }
-  k_fa_tc<D><<<grid, 192, FaCfg<D>::SMEM, st>>>(tq, tk, tv, p);
+  k_fa_tc<D, PAGED><<<grid, 192, FaCfg<D>::SMEM, st>>>(tq, tk, tv, p);
   HP_LAUNCH_CHECK("k_fa_tc");
   return HP_OK;
 }
@@ -382,5 +437,46 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
   const int units = nseq * p.n_qt * Hq;
   const int grid = std::min(units, max_ctas);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d == 128 ? launch_fa<128>(tq, tk, tv, p, grid, st) : launch_fa<64>(tq, tk, tv, p, grid, st);
+  return d == 128 ? launch_fa<128, false>(tq, tk, tv, p, grid, st) : launch_fa<64, false>(tq, tk, tv, p, grid, st);
+}
+
+extern "C" int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache, const void* vcache,
+                                     const int* block_table, int max_pages, const int* cu_seqlens,
+                                     const int* prior_lens, int nseq, int total_tokens, int max_seqlen,
+                                     void* o, int ldo, int Hq, int Hkv, int d, int page, int num_blocks,
+                                     float scale, int max_ctas, void* stream) {
+  HP_CHECK_ARG(q && kcache && vcache && block_table && cu_seqlens && prior_lens && o,
+               "hp_prefill_attn_paged: null pointer");
+  HP_CHECK_ARG(d == 64 || d == 128, "hp_prefill_attn_paged: head_dim must be 64 or 128");
+  HP_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0, "hp_prefill_attn_paged: Hkv must divide Hq");
+  HP_CHECK_ARG(page >= 64 && page % 64 == 0, "hp_prefill_attn_paged: page must be a multiple of 64");
+  HP_CHECK_ARG(nseq >= 1 && max_seqlen >= 1 && total_tokens >= 1 && max_pages >= 1 && num_blocks >= 1,
+               "hp_prefill_attn_paged: empty batch");
+  HP_CHECK_ARG(max_ctas >= 1, "hp_prefill_attn_paged: max_ctas must be >= 1");
+  HP_CHECK_ARG(ldo % 8 == 0, "hp_prefill_attn_paged: output pitch must be a multiple of 8");
+  HP_CHECK_ARG((reinterpret_cast<uintptr_t>(kcache) & 15) == 0 && (reinterpret_cast<uintptr_t>(vcache) & 15) == 0,
+               "hp_prefill_attn_paged: caches must be 16-byte aligned");
+  CUtensorMap tq;
+  int rc = cached_tmap_bf16(&tq, q, uint64_t(total_tokens), uint64_t(Hq) * d, ldq, 128, 64, true);
+  if (rc) return rc;
+  FaParams p{};
+  p.cu_seqlens = cu_seqlens;
+  p.nseq = nseq;
+  p.n_qt = (max_seqlen + FQ - 1) / FQ;
+  p.Hq = Hq;
+  p.G = Hq / Hkv;
+  p.out = static_cast<__nv_bfloat16*>(o);
+  p.ldo = ldo;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.kc = static_cast<const __nv_bfloat16*>(kcache);
+  p.vc = static_cast<const __nv_bfloat16*>(vcache);
+  p.block_table = block_table;
+  p.prior_lens = prior_lens;
+  p.max_pages = max_pages;
+  p.page = page;
+  p.Hkv = Hkv;
+  const int units = nseq * p.n_qt * Hq;
+  const int grid = std::min(units, max_ctas);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return d == 128 ? launch_fa<128, true>(tq, tq, tq, p, grid, st) : launch_fa<64, true>(tq, tq, tq, p, grid, st);
 }

@@ -178,10 +178,74 @@ class B200Executor:
     def decode_step_s(self, es: ExecutionState) -> float:
         return self.model.num_layers * self._measure("decode", es)
 
+    def _hybrid_args(self, chunks, decode_ctx_lens):
+        """Device inputs of one hybrid batch: chunk rows first, then decode
+        rows; every sequence gets its own run of pool pages (mod pool size)."""
+        chunks = [(int(n), int(p)) for n, p in chunks]
+        ctxs = [int(c) for c in decode_ctx_lens]
+        Tc = sum(n for n, _ in chunks)
+        B = len(ctxs)
+        T = Tc + B
+        if T < 1:
+            raise InvalidArgumentError("hybrid batch is empty")
+        if T > self.max_prefill_tokens:
+            raise InvalidArgumentError(f"hybrid batch of {T} tokens exceeds max_prefill_tokens")
+        if B > self.max_decode_batch:
+            raise InvalidArgumentError(f"decode batch {B} exceeds max_decode_batch")
+        seqs = chunks + [(1, c - 1) for c in ctxs]
+        pages = [-(-(n + p) // PAGE) for n, p in seqs]
+        mp = max(pages)
+        bt = torch.zeros(len(seqs), mp, dtype=torch.int64)
+        pos, slots = [], []
+        nxt = 0
+        for i, ((n, p), pg) in enumerate(zip(seqs, pages)):
+            bt[i, :pg] = (torch.arange(pg) + nxt) % self.pool_blocks
+            nxt += pg
+            ps = torch.arange(p, p + n)
+            pos.append(ps)
+            slots.append(bt[i, ps // PAGE] * PAGE + ps % PAGE)
+        nc = len(chunks)
+        d = dict(device=self.dev, dtype=torch.int32)
+        offs = [0]
+        for n, _ in chunks:
+            offs.append(offs[-1] + n)
+        cu = torch.tensor(offs, **d)
+        return dict(T=T, Tc=Tc, cu=cu, max_chunk=max([n for n, _ in chunks] or [1]),
+                    prior=torch.tensor([p for _, p in chunks] or [0], **d),
+                    cbt=bt[:max(nc, 1)].to(**d), dctx=torch.tensor(ctxs or [1], **d),
+                    dbt=bt[nc:].to(**d) if B else bt[:1].to(**d),
+                    pos=torch.cat(pos).to(**d), slots=torch.cat(slots).to(**d))
+
+    def _launch_hybrid(self, st, a):
+        T = a["T"]
+        self.layer.hybrid(self.px[:T], self.py[:T], self.psc, self.dsc, a["Tc"], a["cu"], a["cu"].shape[0] - 1,
+                          a["max_chunk"], a["prior"], a["cbt"], a["dctx"], a["dbt"], a["pos"], a["slots"],
+                          self.dcache, st.sms, st.torch_stream)
+
     def hybrid_iteration_s(self, chunks, decode_ctx_lens, sms: int) -> float:
-        raise lib.HotPathError(
-            "hybrid (chunked-prefill) iterations need prefix-aware prefill attention "
-            "(prior_lens); not built yet -- SURVEY.md section 8(f) next #1")
+        """One lockstep hybrid iteration (all layers) on `sms` SMs -- the
+        chunked-prefill baseline's device call (reference engine.py:200-208,
+        issued by _ChunkedSim._start_iteration engine.py:795-797).  Measured
+        as one hybrid layer (prefix-aware paged prefill attention for the
+        chunks, paged decode attention for the decode rows, GEMMs over the
+        concatenated stream) times `model.num_layers`."""
+        a = self._hybrid_args(chunks, decode_ctx_lens)
+        st = self.pool.phase(PREFILL, sms)
+        key = ("hybrid", sms, tuple(chunks), tuple(decode_ctx_lens))
+        if key not in self._warm:
+            with torch.cuda.stream(st.torch_stream):
+                self._launch_hybrid(st, a)
+            torch.cuda.synchronize(self.dev)
+            self._warm.add(key)
+        a_ev, b_ev = _ev(), _ev()
+        with torch.cuda.stream(st.torch_stream):
+            torch.cuda._sleep(400_000)
+            a_ev.record(st.torch_stream)
+            self._launch_hybrid(st, a)
+            b_ev.record(st.torch_stream)
+        torch.cuda.synchronize(self.dev)
+        self.calls["hybrid"] = self.calls.get("hybrid", 0) + 1
+        return self.model.num_layers * a_ev.elapsed_time(b_ev) * 1e-3
 
     def alpha(self, phase: str, sms: int, tokens: int) -> float:
         """Measured / SRM at a canonical shape of `tokens` on `sms` SMs."""

@@ -237,6 +237,56 @@ class DeviceLayer:
         return 9
 
 
+    # --------------------------------------------------------------- hybrid
+    def hybrid(self, x, y, sc: PrefillScratch, dsc: DecodeScratch, n_chunk_tokens: int, cu_chunks,
+               n_chunks: int, max_chunk: int, prior_lens, chunk_block_table, dec_ctx_lens, dec_block_table,
+               positions, slots, cache: KVCache, sms: int, stream=None) -> int:
+        """One layer over a hybrid batch (the lockstep chunked-prefill
+        baseline; reference hybrid_kernels workload.py:213-257): rows
+        [0, n_chunk_tokens) of x are prefill-chunk tokens of `n_chunks`
+        sequences (offsets cu_chunks, cached prefixes prior_lens, pages
+        chunk_block_table), the remaining B rows are decode tokens (contexts
+        dec_ctx_lens incl. the new token, pages dec_block_table).  The four
+        linear kernels run once over the concatenated stream; attention is
+        prefix-aware paged prefill attention for the chunks plus paged decode
+        attention for the decode rows.  positions/slots cover all rows.
+        Returns the launch count."""
+        T = x.shape[0]
+        Tc = n_chunk_tokens
+        B = T - Tc
+        Hq, Hkv, d = self.Hq, self.Hkv, self.d
+        qkv = sc.qkv[:T]
+        swap = T <= dsc.max_batch
+
+        def linear(inp, w, out, epi, resid=None):
+            if swap:
+                lib.gemm_swap(inp, w, out, dsc.gemm_ws, dsc.gemm_cnt, epi, resid=resid, max_ctas=sms,
+                              stream=stream)
+            else:
+                lib.gemm(inp, w, out, epi, resid=resid, max_ctas=sms, stream=stream)
+
+        n = 0
+        lib.rmsnorm(x, self.W.attn_norm, sc.xn[:T], EPS, sms, stream)
+        linear(sc.xn[:T], self.W.w_qkv, qkv, lib.EPI_STORE)
+        lib.rope_kv_write(qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k, cache.v, cache.page,
+                          max_ctas=sms, stream=stream)
+        n += 3
+        if Tc > 0:
+            lib.prefill_attn_paged(qkv[:Tc, : Hq * d], cache.k, cache.v, chunk_block_table, cu_chunks,
+                                   prior_lens, n_chunks, max_chunk, sc.attn[:Tc], Hq, Hkv, d, cache.page,
+                                   self.scale, max_ctas=sms, stream=stream)
+            n += 1
+        if B > 0:
+            lib.decode_attn(qkv[Tc:], cache.k, cache.v, dec_block_table, dec_ctx_lens, sc.attn[Tc:T], Hq,
+                            Hkv, d, cache.page, self.scale, ws=dsc.attn_ws, max_ctas=sms, stream=stream)
+            n += 1
+        linear(sc.attn[:T], self.W.w_o, sc.h[:T], lib.EPI_RESID, resid=x)
+        lib.rmsnorm(sc.h[:T], self.W.mlp_norm, sc.xn[:T], EPS, sms, stream)
+        linear(sc.xn[:T], self.W.w_ug, sc.act[:T], lib.EPI_SILU)
+        linear(sc.act[:T], self.W.w_down, y, lib.EPI_RESID, resid=sc.h[:T])
+        return n + 4
+
+
 def decode_slots(block_table: torch.Tensor, ctx_lens: torch.Tensor, page: int = PAGE):
     """positions = ctx-1 and cache slots of each sequence's newest token."""
     pos = (ctx_lens - 1).to(torch.int64)

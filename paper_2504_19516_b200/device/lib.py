@@ -39,6 +39,8 @@ SIGNATURES = {
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
+    "hp_prefill_attn_paged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _i, _i, _i, _f,
+                                   _i, _p]),
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_decode_attn": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _f, _p, _sz, _i, _p]),
     "hp_probe": (_i, [_i, _i, _i64, _p, _p]),
@@ -179,6 +181,17 @@ def prefill_attn(q, k, v, o, cu_seqlens, nseq: int, max_seqlen: int, Hq: int, Hk
     check(load().hp_prefill_attn(_ptr(q), q.stride(0), _ptr(k), k.stride(0), _ptr(v), v.stride(0),
                                  _ptr(o), o.stride(0), _ptr(cu_seqlens), nseq, q.shape[0], max_seqlen, Hq, Hkv,
                                  d, scale, max_ctas, _stream(stream)), "hp_prefill_attn")
+
+
+def prefill_attn_paged(q, kcache, vcache, block_table, cu_seqlens, prior_lens, nseq: int, max_seqlen: int,
+                       o, Hq: int, Hkv: int, d: int, page: int, scale: float, max_ctas: int = 148,
+                       stream=None) -> None:
+    """Chunked-prefill attention: new tokens (rows of q) over cached prefix + span."""
+    check(load().hp_prefill_attn_paged(_ptr(q), q.stride(0), _ptr(kcache), _ptr(vcache), _ptr(block_table),
+                                       block_table.shape[1], _ptr(cu_seqlens), _ptr(prior_lens), nseq,
+                                       q.shape[0], max_seqlen, _ptr(o), o.stride(0), Hq, Hkv, d, page,
+                                       kcache.shape[0], scale, max_ctas, _stream(stream)),
+          "hp_prefill_attn_paged")
 
 
 def decode_attn_ws_bytes(B: int, Hq: int, d: int, max_splits: int) -> int:

@@ -83,6 +83,26 @@ class DeviceModel:
             x = y
         return x
 
+    def hybrid(self, tokens: torch.Tensor, n_chunk_tokens: int, cu_chunks: torch.Tensor, max_chunk: int,
+               prior_lens: torch.Tensor, chunk_block_table: torch.Tensor, dec_ctx_lens: torch.Tensor,
+               dec_block_table: torch.Tensor, positions: torch.Tensor, slots: torch.Tensor, sms: int,
+               stream=None, hidden_out: list | None = None) -> torch.Tensor:
+        """One lockstep hybrid iteration through all layers (the chunked-prefill
+        baseline, reference _ChunkedSim engine.py:741-800): prefill-chunk rows
+        first, then one row per decode sequence.  Returns final hidden [T, h]."""
+        T = tokens.shape[0]
+        x = self.buf[0][:T]
+        torch.index_select(self.embed, 0, tokens.long(), out=x)
+        n_chunks = cu_chunks.shape[0] - 1
+        for i, (lyr, cache) in enumerate(zip(self.layers, self.caches)):
+            y = self.buf[(i + 1) % 2][:T]
+            lyr.hybrid(x, y, self.psc, self.dsc, n_chunk_tokens, cu_chunks, n_chunks, max_chunk, prior_lens,
+                       chunk_block_table, dec_ctx_lens, dec_block_table, positions, slots, cache, sms, stream)
+            if hidden_out is not None:
+                hidden_out.append(y.clone())
+            x = y
+        return x
+
     def logits_of(self, hidden: torch.Tensor, sms: int, stream=None) -> torch.Tensor:
         n = hidden.shape[0]
         lib.rmsnorm(hidden, self.final_norm, self.norm_out[:n], EPS, sms, stream)

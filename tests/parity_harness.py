@@ -257,3 +257,131 @@ def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, dev
                                                       kc[bt[b, (c - 1) // PAGE], :, (c - 1) % PAGE]))
                                         for b, c in enumerate(ctxs)))
     return res
+
+
+def run_tiny_chunked(seed: int = 0, chunk_budget: int = 512, decode_steps: int = 6, device: int = 0) -> dict:
+    """Config 1 through the lockstep chunked-prefill path (hybrid batches,
+    reference _ChunkedSim engine.py:741-800 / hybrid_kernels workload.py:
+    213-257) on the device vs the oracle's `layer_hybrid`.
+
+    The 9 prompts of `run_tiny` are admitted FIFO; every iteration packs the
+    running decode tokens first, then prompt chunks up to `chunk_budget`
+    tokens (so chunks carry cached prefixes and several sequences share an
+    iteration).  A prompt's completion emits its greedy token (teacher-forced
+    on the oracle's) and the sequence decodes `decode_steps` more tokens."""
+    import torch
+
+    from paper_2504_19516_b200.device.layer import LayerWeights
+    from paper_2504_19516_b200.device.model import DeviceModel
+
+    vocab = 1024
+    m, Wl, embed, final_norm, lm_head = tiny_weights(seed, vocab)
+    dev = torch.device("cuda", device)
+    rng = np.random.default_rng(seed + 1)
+    prompts = [rng.integers(0, vocab, 1024)] + [rng.integers(0, vocab, c) for c in TINY_CTX]
+    lens = [len(p) for p in prompts]
+    nseq = len(prompts)
+    need = [-(-(L + decode_steps + 2) // PAGE) for L in lens]
+    nblk = sum(need) + 5
+    perm = rng.permutation(nblk)
+    max_pages = max(need)
+    bt = np.zeros((nseq, max_pages), dtype=np.int32)
+    k = 0
+    for i, nb in enumerate(need):
+        bt[i, :nb] = perm[k:k + nb]
+        k += nb
+
+    def t(a, dt=torch.bfloat16):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(dev)
+
+    dW = [LayerWeights.from_numpy(dev, w.w_qkv, w.w_o, w.w_gate, w.w_up, w.w_down, w.attn_norm,
+                                  w.mlp_norm) for w in Wl]
+    dm = DeviceModel(m, vocab, nblk, dev, weights=dW, embed=t(embed), final_norm=t(final_norm),
+                     lm_head=t(lm_head), max_prefill_tokens=chunk_budget, max_batch=nseq,
+                     max_pages=max_pages)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    d, Hq, Hkv = m.head_dim, m.num_heads, m.num_kv_heads
+    table = O.rope_table(4096, d)
+    kc = [np.zeros((nblk, Hkv, PAGE, d), np.float32) for _ in range(m.num_layers)]
+    vc = [np.zeros((nblk, Hkv, PAGE, d), np.float32) for _ in range(m.num_layers)]
+
+    progress = [0] * nseq
+    queue = list(range(nseq))
+    running: list[int] = []       # decoding sequences
+    ctx = [0] * nseq              # tokens in cache incl. the pending one (decoders)
+    last_tok = [0] * nseq
+    emitted = [0] * nseq
+    stats = {"iterations": 0, "max_chunks_per_iter": 0, "chunks_with_prefix": 0, "excess": [],
+             "matches": 0, "mismatches": 0, "tie_flips": 0, "near_ties": 0}
+    while queue or running:
+        dec = list(running)
+        budget = chunk_budget - len(dec)
+        chunks = []  # (seq, take, prior)
+        for sid in list(queue):
+            if budget <= 0:
+                break
+            take = min(budget, lens[sid] - progress[sid])
+            chunks.append((sid, take, progress[sid]))
+            budget -= take
+        toks = [prompts[s][p:p + n] for s, n, p in chunks] + [np.array([last_tok[s]]) for s in dec]
+        tokens = np.concatenate(toks).astype(np.int32)
+        seqs = [(n, p) for _, n, p in chunks] + [(1, ctx[s] - 1) for s in dec]
+        rows_bt = bt[[s for s, _, _ in chunks] + dec]
+        pos = np.concatenate([np.arange(p, p + n) for n, p in seqs]).astype(np.int32)
+        slots = np.concatenate([rows_bt[i, np.arange(p, p + n) // PAGE] * PAGE + np.arange(p, p + n) % PAGE
+                                for i, (n, p) in enumerate(seqs)]).astype(np.int32)
+        Tc = sum(n for _, n, _ in chunks)
+        cu = np.concatenate([[0], np.cumsum([n for _, n, _ in chunks])]).astype(np.int32)
+        prior = np.array([p for _, _, p in chunks] or [0], dtype=np.int32)
+        cbt = bt[[s for s, _, _ in chunks]] if chunks else bt[:1]
+        dbt = bt[dec] if dec else bt[:1]
+        dctx = np.array([ctx[s] for s in dec] or [1], dtype=np.int32)
+        hid = dm.hybrid(t(tokens, torch.int32), Tc, t(cu, torch.int32), max([n for _, n, _ in chunks] or [1]),
+                        t(prior, torch.int32), t(cbt, torch.int32), t(dctx, torch.int32), t(dbt, torch.int32),
+                        t(pos, torch.int32), t(slots, torch.int32), sms)
+        dh = hid.float().cpu().numpy()
+        x = embed[tokens]
+        for li, W in enumerate(Wl):
+            x = O.layer_hybrid(x, W, Hq, Hkv, d, seqs, table, kc[li], vc[li], rows_bt, bf16_boundaries=True)
+        stats["excess"].append(excess(dh, x))
+        stats["iterations"] += 1
+        stats["max_chunks_per_iter"] = max(stats["max_chunks_per_iter"], len(chunks))
+        stats["chunks_with_prefix"] += sum(1 for _, _, p in chunks if p > 0)
+        # rows whose next token is sampled: completed prompts and decoders
+        emit_rows, emit_seqs = [], []
+        r = 0
+        for s, n, p in chunks:
+            r += n
+            progress[s] += n
+            if progress[s] == lens[s]:
+                emit_rows.append(r - 1)
+                emit_seqs.append(s)
+                queue.remove(s)
+        for j, s in enumerate(dec):
+            emit_rows.append(Tc + j)
+            emit_seqs.append(s)
+        if emit_rows:
+            idx = torch.tensor(emit_rows, device=dev, dtype=torch.long)
+            dl = dm.logits_of(hid[idx].contiguous(), sms).float().cpu().numpy()
+            rt, mg, lg = O.greedy_tokens(x[emit_rows], final_norm, lm_head)
+            for rr, dv, g, l in zip(rt, dl.argmax(-1), mg, lg):
+                tie = g <= MARGIN_ULPS * _ulp_bf16(np.max(l))
+                stats["near_ties"] += int(tie)
+                if rr == dv:
+                    stats["matches"] += 1
+                elif tie:
+                    stats["tie_flips"] += 1
+                else:
+                    stats["mismatches"] += 1
+            for s, tok in zip(emit_seqs, rt):
+                last_tok[s] = int(tok)
+                emitted[s] += 1
+                if s not in running:
+                    running.append(s)
+                    ctx[s] = lens[s] + 1
+                else:
+                    ctx[s] += 1
+        running = [s for s in running if emitted[s] <= decode_steps]
+    stats["max_excess"] = max(stats["excess"])
+    del stats["excess"]
+    return stats

@@ -56,3 +56,19 @@ def test_engine_runs_on_measured_latencies(ex):
     for entry in rep.decision_log:
         assert entry["dm"] % 8 == 0 or entry["dm"] == gpu.num_sms
     assert ex.calls["prefill"] > 0 and ex.calls["decode"] > 0
+
+
+def test_hybrid_iteration_and_chunked_policy_on_hardware(ex):
+    # GroundTruthOracle.hybrid_iteration_s (engine.py:200-208) measured on the B200
+    t1 = ex.hybrid_iteration_s([(1024, 0)], [], 148)
+    t2 = ex.hybrid_iteration_s([(1024, 3072)], [2048] * 32, 148)
+    t3 = ex.hybrid_iteration_s([], [1024] * 16, 148)
+    assert 0 < t3 < t1 < t2
+    gpu = b200_spec()
+    cfg = E.SimConfig(gpu=gpu, model=MODEL_PRESETS["llama3-8b"],
+                      slo=S.SloSpec(norm_ttft_s_per_token=1.5e-3, tpot_s=0.1),
+                      policy=E.PolicySpec(name="chunked", chunk_size=1024), seed=0)
+    trace = [Request(i, 0.002 * i, 512 + 256 * i, 4) for i in range(6)]
+    rep = E.run(cfg, trace, oracle=ex)
+    assert rep.aggregates["finished"] == len(trace)
+    assert ex.calls["hybrid"] > 0

@@ -298,3 +298,82 @@ def test_partition_confinement_under_graph_replay():
     sms = set(buf[:, 0].tolist())
     assert len(sms) <= 24, sorted(sms)
     part.close()
+
+
+# --------------------------------------------------- paged prefill attention
+def _paged_ref(q, kc_logical, vc_logical, bt, lens, priors, scale, G):
+    """fp32 reference: sequence s's rows attend cache positions <= prior+i."""
+    outs = []
+    r0 = 0
+    page = kc_logical.shape[2]
+    for s, (n, p) in enumerate(zip(lens, priors)):
+        L = p + n
+        pages = bt[s, : -(-L // page)].long()
+        k = kc_logical[pages].permute(0, 2, 1, 3).reshape(-1, kc_logical.shape[1], kc_logical.shape[3])[:L]
+        v = vc_logical[pages].permute(0, 2, 1, 3).reshape(-1, vc_logical.shape[1], vc_logical.shape[3])[:L]
+        qs = q[r0:r0 + n].float()
+        kk = k.float().repeat_interleave(G, dim=1)
+        vv = v.float().repeat_interleave(G, dim=1)
+        sc = torch.einsum("thd,lhd->htl", qs, kk) * scale
+        mask = torch.arange(L, device=DEV)[None, :] <= (p + torch.arange(n, device=DEV))[:, None]
+        sc = sc.masked_fill(~mask[None], float("-inf"))
+        outs.append(torch.einsum("htl,lhd->thd", sc.softmax(-1), vv))
+        r0 += n
+    return torch.cat(outs)
+
+
+@pytest.mark.parametrize("d,Hq,Hkv,lens,priors", [
+    (128, 32, 8, [384, 77, 1], [0, 1000, 4095]),
+    (128, 32, 8, [1024], [2048]),
+    (64, 4, 2, [200, 129, 64], [17, 0, 300]),
+    (64, 4, 2, [1], [0]),
+])
+def test_prefill_attn_paged(d, Hq, Hkv, lens, priors, gen):
+    page = 64
+    G = Hq // Hkv
+    need = [-(-(n + p) // page) for n, p in zip(lens, priors)]
+    nblk = sum(need) + 3
+    perm = torch.randperm(nblk, generator=torch.Generator().manual_seed(5))
+    bt = torch.zeros(len(lens), max(need), dtype=torch.int32)
+    k = 0
+    for i, nb in enumerate(need):
+        bt[i, :nb] = perm[k:k + nb]
+        k += nb
+    bt = bt.to(DEV)
+    kc = bf((nblk, Hkv, page, d), gen=gen)
+    vc = bf((nblk, Hkv, page, d), gen=gen)
+    T = sum(lens)
+    q = bf((T, Hq * d), gen=gen)
+    o = torch.empty(T, Hq * d, device=DEV, dtype=torch.bfloat16)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), dtype=torch.int32, device=DEV)
+    pr = torch.tensor(priors, dtype=torch.int32, device=DEV)
+    scale = 1 / math.sqrt(d)
+    lib.prefill_attn_paged(q, lib.kv_pack(kc), lib.kv_pack(vc), bt, cu, pr, len(lens), max(lens), o, Hq, Hkv,
+                           d, page, scale, max_ctas=148)
+    ref = _paged_ref(q.view(T, Hq, d), kc, vc, bt, lens, priors, scale, G).reshape(T, Hq * d)
+    assert rel_err(o, ref) < 2e-2
+
+
+def test_prefill_attn_paged_matches_dense_without_prefix(gen):
+    # prior_lens = 0: the paged path must agree with the dense (qkv-view) kernel
+    from paper_2504_19516_b200.device.layer import KVCache
+
+    T, Hq, Hkv, d, page = 700, 32, 8, 128, 64
+    qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
+    q, kk, vv = qkv[:, :Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
+    cu = torch.tensor([0, T], dtype=torch.int32, device=DEV)
+    o_dense = torch.empty(T, Hq * d, device=DEV, dtype=torch.bfloat16)
+    lib.prefill_attn(q, kk, vv, o_dense, cu, 1, T, Hq, Hkv, d, 1 / math.sqrt(d), max_ctas=148)
+    pages = -(-T // page)
+    cache = KVCache(pages, Hkv, d, DEV)
+    kl = torch.zeros(pages * page, Hkv, d, device=DEV, dtype=torch.bfloat16)
+    vl = torch.zeros_like(kl)
+    kl[:T] = kk.reshape(T, Hkv, d)
+    vl[:T] = vv.reshape(T, Hkv, d)
+    cache.k.copy_(lib.kv_pack(kl.view(pages, page, Hkv, d).permute(0, 2, 1, 3).contiguous()))
+    cache.v.copy_(lib.kv_pack(vl.view(pages, page, Hkv, d).permute(0, 2, 1, 3).contiguous()))
+    bt = torch.arange(pages, dtype=torch.int32, device=DEV)[None]
+    o_paged = torch.empty_like(o_dense)
+    lib.prefill_attn_paged(q, cache.k, cache.v, bt, cu, torch.zeros(1, dtype=torch.int32, device=DEV), 1, T,
+                           o_paged, Hq, Hkv, d, page, 1 / math.sqrt(d), max_ctas=148)
+    assert torch.equal(o_paged, o_dense)

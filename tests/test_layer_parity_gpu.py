@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from parity_harness import ATOL, run_llama_layer, run_tiny  # noqa: E402
+from parity_harness import ATOL, run_llama_layer, run_tiny, run_tiny_chunked  # noqa: E402
 
 
 def test_tiny_model_config1_prefill_and_greedy_decode():
@@ -38,3 +38,14 @@ def test_llama3_8b_layer_ragged_prefill_tail():
     r = run_llama_layer(T=333, B=3, ctx=65, seed=3)
     assert r["prefill_excess"] <= ATOL, r
     assert r["decode_excess"] <= ATOL, r
+
+
+@pytest.mark.parametrize("budget", [512, 200])
+def test_tiny_model_chunked_prefill_hybrid_batches(budget):
+    # lockstep hybrid batches (chunks with cached prefixes + decode rows),
+    # reference _ChunkedSim engine.py:741-800, hybrid_kernels workload.py:213-257
+    r = run_tiny_chunked(seed=0, chunk_budget=budget, decode_steps=6)
+    assert r["max_excess"] <= ATOL, r
+    assert r["mismatches"] == 0, r
+    assert r["chunks_with_prefix"] >= 2 and r["max_chunks_per_iter"] >= 2, r
+    assert r["tie_flips"] <= 2, r

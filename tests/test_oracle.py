@@ -148,3 +148,42 @@ def test_decode_step_consistent_with_prefill():
     yd = O.layer_decode(x[T - 1:], W, Hq, Hkv, d, np.array([T]), table, kc, vc, np.array([[0, 1]]),
                         bf16_boundaries=False)
     assert np.max(np.abs(yd[0] - y[T - 1])) < 1e-4
+
+
+def _tiny_layer(rng, h=64, Hq=4, Hkv=2, d=16, inter=96):
+    def w(*s):
+        return O.bf16_round((rng.normal(size=s) * 0.05).astype(np.float32))
+
+    return O.LayerWeights(w((Hq + 2 * Hkv) * d, h), w(h, h), w(inter, h), w(inter, h), w(h, inter),
+                          O.bf16_round(1 + 0.1 * rng.normal(size=h).astype(np.float32)),
+                          O.bf16_round(1 + 0.1 * rng.normal(size=h).astype(np.float32))), Hq, Hkv, d
+
+
+def test_layer_hybrid_chunked_equals_unchunked_prefill_and_decode():
+    # hybrid_kernels (workload.py:213-257): splitting a prompt into chunks with
+    # cached prefixes, and packing decode rows beside them, changes nothing
+    rng = np.random.default_rng(7)
+    W, Hq, Hkv, d = _tiny_layer(rng)
+    page, T = 8, 45
+    table = O.rope_table(128, d)
+    x = O.bf16_round(rng.normal(size=(T, 64)).astype(np.float32))
+    ref, _, _ = O.layer_prefill(x, W, Hq, Hkv, d, np.arange(T), table, bf16_boundaries=False)
+    nblk = 20
+    bt = rng.permutation(nblk)[None, :8]
+    kc = np.zeros((nblk, Hkv, page, d), np.float32)
+    vc = np.zeros_like(kc)
+    parts = []
+    for p, n in [(0, 13), (13, 20), (33, 12)]:
+        parts.append(O.layer_hybrid(x[p:p + n], W, Hq, Hkv, d, [(n, p)], table, kc, vc, bt,
+                                    bf16_boundaries=False))
+    np.testing.assert_allclose(np.concatenate(parts), ref, atol=2e-5, rtol=1e-4)
+    # a decode row (1, ctx-1) beside a chunk equals layer_decode on the same cache
+    xd = O.bf16_round(rng.normal(size=(1, 64)).astype(np.float32))
+    kc2, vc2 = kc.copy(), vc.copy()
+    bt2 = np.stack([bt[0], rng.permutation(np.arange(8, 20))[:8]])
+    xc = O.bf16_round(rng.normal(size=(5, 64)).astype(np.float32))
+    hyb = O.layer_hybrid(np.concatenate([xc, xd]), W, Hq, Hkv, d, [(5, 0), (1, T)], table, kc, vc,
+                         bt2[::-1].copy(), bf16_boundaries=False)
+    dec = O.layer_decode(xd, W, Hq, Hkv, d, np.array([T + 1]), table, kc2, vc2, bt2[:1],
+                         bf16_boundaries=False)
+    np.testing.assert_allclose(hyb[5:], dec, atol=2e-5, rtol=1e-4)
