@@ -308,6 +308,26 @@ def main(argv=None) -> int:
     # ---- time-sliced baseline (same kernels, full GPU, alternating)
     ts_eq = cr.time_sliced(args.steps, n)  # equal work
 
+    # ---- chunked-prefill baseline (lockstep hybrid batches, SGLang-1024/2048
+    # analogue; reference _ChunkedSim engine.py:741-800) on the same kernels
+    chunked = [cr.chunked(c, reps=max(1, min(3, args.steps))) for c in (1024, 2048)]
+
+    # ---- SM idle: partition-level (SM-time with no work in either partition)
+    # and the wave model's intra-kernel idle of the prefill layer on pm SMs
+    from paper_2504_19516_b200.device import lib as hplib
+    from paper_2504_19516_b200.perf_model import wave_stats
+
+    wl = cr.layer.W
+    units = {"qkv": hplib.gemm_tiles(T, wl.w_qkv.shape[0]), "o_proj": hplib.gemm_tiles(T, wl.w_o.shape[0]),
+             "mlp_up_gate": hplib.gemm_tiles(T, wl.w_ug.shape[0]),
+             "mlp_down": hplib.gemm_tiles(T, wl.w_down.shape[0]),
+             "attn": min(-(-T // 128) * model.num_heads, pm)}
+    g_s = res.group_s
+    wave_idle = sum(g_s[g] * wave_stats(units[g], 1, pm).idle_ratio for g in units) / sum(g_s.values())
+
+    # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
+    dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}
+
     # ---- roofline of the dominant kernel (mlp_up_gate GEMM, tensor-bound)
     ug = statistics.mean(res.upgate_s)
     achieved = cr.upgate_flops() / ug / 1e12
@@ -352,11 +372,17 @@ def main(argv=None) -> int:
                             "p50_tpot_us": 1e6 * ts_tpot},
             "equal_work": {"tokens_per_s": ts_eq.tokens_per_s, "span_ratio": ts_eq.span_s / res.span_s},
         },
+        "chunked_baseline": chunked,
+        "sm_idle_pct": {"partition": 100 * res.partition_idle(N), "wave_model_prefill_layer": 100 * wave_idle,
+                        "prefill_group_us": {g: 1e6 * v for g, v in g_s.items()}},
         "split_sweep": candidates,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "mlp_up_gate (tcgen05 GEMM + SiLU)",
                      "peak_basis": f"bf16_tflops burst ({peak_src}) x pm/N = {tf_burst} x {pm}/{N}",
                      "frac_of_full_gpu_peak": achieved / tf_burst},
+        "roofline_decode_attn": {"bound": "hbm", "unit": "GB/s", "peak": hbm_gbs,
+                                 "bytes_per_launch": cr.decode_attn_bytes(),
+                                 **{k: {"achieved": v, "frac": v / hbm_gbs} for k, v in dattn.items()}},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_tokens / e2e_span, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

@@ -32,6 +32,9 @@ from .layer import (PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights, Pre
 from .partition import DECODE, PREFILL, PartitionPool, PhaseStreams
 
 
+GROUPS = ("qkv", "attn", "o_proj", "mlp_up_gate", "mlp_down")
+
+
 def _ev():
     return torch.cuda.Event(enable_timing=True)
 
@@ -48,6 +51,13 @@ class CoRunResult:
     prefill_layer_s: list = field(default_factory=list)   # per prefill layer
     decode_layer_s: list = field(default_factory=list)    # per decode layer-step
     upgate_s: list = field(default_factory=list)          # dominant kernel launches
+    group_s: dict = field(default_factory=dict)           # median seconds per prefill kernel group
+
+    def partition_idle(self, n: int) -> float:
+        """SM idle fraction of the co-run: 1 - (pm * prefill busy + dm *
+        decode busy) / (N * span) -- SM-time no partition had work for."""
+        busy = self.pm * sum(self.prefill_layer_s) + self.dm * sum(self.decode_layer_s)
+        return max(0.0, 1.0 - busy / (n * self.span_s))
 
     @property
     def tokens(self) -> int:
@@ -89,7 +99,10 @@ class CoRunner:
         # decode workload: B sequences of context C over a shuffled block pool
         pages = -(-self.C // PAGE)
         nblk = self.B * pages
-        self.dcache = KVCache(nblk, model.num_kv_heads, model.head_dim, self.dev)
+        # one page pool: decode sequences use the first B*pages blocks; the
+        # chunked baseline's prefill sequence uses the last pblocks
+        self.dcache = KVCache(nblk + pblocks, model.num_kv_heads, model.head_dim, self.dev)
+        self.chunk_pages = torch.arange(nblk, nblk + pblocks, dtype=torch.int32, device=self.dev)[None]
         self.dcache.k.normal_(generator=None)
         self.dcache.v.normal_(generator=None)
         perm = torch.randperm(nblk, generator=gen).to(torch.int32)
@@ -162,7 +175,7 @@ class CoRunner:
         ctrl = torch.cuda.current_stream(self.dev)
         start, end_p, end_d = _ev(), _ev(), _ev()
         p_ev = [(_ev(), _ev()) for _ in range(steps)]
-        ug_ev = [{"mlp_up_gate": (_ev(), _ev())} for _ in range(steps)] if time_upgate else None
+        ug_ev = ([{g: (_ev(), _ev()) for g in GROUPS} for _ in range(steps)] if time_upgate else None)
         d_ev = [(_ev(), _ev()) for _ in range(steps * decode_per_step)]
         torch.cuda._sleep(400_000)
         start.record(ctrl)
@@ -199,6 +212,8 @@ class CoRunner:
         res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
         if ug_ev:
             res.upgate_s = [a.elapsed_time(b) * 1e-3 for a, b in (e["mlp_up_gate"] for e in ug_ev)]
+            res.group_s = {g: statistics.median(e[g][0].elapsed_time(e[g][1]) * 1e-3 for e in ug_ev)
+                           for g in GROUPS}
         return res
 
     def corun_e2e(self, pm: int, dm: int, steps: int, decode_per_step: int, host_px, host_py,
@@ -286,6 +301,88 @@ class CoRunner:
         res.prefill_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in p_ev]
         res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
         return res
+
+    def chunked(self, chunk: int, reps: int = 1) -> dict:
+        """The lockstep chunked-prefill baseline (reference _ChunkedSim,
+        engine.py:741-800; SGLang-style hybrid batches) on real kernels, full
+        GPU: every iteration carries the B decode tokens plus the next
+        chunk - B tokens of the T-token prompt (prefix-aware attention over
+        the chunks already cached).  Returns layer-level tokens/s, TTFT (all
+        iterations until the prompt is done) and TPOT (median iteration)."""
+        st = self.pool.full(PREFILL)
+        take = max(1, chunk - self.B)
+        plan = []
+        p = 0
+        while p < self.T:
+            n = min(take, self.T - p)
+            plan.append((n, p))
+            p += n
+        dev = self.dev
+        i32 = dict(dtype=torch.int32, device=dev)
+        args = []
+        for n, p in plan:
+            tot = n + self.B
+            pos = torch.cat([torch.arange(p, p + n, **i32), self.d_pos])
+            slots = torch.cat([self.chunk_pages[0, torch.arange(p, p + n, device=dev) // PAGE] * PAGE
+                               + torch.arange(p, p + n, **i32) % PAGE, self.d_slots])
+            args.append((tot, n, torch.tensor([0, n], **i32), torch.tensor([p], **i32), pos, slots))
+        xb = torch.randn(max(a[0] for a in args), self.model.hidden, device=dev).to(torch.bfloat16)
+        yb = torch.empty_like(xb)
+
+        def run_iter(a):
+            tot, n, cu, prior, pos, slots = a
+            self.layer.hybrid(xb[:tot], yb[:tot], self.psc, self.dsc, n, cu, 1, n, prior, self.chunk_pages,
+                              self.ctx, self.block_table, pos, slots, self.dcache, st.sms, st.torch_stream)
+
+        with torch.cuda.stream(st.torch_stream):
+            for a in args:  # warm (tensor maps)
+                run_iter(a)
+        torch.cuda.synchronize()
+        evs = []
+        with torch.cuda.stream(st.torch_stream):
+            torch.cuda._sleep(400_000)
+            for _ in range(reps):
+                for a in args:
+                    e0, e1 = _ev(), _ev()
+                    e0.record(st.torch_stream)
+                    run_iter(a)
+                    e1.record(st.torch_stream)
+                    evs.append((e0, e1))
+        torch.cuda.synchronize()
+        it = [a.elapsed_time(b) * 1e-3 for a, b in evs]
+        per_prompt = sum(it) / reps
+        tokens = (self.T + self.B * len(plan))
+        return {"chunk": chunk, "iterations_per_prompt": len(plan), "tokens_per_s": tokens / per_prompt,
+                "ttft_us": 1e6 * per_prompt, "tpot_p50_us": 1e6 * statistics.median(it)}
+
+    def decode_attn_bytes(self) -> int:
+        """Algorithmic HBM bytes of one decode-attention launch (workload.py:
+        184-188): K+V over every context, the new token's K/V, q and out."""
+        m = self.model
+        kv_dim = m.num_kv_heads * m.head_dim
+        return self.B * (self.C * 2 * kv_dim * 2 + 2 * kv_dim * 2 + 2 * m.hidden * 2)
+
+    def decode_attn_gbs(self, sms: int, reps: int = 10) -> float:
+        """Decode attention alone on `sms` SMs (median of reps; the 269 MB KV
+        stream exceeds L2, so each launch reads HBM), GB/s algorithmic."""
+        st = self.pool.phase(DECODE, sms)
+        m = self.model
+        qkv = self.dsc.qkv[:self.B]
+        evs = []
+        with torch.cuda.stream(st.torch_stream):
+            for i in range(reps + 1):
+                torch.cuda._sleep(50_000)
+                a, b = _ev(), _ev()
+                a.record(st.torch_stream)
+                lib.decode_attn(qkv, self.dcache.k, self.dcache.v, self.block_table, self.ctx,
+                                self.dsc.attn[:self.B], m.num_heads, m.num_kv_heads, m.head_dim, PAGE,
+                                self.layer.scale, ws=self.dsc.attn_ws, max_ctas=st.sms, stream=st.torch_stream)
+                b.record(st.torch_stream)
+                if i:
+                    evs.append((a, b))
+        torch.cuda.synchronize()
+        t = statistics.median(a.elapsed_time(b) for a, b in evs) * 1e-3
+        return self.decode_attn_bytes() / t / 1e9
 
     # ------------------------------------------------------------ workload
     def prefill_flops(self) -> float:
