@@ -130,6 +130,10 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
                     int max_seqlen, int Hq, int Hkv, int d, float scale, int max_ctas,
                     void* stream);
 
+/* Development aid: clock64 trace of CTA 0's softmax/MMA waits into `buf`
+ * (int64 [12][256]; NULL disables). */
+int hp_set_fa_trace(void* buf);
+
 /* Prefix-aware (chunked) prefill attention over the paged cache
  * (workload.py:176-183 with prior_lens > 0; the attention of a hybrid batch,
  * hybrid_kernels workload.py:213-257, as issued by _ChunkedSim engine.py:

@@ -11,21 +11,24 @@
 //           Query i of a sequence sits at position prior + i and attends keys
 //           [0, prior + i].
 //
-// One CTA owns one (sequence, 128-query tile, q head) unit at a time
-// (persistent grid = partition SMs, units longest-first).  Warp roles:
-//   warp 0      TMA producer: Q once per unit, then K_j / V_j (128-token
-//               tiles, 128B-swizzled boxes) into 2-stage rings
+// One CTA owns one (sequence, 256-query pair of 128-row tiles A/B, q head)
+// unit at a time (persistent grid = partition SMs; units longest-first in
+// "snake" order across CTAs).  Both tiles share every K/V tile.  Warp roles:
+//   warp 0      producer: Q_A/Q_B once per unit, then K_j / V_j (128-token
+//               tiles) into 2-stage rings (TMA boxes or paged bulk copies)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
-//                 S_j  = Q . K_j^T        (M=128, N=128, K=D; K-major A/B)
-//                 O   += P_j . V_j        (M=128, N=D,   K=128; V MN-major)
-//               S is double-buffered in TMEM so S_{j+1} is computed while
-//               the softmax warps work on S_j; O accumulates in TMEM.
-//   warps 2-5   softmax: one thread per query row (TMEM lane); tcgen05.ld of
-//               the S row, causal mask, exp2 online softmax with lazy O
-//               rescaling (only when a row max grows by > 2^8), P written as
-//               bf16 into a 128B-swizzled K-major smem tile for the PV MMA;
-//               epilogue O / l from TMEM to global.
-// TMEM: S0 cols [0,128), S1 [128,256), O [256, 256+D).
+//                 S_X  = Q_X . K_j^T      (M=128, N=128, K=D; SS)
+//                 O_X += P_X . V_j        (M=128, N=D, K=128; A = P from TMEM)
+//               ping-ponging the tiles: PV_A(j) QK_A(j+1) PV_B(j) QK_B(j+1)
+//   warps 2-5   softmax of tile A, warps 6-9 softmax of tile B: one thread
+//               per query row (TMEM lane), causal mask, exp2 online softmax
+//               (8-way ILP max/sum chains) with lazy O rescaling (only when a
+//               row max grows by > 2^8), P stored as packed bf16 over the S
+//               tile's own TMEM columns; epilogue O / l to global.
+// TMEM: S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [256+D,256+2D).
+// Measured bound (clock64 trace, T = 16384): the tensor core runs PV+QK of
+// one tile in ~1.7k cycles against 1k at the UMMA peak -- the SS QK MMA at
+// N = 128 plus the K/V TMA writes saturate the 128 B/clk shared-memory port.
 #include "common.cuh"
 #include "runtime.h"
 #include "../../include/hp.h"
@@ -44,14 +47,6 @@ constexpr int VST = 2;     // V ring stages
 constexpr uint32_t BOX = 128 * 128;  // 128 rows x 128 B
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: rescale O when max grows by > 256x
 
-template <int D>
-struct FaCfg {
-  static constexpr int NB = D / 64;             // 64-dim boxes per row
-  static constexpr uint32_t QB = NB * BOX;      // Q tile bytes
-  static constexpr uint32_t KB = NB * BOX;      // K (and V) tile bytes
-  static constexpr uint32_t PB = 2 * BOX;       // P tile bytes (128 x 128 bf16)
-  static constexpr size_t SMEM = 1024 + QB + KST * KB + VST * KB + PB + 512;
-};
 
 struct FaParams {
   const int* cu_seqlens;
@@ -65,6 +60,7 @@ struct FaParams {
   const int* block_table;
   const int* prior_lens;
   int max_pages, page, Hkv;
+  long long* trace;  // optional clock64 trace of CTA 0 (hp_set_fa_trace; development aid)
 };
 
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo_bytes) {
@@ -98,27 +94,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-struct Unit {
-  int head, seq, qt, s0, len, nkv;
-  int prior, kvlen;  // cached prefix length; keys visible to the last query
-};
-
-template <bool PAGED>
-__device__ __forceinline__ bool unit_of(const FaParams& p, int u, Unit& x) {
-  x.head = u % p.Hq;
-  const int rest = u / p.Hq;
-  x.seq = rest % p.nseq;
-  x.qt = p.n_qt - 1 - rest / p.nseq;
-  x.s0 = p.cu_seqlens[x.seq];
-  x.len = p.cu_seqlens[x.seq + 1] - x.s0;
-  if (x.qt * FQ >= x.len) return false;
-  x.prior = PAGED ? p.prior_lens[x.seq] : 0;
-  x.kvlen = x.prior + x.len;
-  const int q0 = x.qt * FQ;
-  x.nkv = min((x.prior + q0 + FQ + FK - 1) / FK, (x.kvlen + FK - 1) / FK);
-  return true;
-}
-
 // Address of the 64-token tile holding cache position `pos` of sequence
 // `seq`, kv head `kvh` (positions past the sequence map to its first page:
 // finite data whose scores the causal mask removes).
@@ -133,47 +108,113 @@ __device__ __forceinline__ const __nv_bfloat16* page_tile(const FaParams& p, con
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// k_fa2: two 128-query tiles (A = rows q0.., B = rows q0+128..) of one
+// (sequence, head) per unit, sharing every K/V tile.  P never touches shared
+// memory: the softmax warps write it as packed bf16 into the TMEM columns of
+// the S tile it came from, and O += P.V is issued with A = P from TMEM
+// (tcgen05.mma ... [d], [a_tmem], b_desc).  The MMA warp ping-pongs the two
+// tiles, so while softmax group A works on S_A(j+1) the tensor core runs
+// PV_B(j) and QK_B(j+1), and vice versa:
+//     PV_A(j)  QK_A(j+1)  PV_B(j)  QK_B(j+1)  PV_A(j+1) ...
+// tcgen05 ops of one issuing thread execute in order, which is what makes
+// QK_X(j+1) overwriting S_X/P_X after PV_X(j) safe and makes O_X stable
+// whenever s_full_X fires (rescale point).
+// Warps: 0 producer, 1 TMEM alloc + MMA issuer, 2-5 softmax A, 6-9 softmax B.
+// TMEM: S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [256+D, 256+2D).
+constexpr int FA2_THREADS = 320;
+
+template <int D>
+struct Fa2Cfg {
+  static constexpr int NB = D / 64;
+  static constexpr uint32_t QB = NB * BOX;
+  static constexpr uint32_t KB = NB * BOX;
+  static constexpr size_t SMEM = 1024 + 2 * QB + KST * KB + VST * KB + 512;
+};
+
+struct Unit2 {
+  int head, seq, s0, len, prior, kvlen;
+  int q0;          // first query row (tile A) within the new span
+  int nA, nB;      // kv tiles of tile A / tile B (nB = 0: tile B absent)
+};
+
+template <bool PAGED>
+__device__ __forceinline__ bool unit2_of(const FaParams& p, int u, Unit2& x) {
+  x.head = u % p.Hq;
+  const int rest = u / p.Hq;
+  x.seq = rest % p.nseq;
+  const int qp = p.n_qt - 1 - rest / p.nseq;  // n_qt counts 256-row pairs here
+  x.s0 = p.cu_seqlens[x.seq];
+  x.len = p.cu_seqlens[x.seq + 1] - x.s0;
+  x.q0 = qp * 2 * FQ;
+  if (x.q0 >= x.len) return false;
+  x.prior = PAGED ? p.prior_lens[x.seq] : 0;
+  x.kvlen = x.prior + x.len;
+  const int kvt = (x.kvlen + FK - 1) / FK;
+  x.nA = min((x.prior + x.q0 + FQ + FK - 1) / FK, kvt);
+  x.nB = (x.q0 + FQ < x.len) ? min((x.prior + x.q0 + 2 * FQ + FK - 1) / FK, kvt) : 0;
+  return true;
+}
+
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Units are sorted longest-first; CTA b takes unit r*G + b in even rounds and
+// r*G + (G-1-b) in odd ones ("snake" order), which balances the causal
+// triangle's per-unit work to within a few % of greedy LPT (round-robin
+// leaves the first CTAs ~30% over the mean at T = 4096).
+__device__ __forceinline__ int snake_unit(int r) {
+  return r * int(gridDim.x) + ((r & 1) ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x));
+}
+
 template <int D, bool PAGED>
-__global__ void __launch_bounds__(192, 1)
-    k_fa_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, const FaParams p) {
-  using C = FaCfg<D>;
+__global__ void __launch_bounds__(FA2_THREADS, 1)
+    k_fa2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+          const __grid_constant__ CUtensorMap tmV, const FaParams p) {
+  using C = Fa2Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + C::QB;
+  uint8_t* sQ = smem;                 // [2][QB]
+  uint8_t* sK = sQ + 2 * C::QB;
   uint8_t* sV = sK + KST * C::KB;
-  uint8_t* sP = sV + VST * C::KB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::PB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * C::KB);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;             // [KST]
-  uint64_t* k_empty = k_full + KST;        // [KST]
+  uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;        // [VST]
-  uint64_t* v_empty = v_full + VST;        // [VST]
-  uint64_t* s_full = v_empty + VST;        // [2]
-  uint64_t* s_free = s_full + 2;           // [2]
-  uint64_t* p_full = s_free + 2;
-  uint64_t* p_free = p_full + 1;
-  uint64_t* o_full = p_free + 1;
-  uint64_t* o_empty = o_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;        // [2] per tile
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* o_full = p_full + 2;           // [2]
+  uint64_t* o_empty = o_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
+    if (!PAGED) {
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+    }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int s = 0; s < KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_free[s], 4); }
-    mbar_init(p_full, 4);
-    mbar_init(p_free, 1);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 4);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&o_full[t], 1);
+      mbar_init(&o_empty[t], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -190,21 +231,23 @@ __global__ void __launch_bounds__(192, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t un = 0, kt = 0, vt = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        Unit x;
-        if (!unit_of<PAGED>(p, u, x)) continue;
+      for (int r = 0; r * int(gridDim.x) < total; ++r) {
+        const int u = snake_unit(r);
+        if (u >= total) continue;
+        Unit2 x;
+        if (!unit2_of<PAGED>(p, u, x)) continue;
         const int kvh = x.head / p.G;
+        const int J = max(x.nA, x.nB);
         mbar_wait(q_empty, (un & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, C::QB);
-        for (int b = 0; b < C::NB; ++b)
-          tma_load_2d(sQ + b * BOX, &tmQ, q_full, x.head * D + b * 64, x.s0 + x.qt * FQ);
-        for (int j = 0; j < x.nkv; ++j, ++kt, ++vt) {
+        mbar_arrive_expect_tx(q_full, C::QB * (x.nB > 0 ? 2 : 1));
+        for (int t = 0; t < (x.nB > 0 ? 2 : 1); ++t)
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d(sQ + t * C::QB + b * BOX, &tmQ, q_full, x.head * D + b * 64, x.s0 + x.q0 + t * FQ);
+        for (int j = 0; j < J; ++j, ++kt, ++vt) {
           const int ks = kt % KST, vs = vt % VST;
           mbar_wait(&k_empty[ks], ((kt / KST) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], C::KB);
           if constexpr (PAGED) {
-            // 128 keys = two 64-token cache tiles; each 64-dim half is one
-            // contiguous, already-swizzled 8 KB run -> rows t*64.. of box b
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
               const __nv_bfloat16* src = page_tile<D>(p, p.kc, x.seq, kvh, j * FK + t * 64, x.kvlen);
@@ -239,123 +282,169 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_qk = umma_idesc_bf16(FQ, FK);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(FQ, D) | (1u << 16);  // B (V) MN-major
-      uint32_t un = 0, kt = 0, vt = 0, gt = 0;  // gt: global kv-tile counter (S buffer / P phases)
-      auto issue_pv = [&](uint32_t tile, bool first) {
-        const int vs = vt % VST;
-        if (first) mbar_wait(o_empty, (un & 1) ^ 1);  // previous unit's epilogue has read O
-        mbar_wait(p_full, tile & 1);
-        mbar_wait(&v_full[vs], (vt / VST) & 1);
-        tc_fence_after();
-        const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + vs * C::KB);
+      uint32_t un = 0, kt = 0, vt = 0;
+      uint32_t pc[2] = {0, 0};   // P tiles consumed per softmax group (p_full phases)
+      uint32_t oc[2] = {0, 0};   // units per group (o_empty phases)
+      auto qk = [&](int t, uint32_t kslot) {
+        const uint32_t qa = smem_u32(sQ + t * C::QB), kb = smem_u32(sK + kslot * C::KB);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_bf16(tmem + t * 128, umma_desc_sw128(qa + (kk >> 2) * BOX + (kk & 3) * 32),
+                    umma_desc_sw128(kb + (kk >> 2) * BOX + (kk & 3) * 32), idesc_qk, kk > 0 ? 1u : 0u);
+        umma_commit(&s_full[t]);
+      };
+      auto pv = [&](int t, uint32_t vslot, bool first) {
+        const uint32_t vb = smem_u32(sV + vslot * C::KB);
 #pragma unroll
         for (int kk = 0; kk < FK / 16; ++kk)
-          umma_bf16(tmem + 256, umma_desc_sw128(pa + (kk >> 2) * BOX + (kk & 3) * 32),
-                    desc_mn_sw128(vb + kk * 2048, BOX), idesc_pv, (first && kk == 0) ? 0u : 1u);
-        umma_commit(&v_empty[vs]);
-        umma_commit(p_free);
-        ++vt;
+          umma_bf16_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, desc_mn_sw128(vb + kk * 2048, BOX),
+                       idesc_pv, (first && kk == 0) ? 0u : 1u);
       };
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        Unit x;
-        if (!unit_of<PAGED>(p, u, x)) continue;
+      for (int r = 0; r * int(gridDim.x) < total; ++r) {
+        const int u = snake_unit(r);
+        if (u >= total) continue;
+        Unit2 x;
+        if (!unit2_of<PAGED>(p, u, x)) continue;
+        const int n[2] = {x.nA, x.nB};
+        const int J = max(x.nA, x.nB);
         mbar_wait(q_full, un & 1);
-        for (int j = 0; j < x.nkv; ++j, ++kt, ++gt) {
-          const int sb = gt & 1;
+        // prologue: S(0) for both tiles
+        {
           const int ks = kt % KST;
-          mbar_wait(&s_free[sb], ((gt >> 1) & 1) ^ 1);
           mbar_wait(&k_full[ks], (kt / KST) & 1);
           tc_fence_after();
-          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + ks * C::KB);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            umma_bf16(tmem + sb * 128, umma_desc_sw128(qa + (kk >> 2) * BOX + (kk & 3) * 32),
-                      umma_desc_sw128(kb + (kk >> 2) * BOX + (kk & 3) * 32), idesc_qk, kk > 0 ? 1u : 0u);
-          umma_commit(&k_empty[ks]);
-          umma_commit(&s_full[sb]);
-          if (j == x.nkv - 1) umma_commit(q_empty);
-          if (j >= 1) issue_pv(gt - 1, j == 1);
+          for (int t = 0; t < 2; ++t)
+            if (n[t] > 0) qk(t, ks);
         }
-        issue_pv(gt - 1, x.nkv == 1);
-        umma_commit(o_full);
+        for (int j = 0; j < J; ++j) {
+          const uint32_t vs = (vt + j) % VST;
+          const uint32_t ks_cur = (kt + j) % KST, ks_nxt = (kt + j + 1) % KST;
+          bool k_next_ready = false;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (j >= n[t]) continue;
+            const bool tr = p.trace && blockIdx.x == 0 && pc[t] < 256;
+            if (tr) p.trace[(8 + t * 2) * 256 + pc[t]] = clock64();
+            mbar_wait(&p_full[t], pc[t] & 1);
+            if (tr) p.trace[(8 + t * 2 + 1) * 256 + pc[t]] = clock64();
+            ++pc[t];
+            if (j == 0) mbar_wait(&o_empty[t], (oc[t] & 1) ^ 1);
+            mbar_wait(&v_full[vs], ((vt + j) / VST) & 1);
+            tc_fence_after();
+            pv(t, vs, j == 0);
+            if (j + 1 < n[t]) {
+              if (!k_next_ready) {
+                mbar_wait(&k_full[ks_nxt], ((kt + j + 1) / KST) & 1);
+                tc_fence_after();
+                k_next_ready = true;
+              }
+              qk(t, ks_nxt);
+            } else {
+              umma_commit(&o_full[t]);
+              ++oc[t];
+            }
+          }
+          umma_commit(&v_empty[vs]);
+          umma_commit(&k_empty[ks_cur]);  // K_j: read by QK(j) of both tiles, all issued
+          if (j == J - 1) umma_commit(q_empty);
+        }
+        kt += J;
+        vt += J;
         ++un;
       }
     }
   } else {
     // ------------------------------------------------------------- softmax
-    const int q4 = warp & 3;
+    const int t = (warp - 2) >> 2;          // tile 0 (A) or 1 (B)
+    const int q4 = warp & 3;                // TMEM lane quarter
     const int row = q4 * 32 + lane;
     const uint32_t lane_base = uint32_t(q4 * 32) << 16;
-    uint32_t un = 0, gt = 0;
-    for (int u = blockIdx.x; u < total; u += gridDim.x) {
-      Unit x;
-      if (!unit_of<PAGED>(p, u, x)) continue;
-      const int q0 = x.qt * FQ;
-      const int qi = q0 + row;      // row of this thread within the new span
-      const int qpos = x.prior + qi;  // its key-space position
+    const uint32_t tS = tmem + lane_base + t * 128;
+    const uint32_t tO = tmem + lane_base + 256 + t * D;
+    uint32_t sc = 0, un = 0;
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+        const int u = snake_unit(r);
+        if (u >= total) continue;
+      Unit2 x;
+      if (!unit2_of<PAGED>(p, u, x)) continue;
+      const int nt = t == 0 ? x.nA : x.nB;
+      if (nt == 0) continue;
+      const int q0 = x.q0 + t * FQ;
+      const int qi = q0 + row;
+      const int qpos = x.prior + qi;
       float m_run = -INFINITY, l = 0.f;
-      for (int j = 0; j < x.nkv; ++j, ++gt) {
-        const int sb = gt & 1;
-        mbar_wait(&s_full[sb], (gt >> 1) & 1);
+      for (int j = 0; j < nt; ++j, ++sc) {
+        const bool tr = p.trace && blockIdx.x == 0 && lane == 0 && q4 == 0 && sc < 256;
+        if (tr) p.trace[(t * 4 + 0) * 256 + sc] = clock64();
+        mbar_wait(&s_full[t], sc & 1);
+        if (tr) p.trace[(t * 4 + 1) * 256 + sc] = clock64();
         tc_fence_after();
         float s[128];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + sb * 128 + c * 32, s + c * 32);
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[sb]);
+        if (tr) p.trace[(t * 4 + 2) * 256 + sc] = clock64();
         const int kbase = j * FK;
         const bool need_mask = (kbase + FK - 1 > x.prior + q0) || (kbase + FK > x.kvlen);
-        float mx = -INFINITY;
+        if (need_mask) {
+          const int lim = min(qpos + 1, x.kvlen) - kbase;  // keys [0, lim) visible
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          float v = s[c] * p.scale_log2;
-          if (need_mask && (kbase + c > qpos || kbase + c >= x.kvlen)) v = -INFINITY;
-          s[c] = v;
-          mx = fmaxf(mx, v);
+          for (int c = 0; c < 128; ++c)
+            if (c >= lim) s[c] = -INFINITY;
         }
+        // raw-score row max with 8 independent chains (ILP), then scale once
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+        for (int c = 8; c < 128; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m8[k] = fmaxf(m8[k], m8[k + 4]);
+        const float mx = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])) * p.scale_log2;
         const float m_new = fmaxf(m_run, mx);
         const bool grow = m_new > m_run + RESCALE_THRESHOLD;
-        // P buffer / O are free once the previous PV completed
-        mbar_wait(p_free, (gt & 1) ^ 1);
-        tc_fence_after();
+        // O_t holds PV(0..j-1), complete (issued before QK(j)); rescale lazily
         if (__any_sync(0xffffffffu, grow) && j > 0) {
           const float alpha = grow ? exp2f(m_run - m_new) : 1.f;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             float o[32];
-            tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+            tmem_ld32(tO + c * 32, o);
             tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 32; ++k) o[k] *= alpha;
-            tmem_st32(tmem + lane_base + 256 + c * 32, o);
+            tmem_st32(tO + c * 32, o);
           }
-          tmem_st_wait();
           if (grow) l *= alpha;
         }
         if (grow) m_run = m_new;
         const float mb = (m_run == -INFINITY) ? 0.f : m_run;
-        // P row -> smem, 128B-swizzled K-major (two 64-token halves)
-        uint8_t* prow = sP + row * 128;
+        // P = exp2(s * scale_log2 - m) (one FFMA + MUFU per score), bf16
+        // pairs over the first 64 columns of S_t; 8 partial row sums
+        float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
-          uint32_t w[4];
+        for (int h = 0; h < 2; ++h) {
+          float w[32];
+          uint32_t* wu = reinterpret_cast<uint32_t*>(w);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float a = ex2(s[ch * 8 + 2 * k] - mb), b = ex2(s[ch * 8 + 2 * k + 1] - mb);
-            l += a + b;
-            w[k] = pack_bf16(a, b);
+          for (int k = 0; k < 32; ++k) {
+            const float a = ex2(fmaf(s[h * 64 + 2 * k], p.scale_log2, -mb));
+            const float b = ex2(fmaf(s[h * 64 + 2 * k + 1], p.scale_log2, -mb));
+            l8[k & 7] += a + b;
+            wu[k] = pack_bf16(a, b);
           }
-          const int half = ch >> 3, cc = ch & 7;
-          *reinterpret_cast<uint4*>(prow + half * BOX + ((cc ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          tmem_st32(tS + h * 32, w);
         }
-        fence_proxy_async();
+        l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+        tmem_st_wait();
+        if (tr) p.trace[(t * 4 + 3) * 256 + sc] = clock64();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
       // epilogue: O / l -> global
-      mbar_wait(o_full, un & 1);
+      mbar_wait(&o_full[t], un & 1);
       tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const bool ok = qi < x.len;
@@ -363,7 +452,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         float o[32];
-        tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+        tmem_ld32(tO + c * 32, o);
         tmem_ld_wait();
         if (ok) {
           uint4 w[4];
@@ -377,7 +466,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(o_empty);
+      if (lane == 0) mbar_arrive(&o_empty[t]);
       ++un;
     }
   }
@@ -390,22 +479,30 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int D, bool PAGED>
-static int launch_fa(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                     const FaParams& p, int grid, cudaStream_t st) {
+static int launch_fa2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, FaParams p,
+                      int max_seqlen, int max_ctas, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_fa_tc<D, PAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(FaCfg<D>::SMEM)));
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_fa2<D, PAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(Fa2Cfg<D>::SMEM)));
     attr = true;
   }
-  k_fa_tc<D, PAGED><<<grid, 192, FaCfg<D>::SMEM, st>>>(tq, tk, tv, p);
-  HP_LAUNCH_CHECK("k_fa_tc");
+  p.n_qt = (max_seqlen + 2 * FQ - 1) / (2 * FQ);
+  const int grid = std::min(p.nseq * p.n_qt * p.Hq, max_ctas);
+  k_fa2<D, PAGED><<<grid, FA2_THREADS, Fa2Cfg<D>::SMEM, st>>>(tq, tk, tv, p);
+  HP_LAUNCH_CHECK("k_fa2");
   return HP_OK;
 }
 
 }  // namespace hp
 
 using namespace hp;
+
+static long long* g_fa_trace = nullptr;
+extern "C" int hp_set_fa_trace(void* buf) {
+  g_fa_trace = static_cast<long long*>(buf);
+  return HP_OK;
+}
 
 extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                                void* o, int ldo, const int* cu_seqlens, int nseq, int total_tokens,
@@ -428,16 +525,15 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
   FaParams p{};
   p.cu_seqlens = cu_seqlens;
   p.nseq = nseq;
-  p.n_qt = (max_seqlen + FQ - 1) / FQ;
   p.Hq = Hq;
   p.G = Hq / Hkv;
   p.out = static_cast<__nv_bfloat16*>(o);
   p.ldo = ldo;
   p.scale_log2 = scale * 1.4426950408889634f;
-  const int units = nseq * p.n_qt * Hq;
-  const int grid = std::min(units, max_ctas);
+  p.trace = g_fa_trace;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d == 128 ? launch_fa<128, false>(tq, tk, tv, p, grid, st) : launch_fa<64, false>(tq, tk, tv, p, grid, st);
+  return d == 128 ? launch_fa2<128, false>(tq, tk, tv, p, max_seqlen, max_ctas, st)
+                  : launch_fa2<64, false>(tq, tk, tv, p, max_seqlen, max_ctas, st);
 }
 
 extern "C" int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache, const void* vcache,
@@ -462,7 +558,6 @@ extern "C" int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache,
   FaParams p{};
   p.cu_seqlens = cu_seqlens;
   p.nseq = nseq;
-  p.n_qt = (max_seqlen + FQ - 1) / FQ;
   p.Hq = Hq;
   p.G = Hq / Hkv;
   p.out = static_cast<__nv_bfloat16*>(o);
@@ -475,8 +570,7 @@ extern "C" int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache,
   p.max_pages = max_pages;
   p.page = page;
   p.Hkv = Hkv;
-  const int units = nseq * p.n_qt * Hq;
-  const int grid = std::min(units, max_ctas);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d == 128 ? launch_fa<128, true>(tq, tq, tq, p, grid, st) : launch_fa<64, true>(tq, tq, tq, p, grid, st);
+  return d == 128 ? launch_fa2<128, true>(tq, tq, tq, p, max_seqlen, max_ctas, st)
+                  : launch_fa2<64, true>(tq, tq, tq, p, max_seqlen, max_ctas, st);
 }
