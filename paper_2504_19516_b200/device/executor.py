@@ -46,7 +46,8 @@ def _ev():
 class B200Executor:
     def __init__(self, model: ModelSpec, gpu: GpuSpec, device: int = 0, seed: int = 0,
                  max_prefill_tokens: int = 32768, max_decode_batch: int = 256,
-                 pool_tokens: int = 1 << 21, sm_step: int = 8, pool: PartitionPool | None = None):
+                 pool_tokens: int = 1 << 21, sm_step: int = 8, pool: PartitionPool | None = None,
+                 memo: bool = False):
         if model.head_dim not in (64, 128):
             raise InvalidArgumentError("B200Executor supports head_dim 64 or 128")
         self.model = model
@@ -77,6 +78,12 @@ class B200Executor:
         self.dsc = DecodeScratch(model, max_decode_batch, 1024, self.dev, max_ctas=self.pool.n)
         self.calls = {"prefill": 0, "decode": 0}
         self._warm: set = set()
+        # memo=True: reuse a measurement for states with the same partition,
+        # prefill lengths, decode batch size and mean KV pages per sequence
+        # (the quantities the step time depends on) -- bounds the GPU time of
+        # long serving traces; off by default (every call measures)
+        self.memo = {} if memo else None
+        self.memo_hits = 0
 
     # ------------------------------------------------------------ workloads
     def _prefill_args(self, lens):
@@ -172,11 +179,28 @@ class B200Executor:
         return max(1, min(8, math.ceil(3.0 * d / max(p, 1e-9))))
 
     # -------------------------------------------------------- oracle protocol
+    def _memo_key(self, phase: str, es: ExecutionState):
+        ctx = es.decode_ctx_lens
+        pages = -(-sum(int(c) for c in ctx) // PAGE) if ctx else 0
+        return (phase, es.prefill_sms if es.prefill_lens else 0, es.decode_sms if ctx else 0,
+                tuple(es.prefill_lens), len(ctx), round(pages / max(1, len(ctx))))
+
+    def _measured(self, phase: str, es: ExecutionState) -> float:
+        if self.memo is None:
+            return self._measure(phase, es)
+        key = self._memo_key(phase, es)
+        v = self.memo.get(key)
+        if v is None:
+            v = self.memo[key] = self._measure(phase, es)
+        else:
+            self.memo_hits += 1
+        return v
+
     def prefill_layer_s(self, es: ExecutionState) -> float:
-        return self._measure("prefill", es)
+        return self._measured("prefill", es)
 
     def decode_step_s(self, es: ExecutionState) -> float:
-        return self.model.num_layers * self._measure("decode", es)
+        return self.model.num_layers * self._measured("decode", es)
 
     def _hybrid_args(self, chunks, decode_ctx_lens):
         """Device inputs of one hybrid batch: chunk rows first, then decode
