@@ -125,6 +125,7 @@ __device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
 // the P.V product, so a slot is held for one MMA chain, not a whole tile.
 template <int D>
 __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParams p) {
+  pdl_trigger();
   constexpr int KK = D / 16;
   constexpr uint32_t HS = uint32_t(DA_TILE) * D * 2;
   const int RS = p.rs;
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();  // q, K/V (incl. the token rope_kv_write just stored), block table
 
   const int total = p.B * p.Hkv * p.max_splits;
   const int page_tiles = p.page / DA_TILE;
@@ -441,6 +443,8 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
 // One warp per (sequence, head): log-sum-exp merge of the split partials.
 template <int D>
 __global__ void k_decode_combine(const DecodeParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp_global >= p.B * p.Hq) return;
@@ -481,12 +485,11 @@ static int launch_decode(DecodeParams& p, int max_ctas, cudaStream_t st) {
     attr = true;
   }
   const int units = p.B * p.Hkv * p.max_splits;
-  k_decode_attn<D><<<std::min(units, max_ctas), DA_THREADS, pl.smem, st>>>(p);
-  HP_LAUNCH_CHECK("k_decode_attn");
+  HP_LAUNCH_PDL("k_decode_attn", k_decode_attn<D>, dim3(std::min(units, max_ctas)), dim3(DA_THREADS), pl.smem,
+                st, p);
   if (p.max_splits > 1) {
     const int warps = p.B * p.Hq;
-    k_decode_combine<D><<<(warps + 7) / 8, 256, 0, st>>>(p);
-    HP_LAUNCH_CHECK("k_decode_combine");
+    HP_LAUNCH_PDL("k_decode_combine", k_decode_combine<D>, dim3((warps + 7) / 8), dim3(256), 0, st, p);
   }
   return HP_OK;
 }

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
     k_fa2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
           const __grid_constant__ CUtensorMap tmV, const FaParams p) {
   using C = Fa2Cfg<D>;
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                 // [2][QB]
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // qkv from the QKV GEMM / rope_kv_write; `out` may still be read upstream
   const uint32_t tmem = *tmem_slot;
   const int total = p.nseq * p.n_qt * p.Hq;
 
@@ -489,8 +491,7 @@ static int launch_fa2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
   }
   p.n_qt = (max_seqlen + 2 * FQ - 1) / (2 * FQ);
   const int grid = std::min(p.nseq * p.n_qt * p.Hq, max_ctas);
-  k_fa2<D, PAGED><<<grid, FA2_THREADS, Fa2Cfg<D>::SMEM, st>>>(tq, tk, tv, p);
-  HP_LAUNCH_CHECK("k_fa2");
+  HP_LAUNCH_PDL("k_fa2", k_fa2<D, PAGED>, dim3(grid), dim3(FA2_THREADS), Fa2Cfg<D>::SMEM, st, tq, tk, tv, p);
   return HP_OK;
 }
 

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
                    const SwapParams p) {
   using C = SwapCfg<BN>;
   constexpr int STAGES = C::STAGES;
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -195,26 +196,38 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     // warp-converged walk (uniform registers), one elected lane issues
     {
       const uint64_t w_policy = l2_policy_evict_first();  // weights: read once per step
-      uint32_t g = 0;
-      int it = begin;
-      Seg s;
-      while (next_seg(p, it, end, s)) {
-        const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
-        for (int kb = s.kb0; kb < s.kb1; ++kb, ++g) {
-          if (int(g % PL) != warp) continue;
-          const int stage = g % STAGES;
-          const uint32_t phase = (g / STAGES) & 1;
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (elect_one()) {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            // 128 rows x 128 k of W: one contiguous 32 KB run (two swizzled 64-k halves)
-            bulk_load_hint(sA + stage * C::A_BYTES, p.w + wtile_offset(mt * SBM, 2 * kb, p.K), C::A_BYTES,
-                           &full[stage], w_policy);
-            tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
-            tma_load_2d(sB + stage * C::B_BYTES + BN * 128, &tmX, &full[stage], kb * SBK + 64, nt * BN);
+      // Weights are constant across the layer chain, so the first ring's worth
+      // of weight tiles is fetched BEFORE the programmatic-dependency wait,
+      // overlapping the predecessor kernel's tail; activation tiles follow it.
+      for (int pass = 0; pass < 2; ++pass) {
+        uint32_t g = 0;
+        int it = begin;
+        Seg s;
+        while (next_seg(p, it, end, s)) {
+          const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
+          for (int kb = s.kb0; kb < s.kb1; ++kb, ++g) {
+            const bool pre = g < uint32_t(STAGES);  // stage issued in pass 0 (weights only)
+            if (int(g % PL) != warp || (pass == 0 && !pre)) continue;
+            const int stage = g % STAGES;
+            const uint32_t phase = (g / STAGES) & 1;
+            if (pass == 0 || !pre) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              if (elect_one()) {
+                mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                // 128 rows x 128 k of W: one contiguous 32 KB run (two swizzled 64-k halves)
+                bulk_load_hint(sA + stage * C::A_BYTES, p.w + wtile_offset(mt * SBM, 2 * kb, p.K), C::A_BYTES,
+                               &full[stage], w_policy);
+              }
+            }
+            if (pass == 1 && elect_one()) {
+              tma_load_2d(sB + stage * C::B_BYTES, &tmX, &full[stage], kb * SBK, nt * BN);
+              tma_load_2d(sB + stage * C::B_BYTES + BN * 128, &tmX, &full[stage], kb * SBK + 64, nt * BN);
+            }
+            __syncwarp();
           }
-          __syncwarp();
+          if (pass == 0 && g >= uint32_t(STAGES)) break;
         }
+        if (pass == 0) pdl_wait();  // X is produced by the stream predecessor
       }
     }
   } else if (warp == SW_MMA) {
@@ -258,6 +271,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       if (acc == 0) acc_phase ^= 1;
     }
   } else {
+    pdl_wait();  // residual, workspace and output are shared with the stream predecessor
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int et = (warp - SW_MMA - 1) * 32 + lane;
@@ -367,7 +381,7 @@ static int launch_swap(const CUtensorMap& tx, const SwapParams& p, int grid,
     HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_swap_sk<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     attr_set = true;
   }
-  k_gemm_swap_sk<BN><<<grid, SW_THREADS, C::SMEM, st>>>(tx, p);
+  HP_LAUNCH_PDL("k_gemm_swap_sk", k_gemm_swap_sk<BN>, dim3(grid), dim3(SW_THREADS), C::SMEM, st, tx, p);
   HP_LAUNCH_CHECK("k_gemm_swap_sk");
   return HP_OK;
 }

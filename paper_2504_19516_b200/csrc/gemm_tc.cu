@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
   using C = GemmCfg<BN>;
   constexpr int STAGES = C::STAGES;
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -96,7 +97,6 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* t_start = reinterpret_cast<uint64_t*>(tmem_slot + 2);
-  if (threadIdx.x == 0) *t_start = globaltimer();
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // activations / residual from the stream predecessor
+  if (threadIdx.x == 0) *t_start = globaltimer();
   const uint32_t tmem_base = *tmem_slot;
 
   const int total = p.m_tiles * p.n_tiles * p.k_splits;
@@ -258,8 +260,7 @@ static int launch(const CUtensorMap& ta, const GemmParams& p, int grid, cudaStre
                                      int(C::SMEM)));
     attr_set = true;
   }
-  k_gemm_tc<BN><<<grid, 192, C::SMEM, st>>>(ta, p);
-  HP_LAUNCH_CHECK("k_gemm_tc");
+  HP_LAUNCH_PDL("k_gemm_tc", k_gemm_tc<BN>, dim3(grid), dim3(192), C::SMEM, st, ta, p);
   return HP_OK;
 }
 

@@ -14,6 +14,8 @@ namespace hp {
 __global__ void k_rmsnorm(const __nv_bfloat16* __restrict__ x, int ldx,
                           const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out,
                           int ldo, int rows, int cols, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
@@ -54,6 +56,8 @@ __global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, 
                                 int d, const int* __restrict__ pos, const float* __restrict__ cs,
                                 const int* __restrict__ slots, __nv_bfloat16* __restrict__ kc,
                                 __nv_bfloat16* __restrict__ vc, int page) {
+  pdl_trigger();
+  pdl_wait();
   const int half = d / 2;
   const int pairs = half / 2;             // threads per head (2 rotary dims each)
   const int per_tok = (Hq + 2 * Hkv) * pairs;
@@ -135,10 +139,9 @@ extern "C" int hp_rmsnorm(const void* x, int ldx, const void* weight, void* out,
   HP_CHECK_ARG(max_ctas >= 1, "hp_rmsnorm: max_ctas must be >= 1");
   const int wpb = 8;
   const int grid = std::min((rows + wpb - 1) / wpb, max_ctas * 4);
-  k_rmsnorm<<<grid, wpb * 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(weight),
-      static_cast<__nv_bfloat16*>(out), ldo, rows, cols, eps);
-  HP_LAUNCH_CHECK("k_rmsnorm");
+  HP_LAUNCH_PDL("k_rmsnorm", k_rmsnorm, dim3(grid), dim3(wpb * 32), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(weight),
+                static_cast<__nv_bfloat16*>(out), ldo, rows, cols, eps);
   return HP_OK;
 }
 
@@ -154,9 +157,9 @@ extern "C" int hp_rope_kv_write(void* qkv, int ldqkv, int T, int Hq, int Hkv, in
   const int threads = 256;
   const long want = (total + threads - 1) / threads;
   const int grid = int(std::min<long>(want, long(max_ctas) * 8));
-  k_rope_kv_write<<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<__nv_bfloat16*>(qkv), ldqkv, T, Hq, Hkv, d, positions, cos_sin, slot_mapping,
-      static_cast<__nv_bfloat16*>(kcache), static_cast<__nv_bfloat16*>(vcache), page);
-  HP_LAUNCH_CHECK("k_rope_kv_write");
+  HP_LAUNCH_PDL("k_rope_kv_write", k_rope_kv_write, dim3(grid), dim3(threads), 0,
+                static_cast<cudaStream_t>(stream), static_cast<__nv_bfloat16*>(qkv), ldqkv, T, Hq, Hkv, d,
+                positions, cos_sin, slot_mapping, static_cast<__nv_bfloat16*>(kcache),
+                static_cast<__nv_bfloat16*>(vcache), page);
   return HP_OK;
 }

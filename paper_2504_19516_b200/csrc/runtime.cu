@@ -1,5 +1,7 @@
 #include "runtime.h"
 
+#include <cstdlib>
+
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -124,6 +126,14 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
   if (g_tmap_cache.size() > 4096) g_tmap_cache.clear();
   g_tmap_cache.emplace(key, *out);
   return HP_OK;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int device_sm_count() {

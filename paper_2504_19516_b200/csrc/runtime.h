@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 
 #include "../../include/hp.h"
 
@@ -68,5 +69,37 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
                      uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
 
 int device_sm_count();
+
+// PDL on unless the environment sets HP_PDL=0 (A/B measurement).
+bool pdl_enabled();
+
+// Launch with programmatic dependent launch (PDL) enabled: the kernel may
+// start while its stream predecessor is still finishing; it must call
+// pdl_wait() (griddepcontrol.wait) before touching any memory the
+// predecessor chain produces or consumes.  Hides the launch latency and the
+// prologue (barrier init, TMEM alloc, descriptor prefetch, weight prefetch)
+// of every layer kernel behind the previous kernel's tail.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define HP_LAUNCH_PDL(name, ...)                                                     \
+  do {                                                                               \
+    cudaError_t _e = ::hp::launch_pdl(__VA_ARGS__);                                  \
+    if (_e != cudaSuccess)                                                           \
+      return ::hp::set_error(HP_ERR_CUDA, std::string(name ": ") + cudaGetErrorString(_e)); \
+  } while (0)
 
 }  // namespace hp
