@@ -130,9 +130,11 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
                     int max_seqlen, int Hq, int Hkv, int d, float scale, int max_ctas,
                     void* stream);
 
-/* Development aid: clock64 trace of CTA 0's softmax/MMA waits into `buf`
- * (int64 [12][256]; NULL disables). */
-int hp_set_fa_trace(void* buf);
+/* Development aid: kernel timeline traces.  kind 0: k_fa2 CTA 0 softmax/MMA
+ * wait stamps (clock64, int64 [12][256]); kind 1: k_gemm_swap_sk per-CTA
+ * globaltimer stamps (uint64 [grid][6]: entry, prologue done, producer
+ * done, MMA done, epilogue done, exit).  NULL disables. */
+int hp_set_trace(int kind, void* buf);
 
 /* Prefix-aware (chunked) prefill attention over the paged cache
  * (workload.py:176-183 with prior_lens > 0; the attention of a hybrid batch,

@@ -499,11 +499,7 @@ static int launch_fa2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
 
 using namespace hp;
 
-static long long* g_fa_trace = nullptr;
-extern "C" int hp_set_fa_trace(void* buf) {
-  g_fa_trace = static_cast<long long*>(buf);
-  return HP_OK;
-}
+
 
 extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* v, int ldv,
                                void* o, int ldo, const int* cu_seqlens, int nseq, int total_tokens,
@@ -531,7 +527,7 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
   p.out = static_cast<__nv_bfloat16*>(o);
   p.ldo = ldo;
   p.scale_log2 = scale * 1.4426950408889634f;
-  p.trace = g_fa_trace;
+  p.trace = static_cast<long long*>(trace_buf(TRACE_FA));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return d == 128 ? launch_fa2<128, false>(tq, tk, tv, p, max_seqlen, max_ctas, st)
                   : launch_fa2<64, false>(tq, tk, tv, p, max_seqlen, max_ctas, st);

@@ -69,6 +69,7 @@ struct SwapParams {
   int* counters;    // [tiles], zero on entry and exit
   const uint8_t* w;  // weights in the tiled layout (hp_tile_weight)
   int epi;
+  unsigned long long* trace;  // optional [grid][6] globaltimer stamps (hp_set_trace; development aid)
 };
 
 struct Seg {
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   using C = SwapCfg<BN>;
   constexpr int STAGES = C::STAGES;
   pdl_trigger();
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 6] = globaltimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -187,6 +189,8 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned long long* tr = p.trace ? p.trace + blockIdx.x * 6 : nullptr;
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
   const int begin = blockIdx.x * p.ipc;
   const int end = min(begin + p.ipc, p.total_iters);
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
         }
         if (pass == 0) pdl_wait();  // X is produced by the stream predecessor
       }
+      if (tr && warp == 0 && lane == 0) tr[2] = globaltimer();
     }
   } else if (warp == SW_MMA) {
     // The whole warp walks the (warp-uniform) schedule so descriptors live in
@@ -270,6 +275,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (tr && lane == 0) tr[3] = globaltimer();
   } else {
     pdl_wait();  // residual, workspace and output are shared with the stream predecessor
     const int q = warp & 3;
@@ -364,12 +370,14 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
       if (acc == 0) acc_phase ^= 1;
     }
   }
+  if (tr && threadIdx.x == (SW_MMA + 1) * 32) tr[4] = globaltimer();
   tc_fence_before();
   __syncthreads();
   if (warp == SW_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+  if (tr && threadIdx.x == 0) tr[5] = globaltimer();
 }
 
 template <int BN>
@@ -436,6 +444,7 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
   p.ws = static_cast<float*>(workspace);
   p.counters = counters;
   p.epi = epilogue;
+  p.trace = static_cast<unsigned long long*>(trace_buf(TRACE_SWAP));
   const bool any_split = p.ipc % p.num_kb != 0 || p.ipc < p.num_kb;
   if (any_split) {
     HP_CHECK_ARG(workspace && counters, "hp_gemm_swap: split tiles need workspace and counters");

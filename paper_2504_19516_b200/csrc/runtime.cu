@@ -128,6 +128,19 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
   return HP_OK;
 }
 
+static void* g_trace[TRACE_KINDS] = {nullptr, nullptr};
+void* trace_buf(int kind) { return g_trace[kind]; }
+
+}  // namespace hp
+
+extern "C" int hp_set_trace(int kind, void* buf) {
+  HP_CHECK_ARG(kind >= 0 && kind < hp::TRACE_KINDS, "hp_set_trace: unknown kind");
+  hp::g_trace[kind] = buf;
+  return HP_OK;
+}
+
+namespace hp {
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HP_PDL");

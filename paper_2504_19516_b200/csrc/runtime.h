@@ -70,6 +70,10 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
 
 int device_sm_count();
 
+// Development aid: per-kernel trace buffers (hp_set_trace); nullptr = off.
+enum { TRACE_FA = 0, TRACE_SWAP = 1, TRACE_KINDS = 2 };
+void* trace_buf(int kind);
+
 // PDL on unless the environment sets HP_PDL=0 (A/B measurement).
 bool pdl_enabled();
 

@@ -39,7 +39,7 @@ SIGNATURES = {
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
-    "hp_set_fa_trace": (_i, [_p]),
+    "hp_set_trace": (_i, [_i, _p]),
     "hp_prefill_attn_paged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _i, _i, _i, _f,
                                    _i, _p]),
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),

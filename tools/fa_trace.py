@@ -13,9 +13,9 @@ cu = torch.tensor([0, T], device=DEV, dtype=torch.int32)
 tr = torch.zeros(12, 256, dtype=torch.int64, device=DEV)
 run = lambda: lib.prefill_attn(q, k, v, o, cu, 1, T, Hq, Hkv, d, 1 / math.sqrt(d), max_ctas=148)
 run(); torch.cuda.synchronize()
-lib.load().hp_set_fa_trace(tr.data_ptr())
+lib.load().hp_set_trace(0, tr.data_ptr())
 run(); torch.cuda.synchronize()
-lib.load().hp_set_fa_trace(None)
+lib.load().hp_set_trace(0, None)
 t = tr.cpu()
 base = int(t[0, 0])
 for i in range(40, 60):
