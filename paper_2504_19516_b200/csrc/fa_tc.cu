@@ -422,23 +422,29 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
         }
         if (grow) m_run = m_new;
         const float mb = (m_run == -INFINITY) ? 0.f : m_run;
-        // P = exp2(s * scale_log2 - m) (one FFMA + MUFU per score), bf16
-        // pairs over the first 64 columns of S_t; 8 partial row sums
-        float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // P = exp2(s * scale_log2 - m): packed f32x2 FFMA + two MUFU per
+        // score pair, bf16 pairs over the first 64 columns of S_t; 4 packed
+        // partial row sums (FADD2).  ~3 issue slots per score.
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nm2 = make_float2(-mb, -mb);
+        float2 l4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float w[32];
           uint32_t* wu = reinterpret_cast<uint32_t*>(w);
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const float a = ex2(fmaf(s[h * 64 + 2 * k], p.scale_log2, -mb));
-            const float b = ex2(fmaf(s[h * 64 + 2 * k + 1], p.scale_log2, -mb));
-            l8[k & 7] += a + b;
-            wu[k] = pack_bf16(a, b);
+            float2 x = __ffma2_rn(make_float2(s[h * 64 + 2 * k], s[h * 64 + 2 * k + 1]), sc2, nm2);
+            x.x = ex2(x.x);
+            x.y = ex2(x.y);
+            l4[k & 3] = __fadd2_rn(l4[k & 3], x);
+            wu[k] = pack_bf16(x.x, x.y);
           }
           tmem_st32(tS + h * 32, w);
         }
-        l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+        const float2 ls = __fadd2_rn(__fadd2_rn(l4[0], l4[1]), __fadd2_rn(l4[2], l4[3]));
+        l += ls.x + ls.y;
         tmem_st_wait();
         if (tr) p.trace[(t * 4 + 3) * 256 + sc] = clock64();
         tc_fence_before();

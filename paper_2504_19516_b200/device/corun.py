@@ -363,25 +363,31 @@ class CoRunner:
         return self.B * (self.C * 2 * kv_dim * 2 + 2 * kv_dim * 2 + 2 * m.hidden * 2)
 
     def decode_attn_gbs(self, sms: int, reps: int = 10) -> float:
-        """Decode attention alone on `sms` SMs (median of reps; the 269 MB KV
-        stream exceeds L2, so each launch reads HBM), GB/s algorithmic."""
+        """Decode attention alone on `sms` SMs, GB/s algorithmic: `reps`
+        back-to-back launches per event pair, median of three pairs."""
         st = self.pool.phase(DECODE, sms)
         m = self.model
         qkv = self.dsc.qkv[:self.B]
+        def launch():
+            lib.decode_attn(qkv, self.dcache.k, self.dcache.v, self.block_table, self.ctx,
+                            self.dsc.attn[:self.B], m.num_heads, m.num_kv_heads, m.head_dim, PAGE,
+                            self.layer.scale, ws=self.dsc.attn_ws, max_ctas=st.sms, stream=st.torch_stream)
+
+        # back-to-back launches between two events: the steady-state
+        # per-launch time (each launch streams 269 MB > L2, so no reuse)
         evs = []
         with torch.cuda.stream(st.torch_stream):
-            for i in range(reps + 1):
-                torch.cuda._sleep(50_000)
+            launch()
+            for _ in range(3):
+                torch.cuda._sleep(200_000)
                 a, b = _ev(), _ev()
                 a.record(st.torch_stream)
-                lib.decode_attn(qkv, self.dcache.k, self.dcache.v, self.block_table, self.ctx,
-                                self.dsc.attn[:self.B], m.num_heads, m.num_kv_heads, m.head_dim, PAGE,
-                                self.layer.scale, ws=self.dsc.attn_ws, max_ctas=st.sms, stream=st.torch_stream)
+                for _ in range(reps):
+                    launch()
                 b.record(st.torch_stream)
-                if i:
-                    evs.append((a, b))
+                evs.append((a, b))
         torch.cuda.synchronize()
-        t = statistics.median(a.elapsed_time(b) for a, b in evs) * 1e-3
+        t = statistics.median(a.elapsed_time(b) for a, b in evs) * 1e-3 / reps
         return self.decode_attn_bytes() / t / 1e9
 
     # ------------------------------------------------------------ workload

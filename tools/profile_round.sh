@@ -23,4 +23,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ge
     -o $OUT/upgate python tools/one_kernel.py gemm4096 $PM 8 > $OUT/ncu_upgate.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_decode_attn -s 2 -c 1 \
     -o $OUT/decode_attn python tools/one_kernel.py decode_attn 148 4 > $OUT/ncu_dattn.out 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fa2 -s 1 -c 1 \
+    -o $OUT/prefill_attn python tools/one_kernel.py attn4096 $PM 3 > $OUT/ncu_fa.out 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_swap -s 2 -c 1 \
+    -o $OUT/swap_o python tools/one_kernel.py swap 148 4 > $OUT/ncu_swap.out 2>&1
 ls -la $OUT
