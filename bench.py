@@ -191,6 +191,31 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------- replica plumbing
+def agree_split(dist, dm: int, n: int, device) -> tuple[int, int]:
+    """Every replica runs rank 0's (dm, n) so the job measures one config."""
+    if dist is None:
+        return dm, n
+    import torch
+
+    t = torch.tensor([dm, n], device=device)
+    dist.broadcast(t, 0)
+    return int(t[0]), int(t[1])
+
+
+def job_totals(dist, span_s: float, tokens: int, device) -> tuple[float, int]:
+    """Whole-job (max-over-ranks device span, total tokens of all replicas)."""
+    if dist is None:
+        return span_s, tokens
+    import torch
+
+    t = torch.tensor([span_s], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tk = torch.tensor([tokens], dtype=torch.float64, device=device)
+    dist.all_reduce(tk)
+    return float(t.item()), int(tk.item())
+
+
 # ------------------------------------------------------------------ main
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
@@ -255,9 +280,7 @@ def main(argv=None) -> int:
     ok = [c for c in candidates if c["slo_ok"]] or candidates
     best = max(ok, key=lambda c: c["tokens_per_s"])
     if dist is not None:  # identical split on every replica (rank 0 decides)
-        t = torch.tensor([best["dm"], best["n"]], device="cuda")
-        dist.broadcast(t, 0)
-        dmv, nv = int(t[0]), int(t[1])
+        dmv, nv = agree_split(dist, best["dm"], best["n"], "cuda")
         best = next((c for c in candidates if c["dm"] == dmv and c["n"] == nv),
                     dict(best, dm=dmv, pm=N - dmv, n=nv))
     pm, dm, n = best["pm"], best["dm"], best["n"]
@@ -273,15 +296,8 @@ def main(argv=None) -> int:
         res = cr.corun(pm, dm, args.steps, n, time_upgate=True)
         torch.cuda.nvtx.range_end(rid)
     torch.cuda.synchronize()
-    span = res.span_s
-    tokens = res.tokens
+    span, tokens = job_totals(dist, res.span_s, res.tokens, "cuda")
     if dist is not None:
-        t = torch.tensor([span], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        span = float(t.item())
-        tk = torch.tensor([tokens], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tk)
-        tokens = int(tk.item())
         dist.barrier()
     value = tokens / span
 
@@ -295,13 +311,7 @@ def main(argv=None) -> int:
     pin_dx.copy_(cr.dx.cpu())
 
     e2e_res = cr.corun_e2e(pm, dm, args.steps, n, pin_px, pin_py, pin_dx, pin_dy)
-    e2e_span = e2e_res.span_s
-    e2e_tokens = e2e_res.tokens
-    if dist is not None:
-        t = torch.tensor([e2e_span], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_span = float(t.item())
-        e2e_tokens *= world
+    e2e_span, e2e_tokens = job_totals(dist, e2e_res.span_s, e2e_res.tokens, "cuda")
     h2d = T * h * 2 + n * DECODE_BATCH * h * 2
     d2h = h2d
 
@@ -318,9 +328,9 @@ def main(argv=None) -> int:
     from paper_2504_19516_b200.perf_model import wave_stats
 
     wl = cr.layer.W
-    units = {"qkv": hplib.gemm_tiles(T, wl.w_qkv.shape[0]), "o_proj": hplib.gemm_tiles(T, wl.w_o.shape[0]),
-             "mlp_up_gate": hplib.gemm_tiles(T, wl.w_ug.shape[0]),
-             "mlp_down": hplib.gemm_tiles(T, wl.w_down.shape[0]),
+    units = {"qkv": hplib.gemm_plan(T, wl.w_qkv.shape[0], pm)[1], "o_proj": hplib.gemm_plan(T, wl.w_o.shape[0], pm)[1],
+             "mlp_up_gate": hplib.gemm_plan(T, wl.w_ug.shape[0], pm)[1],
+             "mlp_down": hplib.gemm_plan(T, wl.w_down.shape[0], pm)[1],
              "attn": min(-(-T // 128) * model.num_heads, pm)}
     g_s = res.group_s
     wave_idle = sum(g_s[g] * wave_stats(units[g], 1, pm).idle_ratio for g in units) / sum(g_s.values())

@@ -95,8 +95,13 @@ int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, co
 int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
                    int ldr, int T, int N, int K, int epilogue, int max_ctas, uint64_t* cta_times,
                    void* stream);
-/* Output tiles (persistent-grid work units) of hp_gemm for T tokens, N features. */
+/* Output tiles (persistent-grid work units) of hp_gemm for T tokens, N
+ * features at the 256-wide tile. */
 int hp_gemm_tiles(int T, int N);
+/* The tile width hp_gemm picks for a `max_ctas`-SM partition (128 or 256:
+ * fewer wave-quantised column-rounds, wave_stats perf_model.py:157-169) and
+ * the resulting tile count. */
+int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles);
 
 /* Swap-AB stream-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
  * hp_gemm; W streams through UMMA-M and the (tile, k-block) space is split

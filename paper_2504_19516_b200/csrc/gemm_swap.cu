@@ -340,13 +340,33 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             float4 a[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int k = 0; k < ncontrib; ++k) {
-              const float* src = base + size_t(k) * (SBM * BN);
+            // two contributors per round with all 16 loads in flight (the
+            // partials are L2 hits; a one-at-a-time loop paid one L2 round
+            // trip per contributor on the GEMM's critical tail)
+            auto ld = [&](int k, int i) {
+              const int f = i * 128 + et;            // float4 index within the chunk
+              const int r = f >> 3, cc = (f & 7) * 4;
+              return __ldcg(reinterpret_cast<const float4*>(base + size_t(k) * (SBM * BN) + size_t(r) * BN +
+                                                            c * 32 + cc));
+            };
+            int k = 0;
+            for (; k + 1 < ncontrib; k += 2) {
+              float4 x0[8], x1[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const int f = i * 128 + et;          // float4 index within the chunk
-                const int r = f >> 3, cc = (f & 7) * 4;
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(src + size_t(r) * BN + c * 32 + cc));
+                x0[i] = ld(k, i);
+                x1[i] = ld(k + 1, i);
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                a[i].x += x0[i].x; a[i].y += x0[i].y; a[i].z += x0[i].z; a[i].w += x0[i].w;
+                a[i].x += x1[i].x; a[i].y += x1[i].y; a[i].z += x1[i].z; a[i].w += x1[i].w;
+              }
+            }
+            if (k < ncontrib) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 x = ld(k, i);
                 a[i].x += x.x; a[i].y += x.y; a[i].z += x.z; a[i].w += x.w;
               }
             }

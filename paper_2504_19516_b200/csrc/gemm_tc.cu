@@ -25,6 +25,7 @@
 #include "../../include/hp.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace hp {
 
@@ -280,7 +281,38 @@ extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, 
   return hp_gemm_traced(X, ldx, W, ldw, Y, ldy, R, ldr, T, N, K, epilogue, max_ctas, nullptr, stream);
 }
 
+// Tile-width choice for a partition of `ctas` SMs.  A persistent grid over
+// `tiles` runs ceil(tiles / ctas) rounds (wave_stats, perf_model.py:157-169);
+// halving BN doubles the tile count, which can cut the rounds' total width
+// when few tiles are left for the last wave (T = 1024 qkv on 148 SMs: 192
+// tiles of 256 = 2 rounds x 256 cols vs 384 tiles of 128 = 3 x 128).  A
+// 128-wide tile is 15-30 % slower per FLOP on B200 (tools/gemm_bn_sweep.py:
+// the activation tile is re-streamed per 128 columns and the MMA is half
+// as wide), folded in as 1.25.
+// HP_GEMM_BN=128|256 forces a width (measurement).
+static int gemm_bn(int T, int N, int ctas) {
+  static const int forced = [] {
+    const char* e = std::getenv("HP_GEMM_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 128 || (forced == 256 && N % 256 == 0)) return forced;
+  if (N % 256 != 0) return 128;
+  const int m = (T + BM - 1) / BM;
+  const long t256 = long(m) * (N / 256), t128 = long(m) * (N / 128);
+  const double c256 = double((t256 + ctas - 1) / ctas) * 256.0;
+  const double c128 = double((t128 + ctas - 1) / ctas) * 128.0 * 1.25;
+  return c128 < c256 ? 128 : 256;
+}
+
 extern "C" int hp_gemm_tiles(int T, int N) { return ((T + BM - 1) / BM) * (N / 256); }
+
+extern "C" int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles) {
+  HP_CHECK_ARG(T >= 1 && N % 128 == 0 && max_ctas >= 1, "hp_gemm_plan: bad shape");
+  const int b = gemm_bn(T, N, max_ctas);
+  if (bn) *bn = b;
+  if (tiles) *tiles = ((T + BM - 1) / BM) * (N / b);
+  return HP_OK;
+}
 
 extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                               const void* R, int ldr, int T, int N, int K, int epilogue, int max_ctas,
@@ -291,9 +323,9 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
   HP_CHECK_ARG(epilogue >= EPI_STORE && epilogue <= EPI_SILU, "hp_gemm: bad epilogue");
   HP_CHECK_ARG(epilogue != EPI_RESID || R != nullptr, "hp_gemm: residual epilogue needs R");
   HP_CHECK_ARG(max_ctas >= 1, "hp_gemm: max_ctas must be >= 1");
-  HP_CHECK_ARG(N % 256 == 0, "hp_gemm: N must be a multiple of 256 (tiled weight layout)");
+  HP_CHECK_ARG(N % 128 == 0, "hp_gemm: N must be a multiple of 128 (tiled weight layout)");
   HP_CHECK_ARG(ldw == K, "hp_gemm: W must be in the tiled layout (ldw == K)");
-  const int BN = 256;
+  const int BN = gemm_bn(T, N, max_ctas);
   CUtensorMap ta;
   int rc = cached_tmap_bf16(&ta, X, T, K, ldx, BM, BK, true);
   if (rc) return rc;
@@ -316,6 +348,6 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
   const int units = p.m_tiles * p.n_tiles;
   const int grid = std::min(units, max_ctas);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return launch<256>(ta, p, grid, st);
+  return BN == 128 ? launch<128>(ta, p, grid, st) : launch<256>(ta, p, grid, st);
 }
 

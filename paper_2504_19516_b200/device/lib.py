@@ -35,6 +35,7 @@ SIGNATURES = {
     "hp_gemm": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
     "hp_gemm_traced": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "hp_gemm_tiles": (_i, [_i, _i]),
+    "hp_gemm_plan": (_i, [_i, _i, _i, C.POINTER(_i), C.POINTER(_i)]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
@@ -182,6 +183,13 @@ def prefill_attn(q, k, v, o, cu_seqlens, nseq: int, max_seqlen: int, Hq: int, Hk
     check(load().hp_prefill_attn(_ptr(q), q.stride(0), _ptr(k), k.stride(0), _ptr(v), v.stride(0),
                                  _ptr(o), o.stride(0), _ptr(cu_seqlens), nseq, q.shape[0], max_seqlen, Hq, Hkv,
                                  d, scale, max_ctas, _stream(stream)), "hp_prefill_attn")
+
+
+def gemm_plan(T: int, N: int, max_ctas: int) -> tuple[int, int]:
+    """(tile width, tile count) hp_gemm uses on a `max_ctas`-SM partition."""
+    bn, tiles = C.c_int(), C.c_int()
+    check(load().hp_gemm_plan(T, N, max_ctas, C.byref(bn), C.byref(tiles)), "hp_gemm_plan")
+    return bn.value, tiles.value
 
 
 def prefill_attn_paged(q, kcache, vcache, block_table, cu_seqlens, prior_lens, nseq: int, max_seqlen: int,

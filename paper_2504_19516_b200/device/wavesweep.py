@@ -31,7 +31,7 @@ from .partition import DECODE, PREFILL, PartitionPool
 
 def measure(pool: PartitionPool, x, w, y, epi, resid, n: int, reps: int = 3):
     st = pool.phase(DECODE, n) if n < pool.n else pool.full(PREFILL)
-    grid = min(lib.gemm_tiles(x.shape[0], w.shape[0]), st.sms)
+    grid = min(lib.gemm_plan(x.shape[0], w.shape[0], st.sms)[1], st.sms)
     times = torch.zeros(grid, 3, dtype=torch.int64, device=x.device)
     best = None
     with torch.cuda.stream(st.torch_stream):
@@ -72,9 +72,9 @@ def main(argv=None) -> int:
                  ("mlp_up_gate", xh, W.w_ug, torch.empty(T, I, **bf), lib.EPI_SILU, None),
                  ("mlp_down", xi, W.w_down, torch.empty(T, h, **bf), lib.EPI_RESID, xh)]
         for name, x, w, y, epi, r in gemms:
-            tiles = lib.gemm_tiles(T, w.shape[0])
             for n in grid:
                 idle, span, sms_seen, n_real = measure(pool, x, w, y, epi, r, n)
+                tiles = lib.gemm_plan(T, w.shape[0], n_real)[1]
                 pred = wave_stats(tiles, 1, n_real)
                 row = {"kernel": name, "T": T, "tiles": tiles, "n": n_real,
                        "predicted_idle": pred.idle_ratio, "waves": pred.waves, "tail_sms": pred.tail_sms,
