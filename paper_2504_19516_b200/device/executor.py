@@ -47,7 +47,12 @@ class B200Executor:
     def __init__(self, model: ModelSpec, gpu: GpuSpec, device: int = 0, seed: int = 0,
                  max_prefill_tokens: int = 32768, max_decode_batch: int = 256,
                  pool_tokens: int = 1 << 21, sm_step: int = 8, pool: PartitionPool | None = None,
-                 memo: bool = False):
+                 memo: bool = False, full_model: bool = False, l_step: int = 4):
+        """full_model=True keeps every layer of `model` resident (distinct
+        random weights, per-layer paged KV pools): a decode step is measured
+        as the whole model's layers back to back and a prefill step as
+        `l_step` distinct layers (scheduler.py:47 l_step), instead of one
+        resident layer scaled by the layer count."""
         if model.head_dim not in (64, 128):
             raise InvalidArgumentError("B200Executor supports head_dim 64 or 128")
         self.model = model
@@ -61,17 +66,33 @@ class B200Executor:
                 "use perf_model.b200_spec() (or [gpu] num_sms = 148)")
         gen = torch.Generator(device="cpu")
         gen.manual_seed(seed)
-        self.layer = DeviceLayer(model, LayerWeights.random(model, self.dev, gen), self.dev,
-                                 max_pos=max(max_prefill_tokens, 1 << 15) + 1)
+        self.full_model = full_model
+        self.l_step = max(1, min(l_step, model.num_layers)) if full_model else 1
+        max_pos = max(max_prefill_tokens, 1 << 15) + 1
+        if full_model:
+            g = torch.Generator(device=self.dev)
+            g.manual_seed(seed)
+            self.layers = [DeviceLayer(model, LayerWeights.random_device(model, self.dev, g), self.dev,
+                                       max_pos=max_pos) for _ in range(model.num_layers)]
+            for lyr in self.layers[1:]:
+                lyr.rope = self.layers[0].rope
+        else:
+            self.layers = [DeviceLayer(model, LayerWeights.random(model, self.dev, gen), self.dev,
+                                       max_pos=max_pos)]
+        self.layer = self.layers[0]
         h = model.hidden
         bf = dict(dtype=torch.bfloat16, device=self.dev)
         self.max_prefill_tokens = max_prefill_tokens
         self.px = torch.randn(max_prefill_tokens, h, generator=gen).to(**bf)
         self.py = torch.empty_like(self.px)
         self.psc = PrefillScratch(model, max_prefill_tokens, self.dev)
-        self.pcache = KVCache(-(-max_prefill_tokens // PAGE), model.num_kv_heads, model.head_dim, self.dev)
+        self.pcaches = [KVCache(-(-max_prefill_tokens // PAGE), model.num_kv_heads, model.head_dim, self.dev)
+                        for _ in range(self.l_step)]
+        self.pcache = self.pcaches[0]
         self.pool_blocks = max(1, pool_tokens // PAGE)
-        self.dcache = KVCache(self.pool_blocks, model.num_kv_heads, model.head_dim, self.dev)
+        self.dcaches = [KVCache(self.pool_blocks, model.num_kv_heads, model.head_dim, self.dev)
+                        for _ in range(len(self.layers))]
+        self.dcache = self.dcaches[0]
         self.max_decode_batch = max_decode_batch
         self.dx = torch.randn(max_decode_batch, h, generator=gen).to(**bf)
         self.dy = torch.empty_like(self.dx)
@@ -113,14 +134,21 @@ class B200Executor:
         return B, ctx, bt, pos, slots
 
     def _launch_prefill(self, ps, args):
+        """One prefill unit: l_step distinct layers (1 unless full_model)."""
         T, cu, nseq, mx, pos, slots = args
-        self.layer.prefill(self.px[:T], self.py[:T], self.psc, cu, nseq, mx, pos, slots, self.pcache,
-                           ps.sms, ps.torch_stream)
+        x, y = self.px[:T], self.py[:T]
+        for i in range(self.l_step):
+            self.layers[i].prefill(x, y, self.psc, cu, nseq, mx, pos, slots, self.pcaches[i], ps.sms,
+                                   ps.torch_stream)
+            x, y = y, x
 
     def _launch_decode(self, ds, args):
+        """One decode unit: every resident layer (the whole model if full_model)."""
         B, ctx, bt, pos, slots = args
-        self.layer.decode(self.dx[:B], self.dy[:B], self.dsc, ctx, pos, slots, bt, self.dcache, ds.sms,
-                          ds.torch_stream)
+        x, y = self.dx[:B], self.dy[:B]
+        for lyr, cache in zip(self.layers, self.dcaches):
+            lyr.decode(x, y, self.dsc, ctx, pos, slots, bt, cache, ds.sms, ds.torch_stream)
+            x, y = y, x
 
     # --------------------------------------------------------------- timing
     def _measure(self, phase: str, es: ExecutionState) -> float:
@@ -171,8 +199,11 @@ class B200Executor:
 
     def _cover_count(self, phase: str, es: ExecutionState) -> int:
         """How many layers of the other phase overlap one layer of `phase`."""
-        p = srm_prefill_layer_s(es, self.model, self.gpu) if es.prefill_lens and es.prefill_sms else 0.0
-        d = (srm_decode_step_s(es, self.model, self.gpu) / self.model.num_layers
+        # SRM estimates of one launch unit of each phase (l_step prefill
+        # layers; one decode layer, or the whole step with full_model)
+        p = (self.l_step * srm_prefill_layer_s(es, self.model, self.gpu)
+             if es.prefill_lens and es.prefill_sms else 0.0)
+        d = (srm_decode_step_s(es, self.model, self.gpu) * len(self.layers) / self.model.num_layers
              if es.decode_ctx_lens and es.decode_sms else 0.0)
         if phase == "prefill":
             return max(1, min(64, math.ceil(3.0 * p / max(d, 1e-9))))
@@ -197,10 +228,10 @@ class B200Executor:
         return v
 
     def prefill_layer_s(self, es: ExecutionState) -> float:
-        return self._measured("prefill", es)
+        return self._measured("prefill", es) / self.l_step
 
     def decode_step_s(self, es: ExecutionState) -> float:
-        return self.model.num_layers * self._measured("decode", es)
+        return self.model.num_layers / len(self.layers) * self._measured("decode", es)
 
     def _hybrid_args(self, chunks, decode_ctx_lens):
         """Device inputs of one hybrid batch: chunk rows first, then decode
@@ -242,9 +273,12 @@ class B200Executor:
 
     def _launch_hybrid(self, st, a):
         T = a["T"]
-        self.layer.hybrid(self.px[:T], self.py[:T], self.psc, self.dsc, a["Tc"], a["cu"], a["cu"].shape[0] - 1,
-                          a["max_chunk"], a["prior"], a["cbt"], a["dctx"], a["dbt"], a["pos"], a["slots"],
-                          self.dcache, st.sms, st.torch_stream)
+        x, y = self.px[:T], self.py[:T]
+        for lyr, cache in zip(self.layers, self.dcaches):
+            lyr.hybrid(x, y, self.psc, self.dsc, a["Tc"], a["cu"], a["cu"].shape[0] - 1, a["max_chunk"],
+                       a["prior"], a["cbt"], a["dctx"], a["dbt"], a["pos"], a["slots"], cache, st.sms,
+                       st.torch_stream)
+            x, y = y, x
 
     def hybrid_iteration_s(self, chunks, decode_ctx_lens, sms: int) -> float:
         """One lockstep hybrid iteration (all layers) on `sms` SMs -- the
@@ -269,7 +303,7 @@ class B200Executor:
             b_ev.record(st.torch_stream)
         torch.cuda.synchronize(self.dev)
         self.calls["hybrid"] = self.calls.get("hybrid", 0) + 1
-        return self.model.num_layers * a_ev.elapsed_time(b_ev) * 1e-3
+        return self.model.num_layers / len(self.layers) * a_ev.elapsed_time(b_ev) * 1e-3
 
     def alpha(self, phase: str, sms: int, tokens: int) -> float:
         """Measured / SRM at a canonical shape of `tokens` on `sms` SMs."""

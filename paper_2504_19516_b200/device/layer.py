@@ -85,6 +85,20 @@ class LayerWeights:
         return cls.from_dense(w(model.qkv_out_dim, h), w(h, h), gate, up, w(h, I), norm(), norm())
 
     @classmethod
+    def random_device(cls, model: ModelSpec, device, gen: torch.Generator, std: float = 0.02):
+        """Random weights drawn on the GPU (a 32-layer model's 14 GB would take
+        minutes through the host generator)."""
+        h, I = model.hidden, model.intermediate
+
+        def w(*shape):
+            return (torch.randn(*shape, generator=gen, device=device) * std).to(torch.bfloat16)
+
+        def norm():
+            return (1.0 + 0.1 * torch.randn(h, generator=gen, device=device)).to(torch.bfloat16)
+
+        return cls.from_dense(w(model.qkv_out_dim, h), w(h, h), w(I, h), w(I, h), w(h, I), norm(), norm())
+
+    @classmethod
     def from_dense(cls, w_qkv, w_o, w_gate, w_up, w_down, attn_norm, mlp_norm):
         """Row-major torch [out, in] device weights -> the resident layout:
         gate/up interleaved, every matrix tiled for bulk-copy streaming."""

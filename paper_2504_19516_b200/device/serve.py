@@ -71,6 +71,9 @@ def main(argv=None) -> int:
     ap.add_argument("--policies", default="bullet,chunked,nopartition")
     ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--full-model", action="store_true",
+                    help="keep all 32 layers resident: decode steps measured over the whole model, "
+                         "prefill steps over l_step distinct layers")
     a = ap.parse_args(argv)
 
     import torch
@@ -93,7 +96,8 @@ def main(argv=None) -> int:
                               TRACE_PRESETS["sharegpt-like"][1], seed=a.seed)
     mine = shard(trace, rank, world)
     ex = B200Executor(MODEL_PRESETS["llama3-8b"], gpu, device=local, max_prefill_tokens=65536,
-                      max_decode_batch=256, pool_tokens=1 << 20, memo=True)
+                      max_decode_batch=256, pool_tokens=(1 << 18) if a.full_model else (1 << 20), memo=True,
+                      full_model=a.full_model)
     lines = []
     for pol in a.policies.split(","):
         agg = run_policy(pol, mine, ex, gpu, a.chunk)
@@ -115,7 +119,9 @@ def main(argv=None) -> int:
                     "mean_prefill_sms": statistics.mean(p["mean_prefill_sms"] for p in per),
                     "mean_decode_sms": statistics.mean(p["mean_decode_sms"] for p in per),
                     "device_calls": dict(ex.calls), "memo_hits": ex.memo_hits,
-                    "timing": "every step time measured on the B200 (CUDA events, green-context partitions)"}
+                    "timing": "every step time measured on the B200 (CUDA events, green-context partitions)",
+                    "measured_unit": "whole-model decode step, l_step prefill layers" if a.full_model
+                    else "one resident layer x num_layers"}
             print(json.dumps(line), flush=True)
             lines.append(line)
     if rank == 0 and a.out:

@@ -72,3 +72,19 @@ def test_hybrid_iteration_and_chunked_policy_on_hardware(ex):
     rep = E.run(cfg, trace, oracle=ex)
     assert rep.aggregates["finished"] == len(trace)
     assert ex.calls["hybrid"] > 0
+
+
+def test_full_model_executor_measures_whole_decode_step():
+    # every layer resident, decode measured over the whole model
+    from paper_2504_19516_b200.device.executor import B200Executor
+
+    m = MODEL_PRESETS["llama3-8b"]
+    fx = B200Executor(m, b200_spec(), max_prefill_tokens=4096, max_decode_batch=32, pool_tokens=1 << 15,
+                      full_model=True, l_step=4)
+    assert len(fx.layers) == m.num_layers and fx.l_step == 4
+    es = ExecutionState(decode_ctx_lens=(1024,) * 16, decode_sms=148)
+    step = fx.decode_step_s(es)
+    pl = fx.prefill_layer_s(ExecutionState(prefill_lens=(2048,), prefill_sms=148))
+    assert 0 < pl < 0.01 and 32 * 40e-6 < step < 0.1
+    del fx
+    torch.cuda.empty_cache()
