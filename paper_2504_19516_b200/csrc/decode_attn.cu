@@ -502,6 +502,22 @@ extern "C" size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits) 
   return size_t(B) * Hq * max_splits * (d + 2) * sizeof(float);
 }
 
+// Split count the launch below picks (1 = no combine kernel).
+static int decode_tps(int B, int Hkv, int max_pages, int page, int max_ctas) {
+  const int max_tiles = max_pages * (page / DA_TILE);
+  const int pairs = B * Hkv;
+  int tps = max_tiles;
+  while (tps > 2 && pairs * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
+  return std::max(1, std::min(tps, (DA_WIN - 1) * (page / DA_TILE)));  // unit pages fit the window
+}
+
+extern "C" int hp_decode_attn_launches(int B, int Hkv, int max_pages, int page, int max_ctas) {
+  if (B < 1 || Hkv < 1 || max_pages < 1 || page < DA_TILE || max_ctas < 1) return 0;
+  const int max_tiles = max_pages * (page / DA_TILE);
+  const int tps = decode_tps(B, Hkv, max_pages, page, max_ctas);
+  return (max_tiles + tps - 1) / tps > 1 ? 2 : 1;
+}
+
 extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const void* vcache,
                               const int* block_table, int max_pages, const int* ctx_lens, void* out,
                               int ldo, int B, int Hq, int Hkv, int d, int page, int num_blocks,
@@ -532,10 +548,7 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   p.scale_log2 = scale * 1.4426950408889634f;
   // split so that the unit count covers the grid ~4x, at least 2 tiles/unit
   const int max_tiles = max_pages * (page / DA_TILE);
-  const int pairs = B * Hkv;
-  int tps = max_tiles;
-  while (tps > 2 && pairs * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
-  p.tps = std::max(1, std::min(tps, (DA_WIN - 1) * (page / DA_TILE)));  // unit pages fit the window
+  p.tps = decode_tps(B, Hkv, max_pages, page, max_ctas);
   p.max_splits = (max_tiles + p.tps - 1) / p.tps;
   if (p.max_splits > 1) {
     HP_CHECK_ARG(workspace != nullptr, "hp_decode_attn: workspace required for split contexts");

@@ -141,9 +141,10 @@ class CoRunner:
             self._graphs[key] = g
         return g
 
-    def launches_per_decode_step(self) -> int:
-        splits = 1  # decode attention may add a split-combine launch
-        return 9 + splits
+    def launches_per_decode_step(self, sms: int) -> int:
+        """Kernels in one decode layer-step on `sms` SMs (the CUDA graph's nodes)."""
+        m = self.model
+        return 8 + lib.decode_attn_launches(self.B, m.num_kv_heads, self.block_table.shape[1], PAGE, sms)
 
     # --------------------------------------------------------------- timing
     def isolated(self, phase: int, sms: int, reps: int = 5) -> float:

@@ -248,7 +248,7 @@ class DeviceLayer:
                       stream=stream)
         lib.gemm_swap(sc.act[:B], self.W.w_down, y, ws, cnt, lib.EPI_RESID, resid=sc.h[:B],
                       max_ctas=sms, stream=stream)
-        return 9
+        return 8 + lib.decode_attn_launches(B, Hkv, block_table.shape[1], cache.page, sms)
 
 
     # --------------------------------------------------------------- hybrid
