@@ -34,6 +34,7 @@ enum { EPI_STORE = 0, EPI_RESID = 1, EPI_SILU = 2 };
 struct GemmParams {
   int Ma, Nb, K;
   int m_tiles, n_tiles, k_splits, kb_per_split, num_kb;
+  int group_m;  // m-tiles per rasterization group (L2 reuse of the activation block)
   const uint8_t* w;  // weights in the tiled layout (hp_tile_weight)
   __nv_bfloat16* out;
   int ldo;
@@ -55,6 +56,23 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
 };
+
+// Tile index -> (m-tile, n-tile).  Tiles are walked in groups of `group_m`
+// m-tiles: a wave of CTAs covers group_m x (grid / group_m) tiles, so the
+// group's activation rows (group_m x 128 x K bf16) stay L2-resident while
+// the weight tiles stream past once per group.  With group_m = m_tiles this
+// is the plain column-major order (every weight tile read once, activations
+// re-read per column -- right when all activations fit in L2).  The order
+// does not change the tile count, so the rounds stay wave_stats(tiles, 1, n).
+__device__ __forceinline__ void tile_coords(const GemmParams& p, int tile, int& mt, int& nt) {
+  const int per_group = p.group_m * p.n_tiles;
+  const int g = tile / per_group;
+  const int first = g * p.group_m;
+  const int gsize = min(p.m_tiles - first, p.group_m);
+  const int r = tile - g * per_group;
+  mt = first + r % gsize;
+  nt = r / gsize;
+}
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
@@ -134,7 +152,8 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t g = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
       const int tile = u / p.k_splits, ks = u % p.k_splits;
-      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      int mt, nt;
+      tile_coords(p, tile, mt, nt);
       const int kb0 = ks * p.kb_per_split;
       const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
@@ -197,7 +216,8 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < total; u += gridDim.x) {
       const int tile = u / p.k_splits;
-      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      int mt, nt;
+      tile_coords(p, tile, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
@@ -335,6 +355,14 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
   p.Nb = N;
   p.K = K;
   p.m_tiles = ceil_div(T, BM);
+  // rasterization group: keep the activation block of a group within ~32 MB
+  // of the 126 MB L2 (decode traffic shares it during co-execution)
+  {
+    const long a_tile_bytes = long(BM) * K * 2;
+    const long budget = 32l << 20;
+    const long all = a_tile_bytes * p.m_tiles;
+    p.group_m = all <= 2 * budget ? p.m_tiles : int(std::max<long>(8, budget / a_tile_bytes));
+  }
   p.n_tiles = N / BN;
   p.k_splits = 1;
   p.num_kb = K / BK;

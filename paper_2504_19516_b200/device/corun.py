@@ -90,7 +90,7 @@ class CoRunner:
         # prefill workload
         self.px = torch.randn(self.T, h, generator=gen).to(**bf)
         self.py = torch.empty(self.T, h, **bf)
-        self.psc = PrefillScratch(model, self.T, self.dev)
+        self.psc = PrefillScratch(model, self.T + self.B, self.dev)  # hybrid batches: chunk + decode rows
         pblocks = -(-self.T // PAGE)
         self.pcache = KVCache(pblocks, model.num_kv_heads, model.head_dim, self.dev)
         self.p_cu = torch.tensor([0, self.T], dtype=torch.int32, device=self.dev)

@@ -268,6 +268,9 @@ class DeviceLayer:
         T = x.shape[0]
         Tc = n_chunk_tokens
         B = T - Tc
+        if T > sc.max_tokens or B > dsc.max_batch or Tc < 0:
+            raise ValueError(f"hybrid batch of {Tc} chunk + {B} decode rows exceeds the scratch "
+                             f"({sc.max_tokens} rows, {dsc.max_batch} decode)")
         Hq, Hkv, d = self.Hq, self.Hkv, self.d
         qkv = sc.qkv[:T]
         swap = T <= dsc.max_batch
