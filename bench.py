@@ -368,7 +368,7 @@ def main(argv=None) -> int:
                "sample": f"numpy oracle: 1 prefill layer x {CPU_SAMPLE_T} tokens + 1 decode step "
                          f"(B={DECODE_BATCH}, ctx {DECODE_CTX}), x2"}
 
-    per_step_launches = 8 + n * cr.launches_per_decode_step(dm)  # prefill layer: 8 kernels
+    per_step_launches = 7 + n * cr.launches_per_decode_step(dm)  # prefill layer: 7 kernels
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * span / args.steps, "higher_is_better": True,

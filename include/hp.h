@@ -89,6 +89,16 @@ int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream
  * (workload.py:162-210) at phase "prefill". */
 int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
             int ldr, int T, int N, int K, int epilogue, int max_ctas, void* stream);
+/* The prefill QKV projection with RoPE and the paged K/V write fused into
+ * its epilogue (kernel group `qkv` + the `kv_write` bytes of `attn`,
+ * workload.py:164-170, 180-182): Y[T, (Hq+2Hkv)d] = X . W^T with q and k heads
+ * rotated (as hp_rope_kv_write does) before the bf16 store, and k / v heads
+ * also written to kcache / vcache at slot_mapping[t].  Replaces hp_gemm
+ * (EPI_STORE) + hp_rope_kv_write on the prefill path. */
+int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, int T, int Hq,
+                     int Hkv, int d, int K, const int* positions, const float* cos_sin,
+                     const int* slot_mapping, void* kcache, void* vcache, int page, int max_ctas,
+                     void* stream);
 /* Same, recording per-CTA {smid, start_ns, end_ns} into cta_times[grid][3]
  * (config-3 wave measurement: measured idle = 1 - sum(busy) / (n * span),
  * against wave_stats(hp_gemm_tiles(T, N), 1, n), perf_model.py:157-169). */

@@ -29,7 +29,7 @@
 
 namespace hp {
 
-enum { EPI_STORE = 0, EPI_RESID = 1, EPI_SILU = 2 };
+enum { EPI_STORE = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_ROPE = 3 };
 
 struct GemmParams {
   int Ma, Nb, K;
@@ -42,6 +42,13 @@ struct GemmParams {
   int ldr;
   int epi;
   uint64_t* cta_times;  // optional [grid][3] = {smid, start_ns, end_ns} (wave measurement)
+  // EPI_ROPE (fused QKV epilogue): rotary embedding of q/k heads, paged K/V write
+  const int* pos;
+  const float* cos_sin;  // fp32 [max_pos, d] = [cos(d/2) | sin(d/2)]
+  const int* slots;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  int page, Hq, Hkv, hd;
 };
 
 constexpr int BM = 128;
@@ -224,7 +231,73 @@ __global__ void __launch_bounds__(192, 1)
       {
         const int gm = mt * BM + row;
         const bool ok = gm < p.Ma;
-        if (p.epi == EPI_SILU) {
+        if (p.epi == EPI_ROPE) {
+          // the tile's BN columns are BN/hd whole heads of the q | k | v blocks
+          const int half = p.hd / 2;
+          const int pos = ok ? p.pos[gm] : 0;
+          const float* cs = p.cos_sin + size_t(pos) * p.hd;
+          int blk = 0, off = 0;
+          if (ok) {
+            const int sl = p.slots[gm];
+            blk = sl / p.page;
+            off = sl % p.page;
+          }
+#pragma unroll 1
+          for (int hh = 0; hh < BN / p.hd; ++hh) {
+            const int head = (nt * BN) / p.hd + hh;
+            const bool rot = head < p.Hq + p.Hkv;
+#pragma unroll 1
+            for (int c = 0; c < half / 32; ++c) {
+              float x[32], y[32];
+              tmem_ld32(taddr + hh * p.hd + c * 32, x);
+              tmem_ld32(taddr + hh * p.hd + half + c * 32, y);
+              tmem_ld_wait();
+              if (!ok) continue;
+              if (rot) {  // y[i] = x cos - x' sin, y' = x' cos + x sin (rotate_half)
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                  const float4 co = *reinterpret_cast<const float4*>(cs + c * 32 + j);
+                  const float4 si = *reinterpret_cast<const float4*>(cs + half + c * 32 + j);
+                  const float cc[4] = {co.x, co.y, co.z, co.w}, ss[4] = {si.x, si.y, si.z, si.w};
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    // rotate the bf16-rounded projection, exactly as the
+                    // unfused GEMM store + hp_rope_kv_write pair does
+                    const float a = __bfloat162float(__float2bfloat16(x[j + k]));
+                    const float b = __bfloat162float(__float2bfloat16(y[j + k]));
+                    x[j + k] = a * cc[k] - b * ss[k];
+                    y[j + k] = b * cc[k] + a * ss[k];
+                  }
+                }
+              }
+              __nv_bfloat16* dst = p.out + size_t(gm) * p.ldo + size_t(head) * p.hd;
+              store_row32(dst + c * 32, x);
+              store_row32(dst + half + c * 32, y);
+              if (head >= p.Hq) {  // k or v head -> paged cache page [page/64][hd/64][64][64], swizzled
+                const int kvh = rot ? head - p.Hq : head - p.Hq - p.Hkv;
+                __nv_bfloat16* cache = rot ? p.kc : p.vc;
+                const size_t base = ((size_t(blk) * p.Hkv + kvh) * (p.page / 64) + off / 64) * (p.hd / 64);
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                  const float* v = part ? y : x;
+                  const int j0 = (part ? half : 0) + c * 32;  // first head dim of these 32
+#pragma unroll
+                  for (int q8 = 0; q8 < 4; ++q8) {
+                    const int j = j0 + q8 * 8;
+                    uint4 w;
+                    w.x = pack_bf16(v[q8 * 8 + 0], v[q8 * 8 + 1]);
+                    w.y = pack_bf16(v[q8 * 8 + 2], v[q8 * 8 + 3]);
+                    w.z = pack_bf16(v[q8 * 8 + 4], v[q8 * 8 + 5]);
+                    w.w = pack_bf16(v[q8 * 8 + 6], v[q8 * 8 + 7]);
+                    const size_t e = (base + j / 64) * 4096 + size_t(off & 63) * 64 +
+                                     ((((j & 63) >> 3) ^ (off & 7)) << 3);
+                    *reinterpret_cast<uint4*>(cache + e) = w;
+                  }
+                }
+              }
+            }
+          }
+        } else if (p.epi == EPI_SILU) {
 #pragma unroll 1
           for (int h = 0; h < BN / 128; ++h) {
 #pragma unroll 1
@@ -294,6 +367,55 @@ using namespace hp;
 extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                               const void* R, int ldr, int T, int N, int K, int epilogue, int max_ctas,
                               uint64_t* cta_times, void* stream);
+
+static int gemm_bn(int T, int N, int ctas);
+
+extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, int T,
+                                int Hq, int Hkv, int d, int K, const int* positions, const float* cos_sin,
+                                const int* slot_mapping, void* kcache, void* vcache, int page, int max_ctas,
+                                void* stream) {
+  HP_CHECK_ARG(X && W && Y && positions && cos_sin && slot_mapping && kcache && vcache,
+               "hp_gemm_qkv_rope: null pointer");
+  HP_CHECK_ARG(T >= 1 && K % 128 == 0 && ldw == K, "hp_gemm_qkv_rope: K must be a multiple of 128 (tiled W)");
+  HP_CHECK_ARG(d == 64 || d == 128, "hp_gemm_qkv_rope: head_dim must be 64 or 128");
+  HP_CHECK_ARG(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0, "hp_gemm_qkv_rope: bad head counts");
+  HP_CHECK_ARG(page >= 64 && page % 64 == 0 && max_ctas >= 1, "hp_gemm_qkv_rope: page must be a multiple of 64");
+  const int N = (Hq + 2 * Hkv) * d;
+  HP_CHECK_ARG(N % 128 == 0 && ldy >= N && ldy % 8 == 0, "hp_gemm_qkv_rope: (Hq+2Hkv)*d must be a multiple of 128");
+  const int BN = gemm_bn(T, N, max_ctas);
+  CUtensorMap ta;
+  int rc = cached_tmap_bf16(&ta, X, T, K, ldx, BM, BK, true);
+  if (rc) return rc;
+  GemmParams p{};
+  p.w = static_cast<const uint8_t*>(W);
+  p.Ma = T;
+  p.Nb = N;
+  p.K = K;
+  p.m_tiles = ceil_div(T, BM);
+  p.n_tiles = N / BN;
+  p.k_splits = 1;
+  p.num_kb = K / BK;
+  p.kb_per_split = p.num_kb;
+  {
+    const long a_tile_bytes = long(BM) * K * 2, budget = 32l << 20, all = a_tile_bytes * p.m_tiles;
+    p.group_m = all <= 2 * budget ? p.m_tiles : int(std::max<long>(8, budget / a_tile_bytes));
+  }
+  p.out = static_cast<__nv_bfloat16*>(Y);
+  p.ldo = ldy;
+  p.epi = EPI_ROPE;
+  p.pos = positions;
+  p.cos_sin = cos_sin;
+  p.slots = slot_mapping;
+  p.kc = static_cast<__nv_bfloat16*>(kcache);
+  p.vc = static_cast<__nv_bfloat16*>(vcache);
+  p.page = page;
+  p.Hq = Hq;
+  p.Hkv = Hkv;
+  p.hd = d;
+  const int grid = std::min(p.m_tiles * p.n_tiles, max_ctas);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return BN == 128 ? launch<128>(ta, p, grid, st) : launch<256>(ta, p, grid, st);
+}
 
 extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                        const void* R, int ldr, int T, int N, int K, int epilogue, int max_ctas,

@@ -4,7 +4,8 @@ decode launch sequences over libb200hot.so.
 The five device launches per pass are the five kernel groups of the
 reference's layer API (`layer_kernels`, workload.py:162-210), in order:
 
-  qkv          rmsnorm + tcgen05 GEMM (+ RoPE / paged-KV write)
+  qkv          rmsnorm + tcgen05 GEMM (prefill: RoPE + paged-KV write fused
+               into the GEMM epilogue; decode: separate rope_kv_write)
   attn         causal GQA flash attention (prefill) | paged decode attention
   o_proj       tcgen05 GEMM with fused residual add
   mlp_up_gate  rmsnorm + tcgen05 GEMM with fused SiLU(gate) * up
@@ -202,10 +203,10 @@ class DeviceLayer:
 
         lib.rmsnorm(x, self.W.attn_norm, sc.xn[:T], EPS, sms, stream)
         mark("qkv", 0)
-        lib.gemm(sc.xn[:T], self.W.w_qkv, qkv, lib.EPI_STORE, max_ctas=sms, stream=stream)
+        # QKV GEMM with RoPE + the paged K/V write fused into its epilogue
+        lib.gemm_qkv_rope(sc.xn[:T], self.W.w_qkv, qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k,
+                          cache.v, cache.page, max_ctas=sms, stream=stream)
         mark("qkv", 1)
-        lib.rope_kv_write(qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k, cache.v, cache.page,
-                          max_ctas=sms, stream=stream)
         mark("attn", 0)
         lib.prefill_attn(qkv[:, : Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:],
                          sc.attn[:T], cu_seqlens, nseq, max_seqlen, Hq, Hkv, d, self.scale,
@@ -221,7 +222,7 @@ class DeviceLayer:
         mark("mlp_down", 0)
         lib.gemm(sc.act[:T], self.W.w_down, y, lib.EPI_RESID, resid=sc.h[:T], max_ctas=sms, stream=stream)
         mark("mlp_down", 1)
-        return 8
+        return 7
 
     # --------------------------------------------------------------- decode
     def decode(self, x, y, sc: DecodeScratch, ctx_lens, positions, slots, block_table,

@@ -35,6 +35,7 @@ SIGNATURES = {
     "hp_gemm": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
     "hp_gemm_traced": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "hp_gemm_tiles": (_i, [_i, _i]),
+    "hp_gemm_qkv_rope": (_i, [_p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_gemm_plan": (_i, [_i, _i, _i, C.POINTER(_i), C.POINTER(_i)]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
@@ -184,6 +185,14 @@ def prefill_attn(q, k, v, o, cu_seqlens, nseq: int, max_seqlen: int, Hq: int, Hk
     check(load().hp_prefill_attn(_ptr(q), q.stride(0), _ptr(k), k.stride(0), _ptr(v), v.stride(0),
                                  _ptr(o), o.stride(0), _ptr(cu_seqlens), nseq, q.shape[0], max_seqlen, Hq, Hkv,
                                  d, scale, max_ctas, _stream(stream)), "hp_prefill_attn")
+
+
+def gemm_qkv_rope(x, w, y, Hq: int, Hkv: int, d: int, positions, cos_sin, slots, kcache, vcache,
+                  page: int, max_ctas: int = 148, stream=None) -> None:
+    """Fused prefill QKV GEMM + RoPE + paged K/V write (hp_gemm_qkv_rope)."""
+    check(load().hp_gemm_qkv_rope(_ptr(x), x.stride(0), _ptr(w), x.shape[1], _ptr(y), y.stride(0), x.shape[0], Hq,
+                                  Hkv, d, x.shape[1], _ptr(positions), _ptr(cos_sin), _ptr(slots), _ptr(kcache),
+                                  _ptr(vcache), page, max_ctas, _stream(stream)), "hp_gemm_qkv_rope")
 
 
 def gemm_plan(T: int, N: int, max_ctas: int) -> tuple[int, int]:

@@ -130,10 +130,14 @@ class TPLayer:
         s, T = self.s, x.shape[0]
         d = s.head_dim
         lib.rmsnorm(x, self.attn_norm, self.xn[:T], EPS, sms, stream)
-        self._linear(self.xn[:T], self.w_qkv, self.qkv[:T], lib.EPI_STORE, None, sms, stream)
         q = self.qkv[:T]
-        lib.rope_kv_write(q, s.heads, s.kv_heads, d, positions, self.rope, slots, kcache, vcache, PAGE,
-                          max_ctas=sms, stream=stream)
+        if T > 256:  # fused GEMM + RoPE + paged K/V write
+            lib.gemm_qkv_rope(self.xn[:T], self.w_qkv, q, s.heads, s.kv_heads, d, positions, self.rope, slots,
+                              kcache, vcache, PAGE, max_ctas=sms, stream=stream)
+        else:
+            self._linear(self.xn[:T], self.w_qkv, q, lib.EPI_STORE, None, sms, stream)
+            lib.rope_kv_write(q, s.heads, s.kv_heads, d, positions, self.rope, slots, kcache, vcache, PAGE,
+                              max_ctas=sms, stream=stream)
         lib.prefill_attn(q[:, :s.heads * d], q[:, s.heads * d:(s.heads + s.kv_heads) * d],
                          q[:, (s.heads + s.kv_heads) * d:], self.attn[:T], cu_seqlens, nseq, max_seqlen,
                          s.heads, s.kv_heads, d, self.scale, max_ctas=sms, stream=stream)

@@ -377,3 +377,50 @@ def test_prefill_attn_paged_matches_dense_without_prefix(gen):
     lib.prefill_attn_paged(q, cache.k, cache.v, bt, cu, torch.zeros(1, dtype=torch.int32, device=DEV), 1, T,
                            o_paged, Hq, Hkv, d, page, 1 / math.sqrt(d), max_ctas=148)
     assert torch.equal(o_paged, o_dense)
+
+
+@pytest.mark.parametrize("T,Hq,Hkv,d", [(300, 32, 8, 128), (1024, 4, 2, 64), (77, 8, 2, 128)])
+def test_gemm_qkv_rope_fused_matches_fp32(T, Hq, Hkv, d, gen):
+    # hp_gemm_qkv_rope: QKV GEMM + RoPE + paged K/V write in one epilogue
+    from paper_2504_19516_b200.device.layer import KVCache, rope_table
+
+    K, page = 512, 64
+    N = (Hq + 2 * Hkv) * d
+    x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
+    pos = torch.randint(0, 4000, (T,), device=DEV, dtype=torch.int32, generator=gen)
+    nblk = -(-T // page) + 4
+    slots = torch.randperm(nblk * page, device=DEV, generator=gen)[:T].to(torch.int32)
+    table = torch.from_numpy(rope_table(4096, d)).to(DEV)
+    cache = KVCache(nblk, Hkv, d, DEV)
+    y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
+    lib.gemm_qkv_rope(x, lib.tile_weight(w), y, Hq, Hkv, d, pos, table, slots, cache.k, cache.v, page, max_ctas=148)
+    ref = (x.float() @ w.float().T).view(T, Hq + 2 * Hkv, d)
+    cs = table[pos.long()]
+    cos, sin = cs[:, None, : d // 2], cs[:, None, d // 2:]
+    a, b = ref[:, : Hq + Hkv, : d // 2], ref[:, : Hq + Hkv, d // 2:]
+    rot = torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
+    ref = torch.cat([rot, ref[:, Hq + Hkv:]], dim=1)
+    assert rel_err(y.view(T, -1, d), ref) < 1e-2
+    kl, vl = lib.kv_unpack(cache.k).float(), lib.kv_unpack(cache.v).float()
+    blk, off = (slots // page).long(), (slots % page).long()
+    assert rel_err(kl[blk, :, off], ref[:, Hq:Hq + Hkv]) < 1e-2
+    assert rel_err(vl[blk, :, off], ref[:, Hq + Hkv:]) < 1e-2
+    assert torch.equal(kl[blk, :, off].to(torch.bfloat16), y.view(T, -1, d)[:, Hq:Hq + Hkv])
+
+
+def test_gemm_qkv_rope_bit_identical_to_unfused_path(gen):
+    from paper_2504_19516_b200.device.layer import KVCache, rope_table
+
+    T, Hq, Hkv, d, K, page = 513, 32, 8, 128, 1024, 64
+    N = (Hq + 2 * Hkv) * d
+    x, w = bf((T, K), gen=gen), lib.tile_weight(bf((N, K), 0.05, gen))
+    pos = torch.arange(T, device=DEV, dtype=torch.int32) + 7
+    slots = torch.arange(T, device=DEV, dtype=torch.int32) + 64
+    table = torch.from_numpy(rope_table(2048, d)).to(DEV)
+    c1, c2 = KVCache(-(-T // page) + 2, Hkv, d, DEV), KVCache(-(-T // page) + 2, Hkv, d, DEV)
+    y1, y2 = (torch.empty(T, N, device=DEV, dtype=torch.bfloat16) for _ in range(2))
+    lib.gemm_qkv_rope(x, w, y1, Hq, Hkv, d, pos, table, slots, c1.k, c1.v, page, max_ctas=148)
+    lib.gemm(x, w, y2, lib.EPI_STORE, max_ctas=148)
+    lib.rope_kv_write(y2, Hq, Hkv, d, pos, table, slots, c2.k, c2.v, page, max_ctas=148)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(c1.k, c2.k) and torch.equal(c1.v, c2.v)
