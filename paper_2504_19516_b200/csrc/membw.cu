@@ -236,21 +236,43 @@ __global__ void __launch_bounds__(128) k_umma_rate(int n, int chains, long long*
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // converged warp: descriptors are built by all lanes (uniform
+    // registers), the unrolled group of 4 MMAs is issued by one elected lane
+    // with compile-time descriptor offsets.  chains < 0: TS form, A from
+    // TMEM columns [256, 256 + 32) (M=128 x K=16 bf16 per MMA).
     constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
-    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 16384);
+    const int ch = chains < 0 ? -chains : chains;
+    const uint64_t ad = umma_desc_sw128(smem_u32(smem)), bd = umma_desc_sw128(smem_u32(smem + 16384));
     const long long t0 = clock64();
-    for (int i = 0; i < n; ++i) {
-      const int k = i & 3;
-      umma_bf16(tmem + (i % chains) * BN, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                i >= chains ? 1u : 0u);
+    for (int i = 0; i < n; i += 4) {
+      const uint32_t d = tmem + ((i / 4) % ch) * BN;
+      const uint32_t acc = i >= 4 * ch ? 1u : 0u;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (chains < 0)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+                "r"(tmem + 256 + 8 * k), "l"(bd + 2 * k), "r"(idesc), "r"(acc | (k > 0 ? 1u : 0u))
+                : "memory");
+          else
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, acc | (k > 0 ? 1u : 0u));
+        }
+      }
+      __syncwarp();
     }
+    __syncwarp();
     const long long t1 = clock64();
-    umma_commit(&bar);
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
     mbar_wait(&bar, 0);
     const long long t2 = clock64();
-    out[blockIdx.x * 2] = t1 - t0;
-    out[blockIdx.x * 2 + 1] = t2 - t0;
+    if (lane_id() == 0) {
+      out[blockIdx.x * 2] = t1 - t0;
+      out[blockIdx.x * 2 + 1] = t2 - t0;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -265,12 +287,16 @@ __global__ void __launch_bounds__(128) k_umma_rate(int n, int chains, long long*
 using namespace hp;
 
 extern "C" int hp_umma_rate(int n, int bn, int chains, int ctas, long long* out, void* stream) {
-  HP_CHECK_ARG(out && n >= 1 && chains >= 1 && chains * bn <= 512 && ctas >= 1, "hp_umma_rate: bad args");
+  HP_CHECK_ARG(out && n >= 4 && chains != 0 && (chains < 0 ? -chains : chains) * bn <= 256 && ctas >= 1,
+               "hp_umma_rate: bad args");
   const size_t smem = 1024 + 16384 + 32768;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (bn == 32) {
     HP_CUDA_TRY(cudaFuncSetAttribute(k_umma_rate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_umma_rate<32><<<ctas, 128, smem, st>>>(n, chains, out);
+  } else if (bn == 64) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma_rate<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma_rate<64><<<ctas, 128, smem, st>>>(n, chains, out);
   } else if (bn == 128) {
     HP_CUDA_TRY(cudaFuncSetAttribute(k_umma_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_umma_rate<128><<<ctas, 128, smem, st>>>(n, chains, out);
