@@ -5,7 +5,8 @@
     python -m paper_2504_19516_b200.device.calibrate --out calib/
 
 Writes
-  gpu.json           B200 GpuSpec: N, measured bf16 and HBM peaks, fitted n_d
+  gpu.json           B200 GpuSpec: N, measured bf16 and HBM peaks, fitted n_d,
+                     measured green-context repartition latency (reconfig_s)
   bandwidth.json     HBM GB/s vs SM count (green-context partitions) -- the
                      Fig. 6a curve behind D_p = D min(1, p / n_d)
   calibration.jsonl  alpha samples (prefill / decode, measured / SRM) and the
@@ -28,7 +29,7 @@ from ..perf_model import srm_decode_step_s, srm_prefill_layer_s
 from ..workload import MODEL_PRESETS
 from . import lib
 from .executor import B200Executor
-from .partition import DECODE, PartitionPool
+from .partition import DECODE, PREFILL, PartitionPool
 
 ROOT = Path(__file__).resolve().parents[2]
 
@@ -51,6 +52,48 @@ def bandwidth_curve(pool: PartitionPool, grid, nbytes: int = 1 << 30, reps: int 
                 best = max(best, nbytes / (a.elapsed_time(b) * 1e-3))
         rows.append((st.sms, best))
     return rows
+
+
+def reconfig_latency(pool: PartitionPool, dm_a: int = 32, dm_b: int = 48, reps: int = 20) -> dict:
+    """The reference's `reconfig_s` (engine.py:132; Table 6: 4.1
+    us) on B200 green contexts: the gap between the end of a kernel on one
+    decode partition and the start of the next kernel, measured with
+    %globaltimer stamps, for (a) the next launch on the same stream, (b) on
+    another stream of the same green context after an event, (c) on a
+    different green-context partition after an event -- a repartition.
+    reconfig_s = median(c) - median(a)."""
+    import statistics
+
+    a_st = pool.phase(DECODE, dm_a)
+    b_st = pool.phase(DECODE, dm_b)
+    same_ctx_other = pool.phase(PREFILL, pool.n - dm_a)  # the pair's other stream (same split)
+    t1 = torch.zeros(a_st.sms, 3, dtype=torch.int64, device="cuda")
+    t2 = torch.zeros(max(a_st.sms, b_st.sms), 3, dtype=torch.int64, device="cuda")
+
+    def gap(first, second, cross: bool) -> float:
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(first.torch_stream):
+            torch.cuda._sleep(400_000)  # both launches queued before the first runs
+            lib.probe(t1, first.sms, spin_ns=5000, stream=first.torch_stream)
+            ev.record(first.torch_stream)
+        st = second.torch_stream if cross else first.torch_stream
+        with torch.cuda.stream(st):
+            if cross:
+                st.wait_event(ev)
+            lib.probe(t2[:second.sms], second.sms, spin_ns=5000, stream=st)
+        torch.cuda.synchronize()
+        end_a = int(t1[:, 2].max())
+        start_b = int(t2[:second.sms, 1].min())
+        return (start_b - end_a) * 1e-9
+
+    res = {}
+    for name, (f, sec, cross) in {"same_stream": (a_st, a_st, False),
+                                  "other_stream_same_split": (a_st, same_ctx_other, True),
+                                  "other_partition": (a_st, b_st, True)}.items():
+        gaps = [gap(f, sec, cross) for _ in range(reps)]
+        res[name + "_us"] = 1e6 * statistics.median(gaps)
+    res["reconfig_s"] = max(0.0, (res["other_partition_us"] - res["same_stream_us"]) * 1e-6)
+    return res
 
 
 def fit_n_d(curve, d_peak: float) -> int:
@@ -80,8 +123,10 @@ def main(argv=None) -> int:
     d_peak = max(bw for _, bw in curve)
     n_d = fit_n_d(curve, d_peak)
     gpu = b200_spec(c_peak=peaks.get("bf16_tflops", 1607.5) * 1e12, d_peak=d_peak, n_d=n_d, num_sms=N)
-    (out / "gpu.json").write_text(json.dumps({k: getattr(gpu, k) for k in
-                                              ("name", "num_sms", "c_peak", "d_peak", "w_peak", "n_d", "n_w")},
+    rc = reconfig_latency(pool)
+    (out / "gpu.json").write_text(json.dumps({**{k: getattr(gpu, k) for k in
+                                                ("name", "num_sms", "c_peak", "d_peak", "w_peak", "n_d", "n_w")},
+                                             "reconfig_s": rc["reconfig_s"], "reconfig_gaps_us": rc},
                                              indent=2) + "\n")
     (out / "bandwidth.json").write_text(json.dumps({"sms_vs_bytes_per_s": curve, "n_d_fit": n_d}, indent=2) + "\n")
 

@@ -52,10 +52,13 @@ def shard(trace, rank: int, world: int):
 
 def run_policy(policy: str, trace, ex, gpu, chunk: int = 1024):
     model = MODEL_PRESETS["llama3-8b"]
+    g = CALIB / "gpu.json"
+    reconfig = json.loads(g.read_text()).get("reconfig_s") if g.exists() else None
     cfg = E.SimConfig(gpu=gpu, model=model,
                       slo=S.SloSpec(norm_ttft_s_per_token=1.5e-3, tpot_s=0.1),
                       sched=S.SchedulerConfig(sm_step=8),
-                      policy=E.PolicySpec(policy, chunk_size=chunk), seed=0)
+                      policy=E.PolicySpec(policy, chunk_size=chunk), seed=0,
+                      **({"reconfig_s": reconfig} if reconfig is not None else {}))
     store = CalibrationStore.load_jsonl(CALIB / "calibration.jsonl") if (CALIB / "calibration.jsonl").exists() else None
     rep = E.run(cfg, trace, oracle=ex, store=store)
     a = dict(rep.aggregates)
