@@ -385,3 +385,66 @@ def run_tiny_chunked(seed: int = 0, chunk_budget: int = 512, decode_steps: int =
     stats["max_excess"] = max(stats["excess"])
     del stats["excess"]
     return stats
+
+
+def run_llama_hybrid(seed: int = 5, device: int = 0) -> dict:
+    """One Llama-3-8B layer over a hybrid batch at full width: two prompt
+    chunks with cached prefixes (priors 0 and 700) plus 5 decode rows, device
+    (DeviceLayer.hybrid: GEMMs over the concatenated rows, paged prefill
+    attention, paged decode attention) vs oracle `layer_hybrid`."""
+    import torch
+
+    from paper_2504_19516_b200.device import lib
+    from paper_2504_19516_b200.device.layer import (DecodeScratch, DeviceLayer, KVCache, LayerWeights,
+                                                    PrefillScratch)
+    from paper_2504_19516_b200.workload import MODEL_PRESETS
+
+    m = MODEL_PRESETS["llama3-8b"]
+    rng = np.random.default_rng(seed)
+    h, I, d, Hq, Hkv = m.hidden, m.intermediate, m.head_dim, m.num_heads, m.num_kv_heads
+    W = O.LayerWeights(_bf(rng.normal(0, 0.02, (m.qkv_out_dim, h))), _bf(rng.normal(0, 0.02, (h, h))),
+                       _bf(rng.normal(0, 0.02, (I, h))), _bf(rng.normal(0, 0.02, (I, h))),
+                       _bf(rng.normal(0, 0.02, (h, I))), _bf(1 + 0.1 * rng.normal(size=h)),
+                       _bf(1 + 0.1 * rng.normal(size=h)))
+    dev = torch.device("cuda", device)
+    seqs = [(200, 0), (130, 700)] + [(1, c - 1) for c in (65, 300, 1000, 64, 129)]
+    nseq = len(seqs)
+    pages = [-(-(n + p) // PAGE) for n, p in seqs]
+    nblk = sum(pages) + 3
+    perm = rng.permutation(nblk)
+    bt = np.zeros((nseq, max(pages)), np.int32)
+    k = 0
+    for i, pg in enumerate(pages):
+        bt[i, :pg] = perm[k:k + pg]
+        k += pg
+    # cached prefixes: random K/V (bf16 values) in every page, identical on both sides
+    kc = _bf(rng.normal(size=(nblk, Hkv, PAGE, d)))
+    vc = _bf(rng.normal(size=(nblk, Hkv, PAGE, d)))
+    T = sum(n for n, _ in seqs)
+    x = _bf(rng.normal(size=(T, h)))
+    table = O.rope_table(2048, d)
+
+    def t(a, dt=torch.bfloat16):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(dev)
+
+    lyr = DeviceLayer(m, LayerWeights.from_numpy(dev, W.w_qkv, W.w_o, W.w_gate, W.w_up, W.w_down, W.attn_norm,
+                                                 W.mlp_norm), dev, max_pos=2048)
+    cache = KVCache(nblk, Hkv, d, dev)
+    cache.k.copy_(lib.kv_pack(t(kc)))
+    cache.v.copy_(lib.kv_pack(t(vc)))
+    nc = 2
+    Tc = seqs[0][0] + seqs[1][0]
+    pos = np.concatenate([np.arange(p, p + n) for n, p in seqs]).astype(np.int32)
+    slots = np.concatenate([bt[i, np.arange(p, p + n) // PAGE] * PAGE + np.arange(p, p + n) % PAGE
+                            for i, (n, p) in enumerate(seqs)]).astype(np.int32)
+    y = torch.empty(T, h, dtype=torch.bfloat16, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    lyr.hybrid(t(x), y, PrefillScratch(m, T, dev), DecodeScratch(m, nseq - nc, max(pages), dev), Tc,
+               t(np.array([0, seqs[0][0], Tc]), torch.int32), nc, max(seqs[0][0], seqs[1][0]),
+               t(np.array([0, 700]), torch.int32), t(bt[:nc], torch.int32),
+               t(np.array([p + 1 for _, p in seqs[nc:]]), torch.int32), t(bt[nc:], torch.int32),
+               t(pos, torch.int32), t(slots, torch.int32), cache, sms)
+    ref = O.layer_hybrid(x, W, Hq, Hkv, d, seqs, table, kc, vc, bt, bf16_boundaries=True)
+    dy = y.float().cpu().numpy()
+    return {"max_abs": float(np.max(np.abs(dy - ref))), "excess": excess(dy, ref),
+            "chunk_excess": excess(dy[:Tc], ref[:Tc]), "decode_excess": excess(dy[Tc:], ref[Tc:])}

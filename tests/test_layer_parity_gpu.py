@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from parity_harness import ATOL, run_llama_layer, run_tiny, run_tiny_chunked  # noqa: E402
+from parity_harness import ATOL, run_llama_hybrid, run_llama_layer, run_tiny, run_tiny_chunked  # noqa: E402
 
 
 def test_tiny_model_config1_prefill_and_greedy_decode():
@@ -49,3 +49,8 @@ def test_tiny_model_chunked_prefill_hybrid_batches(budget):
     assert r["mismatches"] == 0, r
     assert r["chunks_with_prefix"] >= 2 and r["max_chunks_per_iter"] >= 2, r
     assert r["tie_flips"] <= 2, r
+
+
+def test_llama3_8b_layer_hybrid_batch_with_cached_prefixes():
+    r = run_llama_hybrid()
+    assert r["excess"] <= ATOL, r
