@@ -13,7 +13,7 @@ cache of context C).  It can execute, on the B200:
                              alternating (temporal sharing).
 
 Decode steps are captured once per partition into a CUDA graph (one launch
-per layer-step instead of nine).  All times come from CUDA events recorded
+per layer-step instead of nine or ten).  All times come from CUDA events recorded
 on the launching streams.
 """
 

@@ -8,6 +8,8 @@ Implements the `GroundTruthOracle` protocol (reference engine.py:159-208):
   decode_step_s(es)     one decode step (all model layers) for
                         es.decode_ctx_lens on es.decode_sms SMs, with the
                         prefill side of `es` running concurrently
+  hybrid_iteration_s(chunks, decode_ctx_lens, sms)
+                        one lockstep hybrid batch (chunked-prefill baseline)
   alpha(phase, sms, tokens)        measured / SRM at a canonical shape
   contention_bw(sms, prefill_len)  HBM bandwidth of `sms` SMs next to a
                                    prefill on the remaining SMs
@@ -17,10 +19,12 @@ reference's event loop with CUDA-event measurements of the real kernels
 confined to green-context partitions (PartitionPool) instead of the
 synthetic surfaces.  Decisions, queueing and reports stay the reference's.
 
-Every layer of a decode step has identical cost, so a step is measured as
-one decode layer (queued ahead of the timer, so host launch latency is
-excluded) times `model.num_layers`; the prefill side likewise measures one
-layer.  The kernels run on a resident random-init layer; K/V for arbitrary
+By default every layer of a decode step has identical cost, so a step is
+measured as one decode layer (queued ahead of the timer, so host launch
+latency is excluded) times `model.num_layers`, and a prefill layer as one
+resident layer.  With `full_model=True` every layer is resident (distinct
+random weights, per-layer KV pools): a decode step is measured over all
+layers and a prefill step over `l_step` distinct layers.  K/V for arbitrary
 decode batches come from a page pool addressed modulo its size (the bytes
 streamed are what the timing depends on).
 """
