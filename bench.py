@@ -328,12 +328,12 @@ def main(argv=None) -> int:
     from paper_2504_19516_b200.perf_model import wave_stats
 
     wl = cr.layer.W
-    units = {"qkv": hplib.gemm_plan(T, wl.w_qkv.shape[0], pm)[1], "o_proj": hplib.gemm_plan(T, wl.w_o.shape[0], pm)[1],
-             "mlp_up_gate": hplib.gemm_plan(T, wl.w_ug.shape[0], pm)[1],
-             "mlp_down": hplib.gemm_plan(T, wl.w_down.shape[0], pm)[1],
-             "attn": min(-(-T // 128) * model.num_heads, pm)}
+    plans = {g: hplib.gemm_plan(T, w.shape[0], pm) for g, w in
+             (("qkv", wl.w_qkv), ("o_proj", wl.w_o), ("mlp_up_gate", wl.w_ug), ("mlp_down", wl.w_down))}
+    units = {g: (pl[1], pm // pl[2]) for g, pl in plans.items()}  # (tiles, concurrent tile slots)
+    units["attn"] = (-(-T // 256) * model.num_heads, pm)          # k_fa2: 256-query units, one per CTA
     g_s = res.group_s
-    wave_idle = sum(g_s[g] * wave_stats(units[g], 1, pm).idle_ratio for g in units) / sum(g_s.values())
+    wave_idle = sum(g_s[g] * wave_stats(u, 1, n).idle_ratio for g, (u, n) in units.items()) / sum(g_s.values())
 
     # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
     dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}

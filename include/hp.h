@@ -108,10 +108,12 @@ int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, void* Y, int 
 /* Output tiles (persistent-grid work units) of hp_gemm for T tokens, N
  * features at the 256-wide tile. */
 int hp_gemm_tiles(int T, int N);
-/* The tile width hp_gemm picks for a `max_ctas`-SM partition (128 or 256:
- * fewer wave-quantised column-rounds, wave_stats perf_model.py:157-169) and
- * the resulting tile count. */
-int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles);
+/* The tiling hp_gemm picks for a `max_ctas`-SM partition: tile width (128
+ * or 256: fewer wave-quantised column-rounds, wave_stats perf_model.py:
+ * 157-169), tile count, and CTAs per tile (2 = CTA-pair 256 x 256 tiles on
+ * tcgen05.mma.cta_group::2; the persistent grid then has max_ctas / 2 units
+ * of work-in-flight, i.e. waves = wave_stats(tiles, 1, max_ctas / 2)). */
+int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles, int* ctas_per_tile);
 
 /* Swap-AB stream-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
  * hp_gemm; W streams through UMMA-M and the (tile, k-block) space is split
@@ -194,6 +196,9 @@ int hp_membw_pipe(const void* src, size_t bytes, int ctas, int chunk_kb, int pro
 /* tcgen05.mma issue/completion rate: n MMAs (M=128, N=bn, K=16, smem
  * operands) over `chains` accumulators; out[cta] = {issue cycles, done cycles}. */
 int hp_umma_rate(int n, int bn, int chains, int ctas, long long* out, void* stream);
+/* Pair MMA rate: `pairs` 2-CTA clusters issue n tcgen05.mma.cta_group::2
+ * (M=256, N=bn, K=16); out[cta] = issue cycles, out[grid + cta] = done cycles. */
+int hp_umma2_rate(int n, int bn, int pairs, long long* out, void* stream);
 
 /* Per-CTA probe: out[i] = {smid, start_ns, end_ns} for `ctas` CTAs spinning
  * `spin_ns` each -- partition confinement (%smid) and measured idle. */

@@ -107,6 +107,106 @@ __device__ __forceinline__ void add_row32(float* v, const __nv_bfloat16* src) {
   }
 }
 
+// Epilogue of one output tile for the thread owning accumulator row `gm`
+// (TMEM address `taddr` = its lane, column 0 of the tile's accumulator).
+template <int BN>
+__device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr, int gm, int nt) {
+  const bool ok = gm < p.Ma;
+  if (p.epi == EPI_ROPE) {
+    // the tile's BN columns are BN/hd whole heads of the q | k | v blocks
+    const int half = p.hd / 2;
+    const int pos = ok ? p.pos[gm] : 0;
+    const float* cs = p.cos_sin + size_t(pos) * p.hd;
+    int blk = 0, off = 0;
+    if (ok) {
+      const int sl = p.slots[gm];
+      blk = sl / p.page;
+      off = sl % p.page;
+    }
+#pragma unroll 1
+    for (int hh = 0; hh < BN / p.hd; ++hh) {
+      const int head = (nt * BN) / p.hd + hh;
+      const bool rot = head < p.Hq + p.Hkv;
+#pragma unroll 1
+      for (int c = 0; c < half / 32; ++c) {
+        float x[32], y[32];
+        tmem_ld32(taddr + hh * p.hd + c * 32, x);
+        tmem_ld32(taddr + hh * p.hd + half + c * 32, y);
+        tmem_ld_wait();
+        if (!ok) continue;
+        if (rot) {  // y[i] = x cos - x' sin, y' = x' cos + x sin (rotate_half)
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 co = *reinterpret_cast<const float4*>(cs + c * 32 + j);
+            const float4 si = *reinterpret_cast<const float4*>(cs + half + c * 32 + j);
+            const float cc[4] = {co.x, co.y, co.z, co.w}, ss[4] = {si.x, si.y, si.z, si.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              // rotate the bf16-rounded projection, exactly as the
+              // unfused GEMM store + hp_rope_kv_write pair does
+              const float a = __bfloat162float(__float2bfloat16(x[j + k]));
+              const float b = __bfloat162float(__float2bfloat16(y[j + k]));
+              x[j + k] = a * cc[k] - b * ss[k];
+              y[j + k] = b * cc[k] + a * ss[k];
+            }
+          }
+        }
+        __nv_bfloat16* dst = p.out + size_t(gm) * p.ldo + size_t(head) * p.hd;
+        store_row32(dst + c * 32, x);
+        store_row32(dst + half + c * 32, y);
+        if (head >= p.Hq) {  // k or v head -> paged cache page [page/64][hd/64][64][64], swizzled
+          const int kvh = rot ? head - p.Hq : head - p.Hq - p.Hkv;
+          __nv_bfloat16* cache = rot ? p.kc : p.vc;
+          const size_t base = ((size_t(blk) * p.Hkv + kvh) * (p.page / 64) + off / 64) * (p.hd / 64);
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const float* v = part ? y : x;
+            const int j0 = (part ? half : 0) + c * 32;  // first head dim of these 32
+#pragma unroll
+            for (int q8 = 0; q8 < 4; ++q8) {
+              const int j = j0 + q8 * 8;
+              uint4 w;
+              w.x = pack_bf16(v[q8 * 8 + 0], v[q8 * 8 + 1]);
+              w.y = pack_bf16(v[q8 * 8 + 2], v[q8 * 8 + 3]);
+              w.z = pack_bf16(v[q8 * 8 + 4], v[q8 * 8 + 5]);
+              w.w = pack_bf16(v[q8 * 8 + 6], v[q8 * 8 + 7]);
+              const size_t e = (base + j / 64) * 4096 + size_t(off & 63) * 64 +
+                               ((((j & 63) >> 3) ^ (off & 7)) << 3);
+              *reinterpret_cast<uint4*>(cache + e) = w;
+            }
+          }
+        }
+      }
+    }
+  } else if (p.epi == EPI_SILU) {
+#pragma unroll 1
+    for (int h = 0; h < BN / 128; ++h) {
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        float g[32], v[32];
+        tmem_ld32(taddr + h * 128 + c * 32, g);
+        tmem_ld32(taddr + h * 128 + 64 + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = silu(g[j]) * v[j];
+        if (ok) store_row32(p.out + size_t(gm) * p.ldo + nt * (BN / 2) + h * 64 + c * 32, v);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      tmem_ld32(taddr + c * 32, v);
+      tmem_ld_wait();
+      const int col = nt * BN + c * 32;
+      if (ok) {
+        if (p.epi == EPI_RESID) add_row32(v, p.resid + size_t(gm) * p.ldr + col);
+        store_row32(p.out + size_t(gm) * p.ldo + col, v);
+      }
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const GemmParams p) {
@@ -229,101 +329,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       {
-        const int gm = mt * BM + row;
-        const bool ok = gm < p.Ma;
-        if (p.epi == EPI_ROPE) {
-          // the tile's BN columns are BN/hd whole heads of the q | k | v blocks
-          const int half = p.hd / 2;
-          const int pos = ok ? p.pos[gm] : 0;
-          const float* cs = p.cos_sin + size_t(pos) * p.hd;
-          int blk = 0, off = 0;
-          if (ok) {
-            const int sl = p.slots[gm];
-            blk = sl / p.page;
-            off = sl % p.page;
-          }
-#pragma unroll 1
-          for (int hh = 0; hh < BN / p.hd; ++hh) {
-            const int head = (nt * BN) / p.hd + hh;
-            const bool rot = head < p.Hq + p.Hkv;
-#pragma unroll 1
-            for (int c = 0; c < half / 32; ++c) {
-              float x[32], y[32];
-              tmem_ld32(taddr + hh * p.hd + c * 32, x);
-              tmem_ld32(taddr + hh * p.hd + half + c * 32, y);
-              tmem_ld_wait();
-              if (!ok) continue;
-              if (rot) {  // y[i] = x cos - x' sin, y' = x' cos + x sin (rotate_half)
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                  const float4 co = *reinterpret_cast<const float4*>(cs + c * 32 + j);
-                  const float4 si = *reinterpret_cast<const float4*>(cs + half + c * 32 + j);
-                  const float cc[4] = {co.x, co.y, co.z, co.w}, ss[4] = {si.x, si.y, si.z, si.w};
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) {
-                    // rotate the bf16-rounded projection, exactly as the
-                    // unfused GEMM store + hp_rope_kv_write pair does
-                    const float a = __bfloat162float(__float2bfloat16(x[j + k]));
-                    const float b = __bfloat162float(__float2bfloat16(y[j + k]));
-                    x[j + k] = a * cc[k] - b * ss[k];
-                    y[j + k] = b * cc[k] + a * ss[k];
-                  }
-                }
-              }
-              __nv_bfloat16* dst = p.out + size_t(gm) * p.ldo + size_t(head) * p.hd;
-              store_row32(dst + c * 32, x);
-              store_row32(dst + half + c * 32, y);
-              if (head >= p.Hq) {  // k or v head -> paged cache page [page/64][hd/64][64][64], swizzled
-                const int kvh = rot ? head - p.Hq : head - p.Hq - p.Hkv;
-                __nv_bfloat16* cache = rot ? p.kc : p.vc;
-                const size_t base = ((size_t(blk) * p.Hkv + kvh) * (p.page / 64) + off / 64) * (p.hd / 64);
-#pragma unroll
-                for (int part = 0; part < 2; ++part) {
-                  const float* v = part ? y : x;
-                  const int j0 = (part ? half : 0) + c * 32;  // first head dim of these 32
-#pragma unroll
-                  for (int q8 = 0; q8 < 4; ++q8) {
-                    const int j = j0 + q8 * 8;
-                    uint4 w;
-                    w.x = pack_bf16(v[q8 * 8 + 0], v[q8 * 8 + 1]);
-                    w.y = pack_bf16(v[q8 * 8 + 2], v[q8 * 8 + 3]);
-                    w.z = pack_bf16(v[q8 * 8 + 4], v[q8 * 8 + 5]);
-                    w.w = pack_bf16(v[q8 * 8 + 6], v[q8 * 8 + 7]);
-                    const size_t e = (base + j / 64) * 4096 + size_t(off & 63) * 64 +
-                                     ((((j & 63) >> 3) ^ (off & 7)) << 3);
-                    *reinterpret_cast<uint4*>(cache + e) = w;
-                  }
-                }
-              }
-            }
-          }
-        } else if (p.epi == EPI_SILU) {
-#pragma unroll 1
-          for (int h = 0; h < BN / 128; ++h) {
-#pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-              float g[32], v[32];
-              tmem_ld32(taddr + h * 128 + c * 32, g);
-              tmem_ld32(taddr + h * 128 + 64 + c * 32, v);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = silu(g[j]) * v[j];
-              if (ok) store_row32(p.out + size_t(gm) * p.ldo + nt * (BN / 2) + h * 64 + c * 32, v);
-            }
-          }
-        } else {
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            float v[32];
-            tmem_ld32(taddr + c * 32, v);
-            tmem_ld_wait();
-            const int col = nt * BN + c * 32;
-            if (ok) {
-              if (p.epi == EPI_RESID) add_row32(v, p.resid + size_t(gm) * p.ldr + col);
-              store_row32(p.out + size_t(gm) * p.ldo + col, v);
-            }
-          }
-        }
+        epilogue_row<BN>(p, taddr, mt * BM + row, nt);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -343,6 +349,181 @@ __global__ void __launch_bounds__(192, 1)
     p.cta_times[blockIdx.x * 3 + 1] = *t_start;
     p.cta_times[blockIdx.x * 3 + 2] = globaltimer();
   }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair GEMM: a 2-CTA cluster owns a 256 x 256 output tile; the leader
+// issues tcgen05.mma.cta_group::2 (M = 256) reading each CTA's 128 activation
+// rows and 128 weight rows from that CTA's own smem.  A pair MMA runs at the
+// full 4096 MAC/clk/SM where the 1-CTA SS M=128 N=256 form reaches 76 %
+// (profiles/r01_umma_rates.md).  Per stage each CTA stages 16 KB of A and
+// 16 KB of B, so 6 stages fit.
+//   warp 0       producer (own CTA's halves), signals its own `full`
+//   warp 1       leader: TMEM alloc + MMA issue; peer: TMEM alloc + forwards
+//                its `full` completions to the leader's `full` (count 2)
+//   warps 2-5    epilogue of the CTA's 128 rows; arrive on the leader's
+//                `tempty` (count 8: both CTAs' epilogue warps)
+constexpr int PAIR_BN = 256;
+struct GemmPairCfg {
+  static constexpr uint32_t A_BYTES = BM * BK * 2;               // 16 KB: this CTA's 128 rows
+  static constexpr uint32_t B_BYTES = (PAIR_BN / 2) * BK * 2;    // 16 KB: this CTA's 128 weight rows
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr uint32_t TMEM_COLS = 2 * PAIR_BN;
+  static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    k_gemm_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                const GemmParams p) {
+  using C = GemmPairCfg;
+  constexpr int STAGES = C::STAGES;
+  constexpr int BN = PAIR_BN;
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* t_start = reinterpret_cast<uint64_t*>(tmem_slot + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);  // leader: its producer's expect_tx for both CTAs' bytes
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // used on the leader: 4 epilogue warps per CTA
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  pdl_wait();  // activations / residual from the stream predecessor
+  if (threadIdx.x == 0) *t_start = globaltimer();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = p.m_tiles * p.n_tiles;
+
+  if (warp == 0) {
+    // both CTAs' loads complete on the LEADER's `full` (pair TMA); the
+    // leader's producer posts the expected bytes of both halves
+    uint32_t g = 0;
+    const uint32_t lfull = mapa_shared(full, 0);
+    for (int tile = pair; tile < total; tile += npairs) {
+      int mt, nt;
+      tile_coords(p, tile, mt, nt);
+      for (int kb = 0; kb < p.num_kb; ++kb, ++g) {
+        const int stage = g % STAGES;
+        const uint32_t phase = (g / STAGES) & 1;
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          const uint32_t bar = lfull + 8u * stage;
+          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, mt * 2 * BM + int(rank) * BM);
+          // weight rows of this CTA's half: one pre-swizzled [128][64] sub-tile
+          // of the tiled layout, addressed as rows of a [*, 64] tensor
+          const int wrow = int(wtile_offset(nt * BN + int(rank) * (BN / 2), kb, p.K) / 128);
+          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmW, bar, 0, wrow);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1 && !leader) {
+    // peer: nothing to issue (the leader drives the pair's tensor core)
+  } else if (warp == 1) {
+    // leader: MMA issue for the pair (converged walk, one elected lane)
+    constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+    const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
+    const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sB));
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < total; tile += npairs) {
+      mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = adesc0 + uint64_t((stage * C::A_BYTES) >> 4);
+        const uint64_t bd = bdesc0 + uint64_t((stage * C::B_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit_pair(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (elect_one()) umma_commit_pair(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t ltempty = mapa_shared(tempty, 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < total; tile += npairs) {
+      int mt, nt;
+      tile_coords(p, tile, mt, nt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      epilogue_row<BN>(p, taddr, mt * 2 * BM + int(rank) * BM + row, nt);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(ltempty + 8u * acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  }
+  if (p.cta_times != nullptr && threadIdx.x == 0) {
+    p.cta_times[blockIdx.x * 3 + 0] = smid();
+    p.cta_times[blockIdx.x * 3 + 1] = *t_start;
+    p.cta_times[blockIdx.x * 3 + 2] = globaltimer();
+  }
+}
+
+static int launch_pair(const CUtensorMap& ta, const GemmParams& p, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(GemmPairCfg::SMEM)));
+    attr_set = true;
+  }
+  // the tiled weights viewed as a [N*K/64, 64] bf16 tensor: one 128-row box is
+  // one pre-swizzled [128][64] sub-tile, copied verbatim (no TMA swizzle)
+  CUtensorMap tw;
+  int rc = cached_tmap_bf16(&tw, p.w, uint64_t(p.Nb) * p.K / 64, 64, 64, 128, 64, false);
+  if (rc) return rc;
+  HP_LAUNCH_PDL("k_gemm_pair", k_gemm_pair, dim3(grid), dim3(192), GemmPairCfg::SMEM, st, ta, tw, p);
+  return HP_OK;
 }
 
 template <int BN>
@@ -368,6 +549,42 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
                               const void* R, int ldr, int T, int N, int K, int epilogue, int max_ctas,
                               uint64_t* cta_times, void* stream);
 
+// Pair mode (CTA-pair 256 x 256 tiles) unless HP_GEMM_PAIR=0, the tile
+// width is 128, or the partition has a single SM.
+static bool use_pair(int BN, int max_ctas) {
+  static const bool on = [] {
+    const char* e = std::getenv("HP_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on && BN == PAIR_BN && max_ctas >= 2;
+}
+
+// Fill the tile geometry of `p` (T x N output, K reduction) and launch the
+// 1-CTA kernel or the CTA-pair kernel on at most `max_ctas` SMs.
+static int plan_and_launch(const CUtensorMap& ta, GemmParams& p, int T, int N, int K, int BN, int max_ctas,
+                           cudaStream_t st) {
+  const bool pair = use_pair(BN, max_ctas);
+  const int rows = pair ? 2 * BM : BM;
+  p.Ma = T;
+  p.Nb = N;
+  p.K = K;
+  p.m_tiles = ceil_div(T, rows);
+  p.n_tiles = N / BN;
+  p.k_splits = 1;
+  p.num_kb = K / BK;
+  p.kb_per_split = p.num_kb;
+  // rasterization group: keep the activation block of a group within ~32 MB
+  // of the 126 MB L2 (decode traffic shares it during co-execution)
+  const long a_tile_bytes = long(rows) * K * 2;
+  const long budget = 32l << 20;
+  p.group_m = a_tile_bytes * p.m_tiles <= 2 * budget ? p.m_tiles
+                                                     : int(std::max<long>(pair ? 4 : 8, budget / a_tile_bytes));
+  const int units = p.m_tiles * p.n_tiles;
+  if (pair) return launch_pair(ta, p, 2 * std::min(units, max_ctas / 2), st);
+  const int grid = std::min(units, max_ctas);
+  return BN == 128 ? launch<128>(ta, p, grid, st) : launch<256>(ta, p, grid, st);
+}
+
 static int gemm_bn(int T, int N, int ctas);
 
 extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, int T,
@@ -388,18 +605,6 @@ extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, 
   if (rc) return rc;
   GemmParams p{};
   p.w = static_cast<const uint8_t*>(W);
-  p.Ma = T;
-  p.Nb = N;
-  p.K = K;
-  p.m_tiles = ceil_div(T, BM);
-  p.n_tiles = N / BN;
-  p.k_splits = 1;
-  p.num_kb = K / BK;
-  p.kb_per_split = p.num_kb;
-  {
-    const long a_tile_bytes = long(BM) * K * 2, budget = 32l << 20, all = a_tile_bytes * p.m_tiles;
-    p.group_m = all <= 2 * budget ? p.m_tiles : int(std::max<long>(8, budget / a_tile_bytes));
-  }
   p.out = static_cast<__nv_bfloat16*>(Y);
   p.ldo = ldy;
   p.epi = EPI_ROPE;
@@ -412,9 +617,7 @@ extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, 
   p.Hq = Hq;
   p.Hkv = Hkv;
   p.hd = d;
-  const int grid = std::min(p.m_tiles * p.n_tiles, max_ctas);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return BN == 128 ? launch<128>(ta, p, grid, st) : launch<256>(ta, p, grid, st);
+  return plan_and_launch(ta, p, T, N, K, BN, max_ctas, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
@@ -448,11 +651,14 @@ static int gemm_bn(int T, int N, int ctas) {
 
 extern "C" int hp_gemm_tiles(int T, int N) { return ((T + BM - 1) / BM) * (N / 256); }
 
-extern "C" int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles) {
+extern "C" int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles, int* ctas_per_tile) {
   HP_CHECK_ARG(T >= 1 && N % 128 == 0 && max_ctas >= 1, "hp_gemm_plan: bad shape");
   const int b = gemm_bn(T, N, max_ctas);
+  const bool pair = use_pair(b, max_ctas);
+  const int rows = pair ? 2 * BM : BM;
   if (bn) *bn = b;
-  if (tiles) *tiles = ((T + BM - 1) / BM) * (N / b);
+  if (tiles) *tiles = ((T + rows - 1) / rows) * (N / b);
+  if (ctas_per_tile) *ctas_per_tile = pair ? 2 : 1;
   return HP_OK;
 }
 
@@ -473,31 +679,12 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
   if (rc) return rc;
   GemmParams p{};
   p.w = static_cast<const uint8_t*>(W);
-  p.Ma = T;
-  p.Nb = N;
-  p.K = K;
-  p.m_tiles = ceil_div(T, BM);
-  // rasterization group: keep the activation block of a group within ~32 MB
-  // of the 126 MB L2 (decode traffic shares it during co-execution)
-  {
-    const long a_tile_bytes = long(BM) * K * 2;
-    const long budget = 32l << 20;
-    const long all = a_tile_bytes * p.m_tiles;
-    p.group_m = all <= 2 * budget ? p.m_tiles : int(std::max<long>(8, budget / a_tile_bytes));
-  }
-  p.n_tiles = N / BN;
-  p.k_splits = 1;
-  p.num_kb = K / BK;
-  p.kb_per_split = p.num_kb;
   p.out = static_cast<__nv_bfloat16*>(Y);
   p.ldo = ldy;
   p.resid = static_cast<const __nv_bfloat16*>(R);
   p.ldr = ldr;
   p.epi = epilogue;
   p.cta_times = cta_times;
-  const int units = p.m_tiles * p.n_tiles;
-  const int grid = std::min(units, max_ctas);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return BN == 128 ? launch<128>(ta, p, grid, st) : launch<256>(ta, p, grid, st);
+  return plan_and_launch(ta, p, T, N, K, BN, max_ctas, static_cast<cudaStream_t>(stream));
 }
 

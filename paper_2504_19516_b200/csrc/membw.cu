@@ -282,9 +282,91 @@ __global__ void __launch_bounds__(128) k_umma_rate(int n, int chains, long long*
   }
 }
 
+// Pair (cta_group::2) MMA rate: a 2-CTA cluster issues M=256 x N x K=16
+// MMAs from the leader CTA (each CTA supplies its 128 rows of A and half of
+// B from its own smem; each holds its 128 accumulator rows in TMEM).
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_umma2_rate(int n, long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)),
+                 "r"(256u) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (rank == 0 && warp == 0) {
+    constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
+    const uint64_t ad = umma_desc_sw128(smem_u32(smem)), bd = umma_desc_sw128(smem_u32(smem + 16384));
+    const long long t0 = clock64();
+    for (int i = 0; i < n; i += 4) {
+      const uint32_t acc = i >= 4 ? 1u : 0u;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+              "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(acc | (k > 0 ? 1u : 0u))
+              : "memory");
+      }
+      __syncwarp();
+    }
+    const long long t1 = clock64();
+    if (elect_one())
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(&bar)),
+          "h"(uint16_t(3))
+          : "memory");
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t2 = clock64();
+    if (lane_id() == 0) {
+      out[blockIdx.x] = t1 - t0;
+      out[gridDim.x + blockIdx.x] = t2 - t0;
+    }
+  } else if (rank == 1 && warp == 0) {
+    mbar_wait(&bar, 0);  // the leader's multicast commit arrives here too
+  }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u) : "memory");
+  }
+}
+
 }  // namespace hp
 
 using namespace hp;
+
+extern "C" int hp_umma2_rate(int n, int bn, int pairs, long long* out, void* stream) {
+  HP_CHECK_ARG(out && n >= 4 && pairs >= 1 && (bn == 128 || bn == 256), "hp_umma2_rate: bad args");
+  const size_t smem = 1024 + 65536;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (bn == 128) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma2_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma2_rate<128><<<2 * pairs, 128, smem, st>>>(n, out);
+  } else {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma2_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma2_rate<256><<<2 * pairs, 128, smem, st>>>(n, out);
+  }
+  HP_LAUNCH_CHECK("k_umma2_rate");
+  return HP_OK;
+}
 
 extern "C" int hp_umma_rate(int n, int bn, int chains, int ctas, long long* out, void* stream) {
   HP_CHECK_ARG(out && n >= 4 && chains != 0 && (chains < 0 ? -chains : chains) * bn <= 256 && ctas >= 1,

@@ -36,7 +36,7 @@ SIGNATURES = {
     "hp_gemm_traced": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "hp_gemm_tiles": (_i, [_i, _i]),
     "hp_gemm_qkv_rope": (_i, [_p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
-    "hp_gemm_plan": (_i, [_i, _i, _i, C.POINTER(_i), C.POINTER(_i)]),
+    "hp_gemm_plan": (_i, [_i, _i, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
@@ -51,6 +51,7 @@ SIGNATURES = {
     "hp_membw": (_i, [_p, _sz, _i, _i, _p, _p]),
     "hp_membw2d": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "hp_membw_pipe": (_i, [_p, _sz, _i, _i, _i, _p, _p]),
+    "hp_umma2_rate": (_i, [_i, _i, _i, _p, _p]),
     "hp_umma_rate": (_i, [_i, _i, _i, _i, _p, _p]),
 }
 
@@ -195,11 +196,13 @@ def gemm_qkv_rope(x, w, y, Hq: int, Hkv: int, d: int, positions, cos_sin, slots,
                                   _ptr(vcache), page, max_ctas, _stream(stream)), "hp_gemm_qkv_rope")
 
 
-def gemm_plan(T: int, N: int, max_ctas: int) -> tuple[int, int]:
-    """(tile width, tile count) hp_gemm uses on a `max_ctas`-SM partition."""
-    bn, tiles = C.c_int(), C.c_int()
-    check(load().hp_gemm_plan(T, N, max_ctas, C.byref(bn), C.byref(tiles)), "hp_gemm_plan")
-    return bn.value, tiles.value
+def gemm_plan(T: int, N: int, max_ctas: int) -> tuple[int, int, int]:
+    """(tile width, tile count, CTAs per tile) hp_gemm uses on a
+    `max_ctas`-SM partition; its persistent grid runs
+    wave_stats(tiles, 1, max_ctas // ctas_per_tile) rounds."""
+    bn, tiles, cpt = C.c_int(), C.c_int(), C.c_int()
+    check(load().hp_gemm_plan(T, N, max_ctas, C.byref(bn), C.byref(tiles), C.byref(cpt)), "hp_gemm_plan")
+    return bn.value, tiles.value, cpt.value
 
 
 def prefill_attn_paged(q, kcache, vcache, block_table, cu_seqlens, prior_lens, nseq: int, max_seqlen: int,

@@ -31,7 +31,8 @@ from .partition import DECODE, PREFILL, PartitionPool
 
 def measure(pool: PartitionPool, x, w, y, epi, resid, n: int, reps: int = 3):
     st = pool.phase(DECODE, n) if n < pool.n else pool.full(PREFILL)
-    grid = min(lib.gemm_plan(x.shape[0], w.shape[0], st.sms)[1], st.sms)
+    _, tiles, cpt = lib.gemm_plan(x.shape[0], w.shape[0], st.sms)
+    grid = min(tiles * cpt, (st.sms // cpt) * cpt)
     times = torch.zeros(grid, 3, dtype=torch.int64, device=x.device)
     best = None
     with torch.cuda.stream(st.torch_stream):
@@ -74,8 +75,8 @@ def main(argv=None) -> int:
         for name, x, w, y, epi, r in gemms:
             for n in grid:
                 idle, span, sms_seen, n_real = measure(pool, x, w, y, epi, r, n)
-                tiles = lib.gemm_plan(T, w.shape[0], n_real)[1]
-                pred = wave_stats(tiles, 1, n_real)
+                _, tiles, cpt = lib.gemm_plan(T, w.shape[0], n_real)
+                pred = wave_stats(tiles, 1, n_real // cpt)
                 row = {"kernel": name, "T": T, "tiles": tiles, "n": n_real,
                        "predicted_idle": pred.idle_ratio, "waves": pred.waves, "tail_sms": pred.tail_sms,
                        "measured_idle": idle, "span_us": span * 1e6, "distinct_sms": sms_seen,
