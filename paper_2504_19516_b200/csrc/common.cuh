@@ -154,6 +154,14 @@ HP_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// relaxed remote arrive: for signalling tcgen05 (TMEM) progress, which is
+// ordered by tcgen05.wait + tcgen05.fence::before_thread_sync, not by the
+// generic-proxy release (whose cluster-scope drain of the thread's earlier
+// global stores costs ~1.5 k cycles on the softmax critical path)
+HP_DEVICE void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 // wait with cluster-scope acquire (arrivals came from the peer CTA)
 HP_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
