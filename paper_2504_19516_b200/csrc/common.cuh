@@ -140,20 +140,6 @@ HP_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-// spin (no suspend) on a local mbarrier: for a thread on a latency-critical
-// relay path, where a suspended try_wait's wake-up would stall the pipeline
-HP_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 // relaxed remote arrive: for signalling tcgen05 (TMEM) progress, which is
 // ordered by tcgen05.wait + tcgen05.fence::before_thread_sync, not by the
 // generic-proxy release (whose cluster-scope drain of the thread's earlier

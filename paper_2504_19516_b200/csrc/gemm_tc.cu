@@ -492,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       epilogue_row<BN>(p, taddr, mt * 2 * BM + int(rank) * BM + row, nt);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ltempty + 8u * acc);
+      if (lane == 0) mbar_arrive_cluster_relaxed(ltempty + 8u * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
