@@ -354,10 +354,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_umma2_rate(in
 using namespace hp;
 
 extern "C" int hp_umma2_rate(int n, int bn, int pairs, long long* out, void* stream) {
-  HP_CHECK_ARG(out && n >= 4 && pairs >= 1 && (bn == 128 || bn == 256), "hp_umma2_rate: bad args");
+  HP_CHECK_ARG(out && n >= 4 && pairs >= 1 && (bn == 32 || bn == 64 || bn == 128 || bn == 256),
+               "hp_umma2_rate: bad args");
   const size_t smem = 1024 + 65536;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (bn == 128) {
+  if (bn == 32) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma2_rate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma2_rate<32><<<2 * pairs, 128, smem, st>>>(n, out);
+  } else if (bn == 64) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_umma2_rate<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_umma2_rate<64><<<2 * pairs, 128, smem, st>>>(n, out);
+  } else if (bn == 128) {
     HP_CUDA_TRY(cudaFuncSetAttribute(k_umma2_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_umma2_rate<128><<<2 * pairs, 128, smem, st>>>(n, out);
   } else {

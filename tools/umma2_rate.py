@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2504_19516_b200.device import lib
-for bn in (128, 256):
+for bn in (32, 64, 128, 256):
     for pairs in (1, 74):
         n = 8192
         out = torch.zeros(4 * pairs, dtype=torch.int64, device="cuda")

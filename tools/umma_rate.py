@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2504_19516_b200.device import lib
 out = torch.zeros(148 * 2, dtype=torch.int64, device="cuda")
-for bn in (64, 128, 256):
+for bn in (32, 64, 128, 256):
     for chains in (1, 2, -1, -2):
         if abs(chains) * bn > 256:
             continue
