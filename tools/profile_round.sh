@@ -19,7 +19,7 @@ echo "split $SPLIT"
 # launch list of the same bench command (fixed split, no sweep): every launch
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 3000 \
     --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --split $SPLIT > $OUT/ncu_bench.out 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 6 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 6 -c 1 \
     -o $OUT/upgate python tools/one_kernel.py gemm4096 $PM 8 > $OUT/ncu_upgate.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_decode_attn -s 2 -c 1 \
     -o $OUT/decode_attn python tools/one_kernel.py decode_attn 148 4 > $OUT/ncu_dattn.out 2>&1
