@@ -86,7 +86,10 @@ int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream
  * tiled by hp_tile_weight (pass ldw = K).
  * SILU: W rows interleaved in blocks of 64 (gate, up), Y has N/2 columns.
  * The qkv / o_proj / mlp_up_gate / mlp_down kernels of layer_kernels
- * (workload.py:162-210) at phase "prefill". */
+ * (workload.py:162-210) at phase "prefill".  Runs as CTA pairs (2-CTA
+ * clusters, tcgen05.mma.cta_group::2 on 256 x 256 tiles) when the planned
+ * tile width is 256 and max_ctas >= 2, else as single CTAs (hp_gemm_plan;
+ * HP_GEMM_PAIR=0 forces single CTAs for A/B measurement). */
 int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
             int ldr, int T, int N, int K, int epilogue, int max_ctas, void* stream);
 /* The prefill QKV projection with RoPE and the paged K/V write fused into
