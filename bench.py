@@ -268,10 +268,10 @@ def main(argv=None) -> int:
         pm = N - dm
         t_d = cr.isolated(DECODE, dm, reps=3)
         t_p = cr.isolated(PREFILL, pm, reps=3)
-        # decode steps per prefill layer: the counts either side of t_p / t_d
-        # (fit inside the prefill layer, or overrun it by one step)
+        # decode steps per prefill layer around t_p / t_d (isolated times;
+        # co-running decode is slower, so one fewer step may fit)
         nf = max(1, math.floor(t_p / t_d))
-        for n in ([fixed[2]] if fixed else sorted({nf, nf + 1})):
+        for n in ([fixed[2]] if fixed else sorted({max(1, nf - 1), nf, nf + 1})):
             r = cr.corun(pm, dm, 2, n)
             ok = r.p50(r.decode_layer_s) <= ts_tpot and r.p50(r.prefill_layer_s) <= ts_ttft
             candidates.append({"pm": pm, "dm": dm, "n": n, "tokens_per_s": r.tokens_per_s,
