@@ -19,7 +19,6 @@ on the launching streams.
 
 from __future__ import annotations
 
-import math
 import statistics
 from dataclasses import dataclass, field
 

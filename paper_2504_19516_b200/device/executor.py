@@ -36,7 +36,7 @@ import math
 import torch
 
 from ..errors import InvalidArgumentError
-from ..perf_model import ExecutionState, GpuSpec, scaled_peaks, srm_decode_step_s, srm_prefill_layer_s
+from ..perf_model import ExecutionState, GpuSpec, srm_decode_step_s, srm_prefill_layer_s
 from ..workload import ModelSpec
 from . import lib
 from .layer import PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch, decode_slots

@@ -9,12 +9,11 @@ stream through the layers and owns the shared paged-KV block pool.
 
 from __future__ import annotations
 
-import numpy as np
 import torch
 
 from ..workload import ModelSpec
 from . import lib
-from .layer import (PAGE, EPS, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch,
+from .layer import (EPS, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch,
                     decode_slots)
 
 
