@@ -285,10 +285,15 @@ class DeviceLayer:
 
         n = 0
         lib.rmsnorm(x, self.W.attn_norm, sc.xn[:T], EPS, sms, stream)
-        linear(sc.xn[:T], self.W.w_qkv, qkv, lib.EPI_STORE)
-        lib.rope_kv_write(qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k, cache.v, cache.page,
-                          max_ctas=sms, stream=stream)
-        n += 3
+        if swap:
+            linear(sc.xn[:T], self.W.w_qkv, qkv, lib.EPI_STORE)
+            lib.rope_kv_write(qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k, cache.v, cache.page,
+                              max_ctas=sms, stream=stream)
+            n += 3
+        else:  # token-major GEMM with RoPE + paged K/V write fused into the epilogue
+            lib.gemm_qkv_rope(sc.xn[:T], self.W.w_qkv, qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k,
+                              cache.v, cache.page, max_ctas=sms, stream=stream)
+            n += 2
         if Tc > 0:
             lib.prefill_attn_paged(qkv[:Tc, : Hq * d], cache.k, cache.v, chunk_block_table, cu_chunks,
                                    prior_lens, n_chunks, max_chunk, sc.attn[:Tc], Hq, Hkv, d, cache.page,
