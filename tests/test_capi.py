@@ -61,3 +61,25 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(lib, "_LIB", None)
     with pytest.raises(lib.HotPathError, match="no CPU fallback"):
         lib.load(tmp_path / "nope.so")
+
+
+def test_gemm_tile_planner_is_host_side():
+    # hp_gemm_plan: CTA-pair 256x256 tiles by default; 128-wide single-CTA
+    # tiles where they save a wave-quantised round (T=1024 qkv on 148 SMs)
+    assert lib.gemm_plan(4096, 28672, 140) == (256, 16 * 112, 2)
+    assert lib.gemm_plan(4096, 4096, 140) == (256, 16 * 16, 2)
+    bn, tiles, cpt = lib.gemm_plan(1024, 6144, 148)
+    assert (bn, cpt) == (128, 1) and tiles == 8 * 48
+    assert lib.gemm_plan(300, 512, 1)[2] == 1  # one SM: no pair
+    from paper_2504_19516_b200.perf_model import wave_stats
+
+    # the rounds the persistent grid runs are the paper's wave count
+    _, t, c = lib.gemm_plan(4096, 6144, 140)
+    assert wave_stats(t, 1, 140 // c).waves == 6
+
+
+def test_decode_attention_launch_count_is_host_side():
+    # one launch while the context is not split, a combine launch otherwise
+    assert lib.decode_attn_launches(32, 8, 32, 64, 8) == 1
+    assert lib.decode_attn_launches(32, 8, 32, 64, 148) == 2
+    assert lib.decode_attn_launches(0, 8, 32, 64, 148) == 0
