@@ -41,6 +41,8 @@ extern "C" {
 #define HP_EPI_STORE 0 /* qkv projection          (workload.py:164-170) */
 #define HP_EPI_RESID 1 /* o_proj / mlp_down + residual (workload.py:191-194, 205-209) */
 #define HP_EPI_SILU 2  /* mlp_up_gate, silu(g)*u  (workload.py:198-204) */
+#define HP_EPI_PEER 3  /* row-parallel partial scattered to every TP rank (hp_gemm_swap_peer) */
+#define HP_MAX_PEERS 8 /* tensor-parallel degree bound of the fused all-reduce */
 
 /* ---------------------------------------------------------------- runtime */
 int hp_abi_version(void);
@@ -128,6 +130,39 @@ size_t hp_gemm_swap_ws_bytes(int T, int N, int K, int max_ctas);
 int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R,
                  int ldr, int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes,
                  int* counters, int n_counters, int max_ctas, void* stream);
+
+/* Fused row-parallel GEMM + all-reduce for tensor-parallel decode (config 5,
+ * SURVEY.md §8(f)#4; replaces the NCCL all-reduce after o_proj / mlp_down of
+ * a Megatron row-parallel layer).  Symmetric buffers: every
+ * rank r owns recv_r = bf16 [2][world][T][N] and flags_r = int [2][world][tiles]
+ * (tiles = hp_peer_tiles(T, N); flags zero at allocation) and maps every
+ * peer's pair (hp_ipc_*).  Call e (epoch e >= 1, +1 per call, all ranks in
+ * step) uses half (e & 1) of each buffer:
+ *   hp_gemm_swap_peer: the swap-AB GEMM's epilogue writes this rank's partial
+ *     tile straight into slot `rank` of every peer's recv over NVLink, then
+ *     raises flags_q[rank][tile] = epoch (system-scope release) -- the
+ *     transfer of tile i overlaps the MMA of tile i+1;
+ *   hp_peer_reduce: per output tile, wait for every rank's flag >= epoch and
+ *     write out = sum_r recv[r] + resid (fp32 sum, bf16 out, rank order).
+ * peer_recv / peer_flags: the world pointers of half (e & 1), indexed by rank.
+ * Double buffering makes back-to-back calls safe: a rank can reach epoch
+ * e + 2 only after every rank's partial for e + 1, i.e. after they all left
+ * epoch e's reduce. */
+int hp_peer_tiles(int T, int N);
+int hp_gemm_swap_peer(const void* X, int ldx, const void* W, int ldw, int T, int N, int K,
+                      void* const* peer_recv, int* const* peer_flags, int world, int rank, int epoch,
+                      void* workspace, size_t ws_bytes, int* counters, int n_counters, int max_ctas,
+                      void* stream);
+int hp_peer_reduce(const void* recv, const int* flags, int world, int T, int N, int epoch,
+                   const void* resid, int ldr, void* out, int ldo, void* stream);
+/* CUDA IPC for the symmetric buffers: export the handle (HP_IPC_HANDLE_BYTES
+ * opaque bytes) of the allocation block holding dev_ptr plus dev_ptr's
+ * offset in it; a peer maps the block (hp_ipc_open -> base; its pointer is
+ * base + offset) and unmaps it with hp_ipc_close(base). */
+#define HP_IPC_HANDLE_BYTES 64
+int hp_ipc_handle(void* dev_ptr, void* handle_out, size_t* offset_out);
+int hp_ipc_open(const void* handle, void** base_out);
+int hp_ipc_close(void* base);
 
 /* RoPE on q,k in the fused qkv buffer [T, (Hq+2Hkv)*d] (in place) and the
  * paged KV-cache write of k,v (the `kv_write` bytes of the attention kernel,

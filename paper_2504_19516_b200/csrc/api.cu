@@ -4,6 +4,7 @@
 #include "runtime.h"
 #include "../../include/hp.h"
 
+#include <cstring>
 #include <new>
 #include <string>
 
@@ -154,3 +155,38 @@ extern "C" int hp_partition_sms(hp_partition* part, int phase, int* sms) {
 }
 
 extern "C" int hp_partition_destroy(hp_partition* part) { return destroy_partition(part); }
+
+// CUDA IPC for the fused tensor-parallel all-reduce's symmetric buffers.
+static_assert(sizeof(cudaIpcMemHandle_t) <= HP_IPC_HANDLE_BYTES, "IPC handle size");
+
+// The handle names the whole cudaMalloc block; a caching allocator hands out
+// sub-ranges, so the pointer's offset inside its block travels with it.
+extern "C" int hp_ipc_handle(void* dev_ptr, void* handle_out, size_t* offset_out) {
+  HP_CHECK_ARG(dev_ptr && handle_out && offset_out, "hp_ipc_handle: null pointer");
+  const Driver* d = driver();
+  if (!d) return HP_ERR_NO_DEVICE;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = d->memGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr));
+  if (r != CUDA_SUCCESS) return set_error(HP_ERR_CUDA, "cuMemGetAddressRange: " + cu_error_string(r));
+  cudaIpcMemHandle_t h;
+  HP_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memset(handle_out, 0, HP_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = size_t(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return HP_OK;
+}
+
+extern "C" int hp_ipc_open(const void* handle, void** base_out) {
+  HP_CHECK_ARG(handle && base_out, "hp_ipc_open: null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  HP_CUDA_TRY(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return HP_OK;
+}
+
+extern "C" int hp_ipc_close(void* dev_ptr) {
+  HP_CHECK_ARG(dev_ptr, "hp_ipc_close: null pointer");
+  HP_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return HP_OK;
+}

@@ -70,6 +70,12 @@ struct SwapParams {
   const uint8_t* w;  // weights in the tiled layout (hp_tile_weight)
   int epi;
   unsigned long long* trace;  // optional [grid][6] globaltimer stamps (hp_set_trace; development aid)
+  // HP_EPI_PEER (row-parallel layers under tensor parallelism): the partial
+  // tile goes to slot `rank` of every rank's receive buffer [world][T][N]
+  // over peer memory, then flag [rank][tile] := epoch is raised on every rank
+  __nv_bfloat16* peer_out[HP_MAX_PEERS];
+  int* peer_flags[HP_MAX_PEERS];
+  int world, rank, epoch;
 };
 
 struct Seg {
@@ -124,6 +130,20 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
       const float u0 = V[(r + 64) * VLD + j], u1 = V[(r + 65) * VLD + j];
       *reinterpret_cast<uint32_t*>(p.out + size_t(t) * p.ldo + mt * 64 + r) =
           pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+    }
+  } else if (p.epi == HP_EPI_PEER) {
+    // 16-byte stores: thread -> (token j, 8 consecutive features g*8..g*8+7)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int f = i * 128 + et, j = f >> 4, g = f & 15;
+      const int t = nt * BN + c0 + j;
+      if (t < p.T) {
+        const float* c = V + (g * 8) * VLD + j;
+        const uint4 v = make_uint4(pack_bf16(c[0], c[VLD]), pack_bf16(c[2 * VLD], c[3 * VLD]),
+                                   pack_bf16(c[4 * VLD], c[5 * VLD]), pack_bf16(c[6 * VLD], c[7 * VLD]));
+        const size_t off = (size_t(p.rank) * p.T + t) * p.N + mt * SBM + g * 8;
+        for (int q = 0; q < p.world; ++q) *reinterpret_cast<uint4*>(p.peer_out[q] + off) = v;
+      }
     }
   } else {
     for (int j = w; j < 32; j += 4) {
@@ -281,6 +301,17 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int et = (warp - SW_MMA - 1) * 32 + lane;
+    // HP_EPI_PEER: once the whole tile sits in every rank's receive buffer,
+    // publish it with a system-scope release on every rank's flag array
+    auto publish = [&](int tile) {
+      if (p.epi != HP_EPI_PEER) return;
+      epi_sync();
+      if (et == 0) {
+        __threadfence_system();
+        for (int r = 0; r < p.world; ++r)
+          st_release_sys(p.peer_flags[r] + size_t(p.rank) * (p.m_tiles * p.n_tiles) + tile, p.epoch);
+      }
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = begin;
@@ -309,6 +340,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
           epi_sync();
           emit_chunk<BN>(p, V, mt, nt, c * 32, et);
         }
+        publish(s.tile);
       } else {
         float* mine = p.ws + (size_t(s.tile) * p.max_contrib + (blockIdx.x - first)) * (SBM * BN) +
                       size_t(row) * BN;
@@ -384,6 +416,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
             emit_chunk<BN>(p, V, mt, nt, c * 32, et);
           }
           if (et == 0) p.counters[s.tile] = 0;
+          publish(s.tile);
         }
       }
       acc ^= 1;
@@ -431,16 +464,101 @@ extern "C" size_t hp_gemm_swap_ws_bytes(int T, int N, int K, int max_ctas) {
   return size_t(tiles) * max_contrib * SBM * BN * sizeof(float);
 }
 
+// Receive side of the fused tensor-parallel all-reduce.  Block = 16 tokens x
+// one 128-feature tile column (thread: 8 features, 16-byte loads); it waits
+// until every rank published the tile for `epoch`, then writes
+// out = sum over ranks (rank order, fp32) + resid.
+__global__ void __launch_bounds__(256) k_peer_reduce(const __nv_bfloat16* __restrict__ recv, const int* flags,
+                                                     int world, int T, int N, int m_tiles, int bn, int epoch,
+                                                     const __nv_bfloat16* __restrict__ resid, int ldr,
+                                                     __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_trigger();
+  pdl_wait();
+  const int mt = blockIdx.x, t0 = blockIdx.y * 16;
+  const int tile = (t0 / bn) * m_tiles + mt;
+  const int ntiles = m_tiles * ((T + bn - 1) / bn);
+  if (threadIdx.x < world) {
+    const int* f = flags + size_t(threadIdx.x) * ntiles + tile;
+    while (ld_acquire_sys(f) < epoch) __nanosleep(32);
+  }
+  __syncthreads();
+  const int t = t0 + (threadIdx.x >> 4);
+  if (t >= T) return;
+  const int o = mt * SBM + (threadIdx.x & 15) * 8;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto add = [&](uint4 v) {
+    a[0] += bf16lo(v.x); a[1] += bf16hi(v.x); a[2] += bf16lo(v.y); a[3] += bf16hi(v.y);
+    a[4] += bf16lo(v.z); a[5] += bf16hi(v.z); a[6] += bf16lo(v.w); a[7] += bf16hi(v.w);
+  };
+  uint4 v[HP_MAX_PEERS];
+#pragma unroll
+  for (int r = 0; r < HP_MAX_PEERS; ++r)
+    if (r < world) v[r] = __ldcg(reinterpret_cast<const uint4*>(recv + (size_t(r) * T + t) * N + o));
+#pragma unroll
+  for (int r = 0; r < HP_MAX_PEERS; ++r)
+    if (r < world) add(v[r]);
+  if (resid) add(*reinterpret_cast<const uint4*>(resid + size_t(t) * ldr + o));
+  *reinterpret_cast<uint4*>(out + size_t(t) * ldo + o) =
+      make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+}
+
+static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
+                          int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes, int* counters,
+                          int n_counters, int max_ctas, void* stream, void* const* peer_recv,
+                          int* const* peer_flags, int world, int rank, int epoch);
+
 extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                             const void* R, int ldr, int T, int N, int K, int epilogue,
                             void* workspace, size_t ws_bytes, int* counters, int n_counters,
                             int max_ctas, void* stream) {
-  HP_CHECK_ARG(X && W && Y, "hp_gemm_swap: null pointer");
+  HP_CHECK_ARG(Y, "hp_gemm_swap: null pointer");
+  HP_CHECK_ARG(epilogue >= HP_EPI_STORE && epilogue <= HP_EPI_SILU, "hp_gemm_swap: bad epilogue");
+  return gemm_swap_impl(X, ldx, W, ldw, Y, ldy, R, ldr, T, N, K, epilogue, workspace, ws_bytes, counters,
+                        n_counters, max_ctas, stream, nullptr, nullptr, 0, 0, 0);
+}
+
+extern "C" int hp_gemm_swap_peer(const void* X, int ldx, const void* W, int ldw, int T, int N, int K,
+                                 void* const* peer_recv, int* const* peer_flags, int world, int rank, int epoch,
+                                 void* workspace, size_t ws_bytes, int* counters, int n_counters, int max_ctas,
+                                 void* stream) {
+  HP_CHECK_ARG(peer_recv && peer_flags && world >= 1 && world <= HP_MAX_PEERS && rank >= 0 && rank < world,
+               "hp_gemm_swap_peer: bad peer arguments");
+  HP_CHECK_ARG(epoch >= 1, "hp_gemm_swap_peer: epoch must be >= 1 and increase per call");
+  for (int q = 0; q < world; ++q)
+    HP_CHECK_ARG(peer_recv[q] && peer_flags[q], "hp_gemm_swap_peer: null peer buffer");
+  return gemm_swap_impl(X, ldx, W, ldw, nullptr, 0, nullptr, 0, T, N, K, HP_EPI_PEER, workspace, ws_bytes,
+                        counters, n_counters, max_ctas, stream, peer_recv, peer_flags, world, rank, epoch);
+}
+
+extern "C" int hp_peer_reduce(const void* recv, const int* flags, int world, int T, int N, int epoch,
+                              const void* resid, int ldr, void* out, int ldo, void* stream) {
+  HP_CHECK_ARG(recv && flags && out && world >= 1 && world <= HP_MAX_PEERS, "hp_peer_reduce: bad arguments");
+  HP_CHECK_ARG(T >= 1 && T <= 256 && N % SBM == 0, "hp_peer_reduce: T in [1, 256], N a multiple of 128");
+  HP_CHECK_ARG(ldo % 8 == 0 && (resid == nullptr || ldr % 8 == 0), "hp_peer_reduce: pitch not 16-byte aligned");
+  const int m_tiles = N / SBM;
+  HP_LAUNCH_PDL("k_peer_reduce", k_peer_reduce, dim3(m_tiles, (T + 15) / 16), dim3(256), 0,
+                static_cast<cudaStream_t>(stream), static_cast<const __nv_bfloat16*>(recv), flags, world, T, N,
+                m_tiles, swap_bn(T), epoch, static_cast<const __nv_bfloat16*>(resid), ldr,
+                static_cast<__nv_bfloat16*>(out), ldo);
+  HP_LAUNCH_CHECK("k_peer_reduce");
+  return HP_OK;
+}
+
+extern "C" int hp_peer_tiles(int T, int N) {
+  if (T < 1 || T > 256 || N % SBM) return HP_ERR_INVALID;
+  const int BN = swap_bn(T);
+  return (N / SBM) * ((T + BN - 1) / BN);
+}
+
+static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
+                          int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes, int* counters,
+                          int n_counters, int max_ctas, void* stream, void* const* peer_recv,
+                          int* const* peer_flags, int world, int rank, int epoch) {
+  HP_CHECK_ARG(X && W, "hp_gemm_swap: null pointer");
   HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
   HP_CHECK_ARG(N % 128 == 0, "hp_gemm_swap: N must be a multiple of 128 (tiled weight layout)");
   HP_CHECK_ARG(ldw == K, "hp_gemm_swap: W must be in the tiled layout (ldw == K)");
   HP_CHECK_ARG(K % SBK == 0, "hp_gemm_swap: K must be a multiple of 128");
-  HP_CHECK_ARG(epilogue >= HP_EPI_STORE && epilogue <= HP_EPI_SILU, "hp_gemm_swap: bad epilogue");
   HP_CHECK_ARG(epilogue != HP_EPI_RESID || R != nullptr, "hp_gemm_swap: residual epilogue needs R");
   HP_CHECK_ARG(max_ctas >= 1, "hp_gemm_swap: max_ctas must be >= 1");
   HP_CHECK_ARG(ldy % 2 == 0 && (R == nullptr || ldr % 2 == 0), "hp_gemm_swap: odd output pitch");
@@ -465,6 +583,13 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
   p.counters = counters;
   p.epi = epilogue;
   p.trace = static_cast<unsigned long long*>(trace_buf(TRACE_SWAP));
+  for (int q = 0; q < world; ++q) {
+    p.peer_out[q] = static_cast<__nv_bfloat16*>(peer_recv[q]);
+    p.peer_flags[q] = peer_flags[q];
+  }
+  p.world = world;
+  p.rank = rank;
+  p.epoch = epoch;
   const bool any_split = p.ipc % p.num_kb != 0 || p.ipc < p.num_kb;
   if (any_split) {
     HP_CHECK_ARG(workspace && counters, "hp_gemm_swap: split tiles need workspace and counters");

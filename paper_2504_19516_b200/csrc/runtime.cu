@@ -48,6 +48,7 @@ const Driver* driver() {
     ok &= resolve("cuStreamDestroy", g_driver.streamDestroy);
     ok &= resolve("cuDeviceGet", g_driver.deviceGet);
     ok &= resolve("cuGetErrorString", g_driver.getErrorString);
+    ok &= resolve("cuMemGetAddressRange", g_driver.memGetAddressRange);
     g_driver.loaded = ok;
   });
   if (!g_driver.loaded) {

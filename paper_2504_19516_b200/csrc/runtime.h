@@ -52,6 +52,7 @@ struct Driver {
   decltype(&::cuStreamDestroy) streamDestroy = nullptr;
   decltype(&::cuDeviceGet) deviceGet = nullptr;
   decltype(&::cuGetErrorString) getErrorString = nullptr;
+  decltype(&::cuMemGetAddressRange) memGetAddressRange = nullptr;
 };
 
 // Returns nullptr (with hp_last_error set) when the driver is unavailable.

@@ -16,7 +16,9 @@ from ..errors import InvalidArgumentError
 
 LIB_PATH = Path(__file__).resolve().parent.parent / "_lib" / "libb200hot.so"
 
-EPI_STORE, EPI_RESID, EPI_SILU = 0, 1, 2
+EPI_STORE, EPI_RESID, EPI_SILU, EPI_PEER = 0, 1, 2, 3
+MAX_PEERS = 8
+IPC_HANDLE_BYTES = 64
 
 # Every symbol include/hp.h declares, with (restype, argtypes).
 _i, _u64, _p, _f, _sz, _i64 = C.c_int, C.c_uint64, C.c_void_p, C.c_float, C.c_size_t, C.c_int64
@@ -39,6 +41,12 @@ SIGNATURES = {
     "hp_gemm_plan": (_i, [_i, _i, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
+    "hp_peer_tiles": (_i, [_i, _i]),
+    "hp_gemm_swap_peer": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _p, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
+    "hp_peer_reduce": (_i, [_p, _p, _i, _i, _i, _i, _p, _i, _p, _i, _p]),
+    "hp_ipc_handle": (_i, [_p, _p, C.POINTER(_sz)]),
+    "hp_ipc_open": (_i, [_p, C.POINTER(_p)]),
+    "hp_ipc_close": (_i, [_p]),
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
     "hp_set_trace": (_i, [_i, _p]),
@@ -171,6 +179,51 @@ def gemm_swap(x, w, y, ws, counters, epilogue: int = EPI_STORE, resid=None,
                               epilogue, _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                               _ptr(counters), 0 if counters is None else counters.numel(), max_ctas,
                               _stream(stream)), "hp_gemm_swap")
+
+
+def peer_tiles(T: int, N: int) -> int:
+    n = load().hp_peer_tiles(T, N)
+    if n < 0:
+        raise InvalidArgumentError(f"peer_tiles: bad shape T={T} N={N}")
+    return n
+
+
+def gemm_swap_peer(x, w, peer_recv, peer_flags, world: int, rank: int, epoch: int, ws, counters,
+                   max_ctas: int = 148, stream=None) -> None:
+    """Row-parallel decode GEMM whose epilogue scatters this rank's partial
+    into every rank's receive buffer; peer_recv / peer_flags: ctypes arrays
+    of `world` device pointers (see include/hp.h hp_gemm_swap_peer)."""
+    T, K = x.shape
+    N = w.shape[0]
+    check(load().hp_gemm_swap_peer(_ptr(x), x.stride(0), _ptr(w), w.stride(0), T, N, K, peer_recv, peer_flags,
+                                   world, rank, epoch, _ptr(ws), ws.numel() * ws.element_size(), _ptr(counters),
+                                   counters.numel(), max_ctas, _stream(stream)), "hp_gemm_swap_peer")
+
+
+def peer_reduce(recv_ptr: int, flags_ptr: int, world: int, T: int, N: int, epoch: int, out, resid=None,
+                stream=None) -> None:
+    check(load().hp_peer_reduce(recv_ptr, flags_ptr, world, T, N, epoch, _ptr(resid),
+                                resid.stride(0) if resid is not None else 0, _ptr(out), out.stride(0),
+                                _stream(stream)), "hp_peer_reduce")
+
+
+def ipc_handle(t) -> tuple[bytes, int]:
+    """(handle of t's allocation block, t's byte offset inside it)."""
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    off = C.c_size_t()
+    check(load().hp_ipc_handle(_ptr(t), buf, C.byref(off)), "hp_ipc_handle")
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer's block; returns its base pointer in this process."""
+    p = C.c_void_p()
+    check(load().hp_ipc_open(C.create_string_buffer(handle, IPC_HANDLE_BYTES), C.byref(p)), "hp_ipc_open")
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    check(load().hp_ipc_close(ptr), "hp_ipc_close")
 
 
 def rope_kv_write(qkv, Hq: int, Hkv: int, d: int, positions, cos_sin, slots, kcache, vcache,

@@ -17,6 +17,11 @@ process group (NCCL over NVLink / NVSwitch on a B200 node), i.e. on the same
 green-context partition as the phase's kernels, which is where the
 reference charges collective traffic (the n_w term, perf_model.py:172-180).
 All compute is the 1-GPU hot path's kernels on the local shapes.
+
+With `peer=` (a PeerAllReduce, device/peer.py) decode-sized steps
+(T <= peer.T_max) skip both collectives: o_proj and mlp_down scatter their
+partial tiles into every rank's receive buffer from the GEMM epilogue and a
+flag-gated reduce adds the residual.
 """
 
 from __future__ import annotations
@@ -69,11 +74,12 @@ class TPLayer:
 
     def __init__(self, shape: TPShape, w_qkv_l, w_o_l, w_gate_l, w_up_l, w_down_l, attn_norm, mlp_norm,
                  rank: int, group=None, device=None, max_tokens: int = 4096, max_pos: int = 32768,
-                 allreduce=None):
+                 allreduce=None, peer=None):
         """`allreduce(tensor)` overrides the collective (default:
         torch.distributed.all_reduce over `group` on the calling stream)."""
         self.s = shape
         self.allreduce = allreduce
+        self.peer = peer
         self.rank = rank
         self.group = group
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
@@ -155,6 +161,13 @@ class TPLayer:
         return self._tail(x, y, B, sms, stream)
 
     def _tail(self, x, y, T, sms, stream):
+        if self.peer is not None and T <= self.peer.T_max:
+            # fused: every rank adds the (replicated) residual in the reduce
+            self.peer.linear(self.attn[:T], self.w_o, self.h[:T], resid=x, max_ctas=sms, stream=stream)
+            lib.rmsnorm(self.h[:T], self.mlp_norm, self.xn[:T], EPS, sms, stream)
+            self._linear(self.xn[:T], self.w_ug, self.act[:T], lib.EPI_SILU, None, sms, stream)
+            self.peer.linear(self.act[:T], self.w_down, y, resid=self.h[:T], max_ctas=sms, stream=stream)
+            return 0
         epi = self._epi()
         self._linear(self.attn[:T], self.w_o, self.h[:T], epi, x if epi == lib.EPI_RESID else None, sms, stream)
         self._allreduce(self.h[:T], stream)                    # all-reduce #1 (post O-proj)

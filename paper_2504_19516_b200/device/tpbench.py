@@ -37,6 +37,9 @@ def main(argv=None) -> int:
     ap.add_argument("--ctx", type=int, default=2048)
     ap.add_argument("--dm", type=int, default=32)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--fused", action="store_true",
+                    help="decode all-reduces fused into the o_proj/mlp_down epilogues (device/peer.py); on 1 GPU "
+                         "the tp ranks' receive buffers are emulated locally and peers' flags pre-raised")
     a = ap.parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -63,6 +66,14 @@ def main(argv=None) -> int:
     T, B, C = a.prefill, a.batch, a.ctx
     pl = TPLayer(s, *args, rank, group=groups[0], device=dev, max_tokens=T, max_pos=max(T, C) + 1)
     dl = TPLayer(s, *args, rank, group=groups[1], device=dev, max_tokens=B, max_pos=max(T, C) + 1)
+    if a.fused:
+        from .peer import PeerAllReduce
+
+        if world > 1:
+            dl.peer = PeerAllReduce.create(groups[1], B, s.hidden, dev)
+        else:  # rank 0's view of a tp-rank group: scatter to tp local buffers, peers' flags pre-raised
+            dl.peer = PeerAllReduce.local_group(tp, B, s.hidden, dev)[0]
+            dl.peer.flags.fill_(2 ** 31 - 1)
     bf = dict(dtype=torch.bfloat16, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
     px, py = torch.randn(T, s.hidden, **bf), torch.empty(T, s.hidden, **bf)
@@ -125,7 +136,11 @@ def main(argv=None) -> int:
     if rank == 0:
         print(json.dumps({
             "config": f"llama3-70b layer TP={tp}: chunked prefill {T} + decode batch {B} ctx {C}",
-            "world": world, "collective": "nccl all-reduce x2 per layer" if world > 1 else "none (1 GPU: rank-0 shard compute only)",
+            "world": world,
+            "collective": ("decode: fused GEMM-epilogue peer all-reduce x2 per layer; prefill: " if a.fused else "")
+            + ("nccl all-reduce x2 per layer" if world > 1 else
+               "none (1 GPU: rank-0 shard compute only" + (", fused epilogue scatter to tp local buffers)"
+                                                           if a.fused else ")")),
             "prefill_layer_us": t_p, "decode_layer_us": t_d,
             "corun": {"pm": pool.n - a.dm, "dm": a.dm, "prefill_layer_us": co_p, "decode_layer_us": co_d},
             "allreduce_bytes_per_layer": {"prefill": 2 * T * s.hidden * 2, "decode": 2 * B * s.hidden * 2},

@@ -48,7 +48,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, fused=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2504_19516_b200.device import lib
@@ -71,6 +71,10 @@ def _rank(rank, world, port, q):
     parts = shard_dense(W.w_qkv, W.w_o, W.w_gate, W.w_up, W.w_down, HQ, HKV, D, rank, world)
     lyr = TPLayer(tp_shape(H, HQ, HKV, D, INTER, world), *[tt(p) for p in parts], tt(W.attn_norm),
                   tt(W.mlp_norm), rank, device=dev, max_tokens=T, max_pos=1024, allreduce=ar)
+    if fused:  # decode all-reduces through the GEMM epilogue over CUDA IPC peer memory
+        from paper_2504_19516_b200.device.peer import PeerAllReduce
+
+        lyr.peer = PeerAllReduce.create(dist.group.WORLD, B, H, dev)
     kvh = HKV // world
     pages = -(-T // 64)
     kc = torch.zeros(pages + B * 4, kvh, 64, D, dtype=torch.bfloat16, device=dev)
@@ -89,29 +93,45 @@ def _rank(rank, world, port, q):
     yd = torch.empty(B, H, dtype=torch.bfloat16, device=dev)
     lyr.decode(tt(xd), yd, ctx, pos, slots, bt, kc, vc, 148, ws=ws)
     torch.cuda.synchronize()
+    if fused:
+        yd2 = torch.empty_like(yd)  # second call: the other buffer half, epoch 3/4
+        lyr.decode(tt(xd), yd2, ctx, pos, slots, bt, kc, vc, 148, ws=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(yd, yd2)
+        dist.barrier()
+        lyr.peer.close()
     q.put((rank, y.float().cpu().numpy(), yd.float().cpu().numpy()))
     dist.destroy_process_group()
 
 
-def test_tp2_layer_on_device_matches_oracle():
+@pytest.mark.parametrize("fused", [False, True], ids=["nccl_style", "fused_peer"])
+def test_tp2_layer_on_device_matches_oracle(fused):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, fused)) for r in range(world)]
     for p in procs:
+        p.daemon = True
         p.start()
     outs = {}
-    for _ in range(world):
-        r, y, yd = q.get(timeout=300)
-        outs[r] = (y, yd)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    try:
+        for _ in range(world):
+            r, y, yd = q.get(timeout=300)
+            outs[r] = (y, yd)
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
     W, x, xd = _weights()
     table = O.rope_table(1024, D)
     ref, _, _ = O.layer_prefill(x, W, HQ, HKV, D, np.arange(T), table, bf16_boundaries=True)
     assert np.array_equal(outs[0][0], outs[1][0])  # replicated after the all-reduce
+    if fused:
+        assert np.array_equal(outs[0][1], outs[1][1])
     assert excess(outs[0][0], ref) <= ATOL
     # decode oracle over the same cache contents: positions < CTX-1 of the decode
     # sequences were never written (zero K/V), exactly as on the device
