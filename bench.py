@@ -118,7 +118,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU oracle
-def cpu_reference_step(T: int, B: int, C: int, seed: int = 0):
+def cpu_reference_step(T: int, B: int, C: int, seed: int = 0, model: str = "llama3-8b"):
     """Time one bounded sample of the workload with the numpy CPU oracle:
     one Llama-3-8B prefill layer over T tokens + one decode layer-step for
     B sequences of context C.  Returns (seconds, tokens)."""
@@ -127,9 +127,11 @@ def cpu_reference_step(T: int, B: int, C: int, seed: int = 0):
     from oracle import numerics as O
     from paper_2504_19516_b200.workload import MODEL_PRESETS
 
-    m = MODEL_PRESETS["llama3-8b"]
+    from paper_2504_19516_b200.device.layer import mlp_width
+
+    m = MODEL_PRESETS[model]
     rng = np.random.default_rng(seed)
-    h, I, d, Hq, Hkv = m.hidden, m.intermediate, m.head_dim, m.num_heads, m.num_kv_heads
+    h, I, d, Hq, Hkv = m.hidden, mlp_width(m), m.head_dim, m.num_heads, m.num_kv_heads
 
     def w(*s):
         return (rng.standard_normal(s, dtype=np.float32) * 0.02)
@@ -224,6 +226,8 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--prefill-tokens", type=int, default=4096)
+    ap.add_argument("--model", default="llama3-8b", choices=["llama3-8b", "llama3-70b", "moe-a22b"],
+                    help="reference preset (workload.py:70-80); moe-a22b runs its MLP at the activated width")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--split", default=None, help="pm,dm,n: skip the warm-up split sweep (profiling)")
     args = ap.parse_args(argv)
@@ -252,7 +256,7 @@ def main(argv=None) -> int:
     from paper_2504_19516_b200.workload import MODEL_PRESETS
 
     hbm_gbs, tf_burst, tf_sus, peak_src = _peaks()
-    model = MODEL_PRESETS["llama3-8b"]
+    model = MODEL_PRESETS[args.model]
     T = args.prefill_tokens
     cr = CoRunner(model, T, DECODE_BATCH, DECODE_CTX, device=local, seed=1234 + rank)
     N = cr.n
@@ -339,7 +343,9 @@ def main(argv=None) -> int:
     dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}
 
     # ---- all four prefill GEMMs together (north-star target: >= 85 % of the partition's tensor peak)
-    gemm_flops = 2.0 * T * model.hidden * (model.qkv_out_dim + model.hidden + 3 * model.intermediate)
+    from paper_2504_19516_b200.device.layer import mlp_width
+
+    gemm_flops = 2.0 * T * model.hidden * (model.qkv_out_dim + model.hidden + 3 * mlp_width(model))
     gemm_s = sum(g_s[g] for g in ("qkv", "o_proj", "mlp_up_gate", "mlp_down"))
 
     # ---- roofline of the dominant kernel (mlp_up_gate GEMM, tensor-bound)
@@ -350,7 +356,7 @@ def main(argv=None) -> int:
     peak = tf_burst * pm / N
     traffic = None
     prof = ROOT / "profiles" / "roofline_traffic.json"
-    if prof.exists():
+    if prof.exists() and args.model == "llama3-8b" and T == 4096:  # the capture's shape
         try:
             traffic = json.loads(prof.read_text()).get("mlp_up_gate_bytes_per_launch")
         except Exception:
@@ -361,7 +367,7 @@ def main(argv=None) -> int:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         secs, toks = 0.0, 0
         for _ in range(2):
-            s, t = cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX)
+            s, t = cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX, model=args.model)
             secs += s
             toks += t
         cpu = {"value": toks / secs, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
@@ -373,10 +379,10 @@ def main(argv=None) -> int:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * span / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init Llama-3-8B layer weights, N(0,1) activations and KV)",
-        "config": {"workload": f"llama3-8b 1 layer: prefill chunk {T} tok on {pm} SMs || decode batch "
+        "data": f"synthetic (random-init {model.name} layer weights, N(0,1) activations and KV)",
+        "config": {"workload": f"{model.name} 1 layer: prefill chunk {T} tok on {pm} SMs || decode batch "
                                f"{DECODE_BATCH} ctx {DECODE_CTX} on {dm} SMs (green contexts)",
-                   "model": "llama3-8b (1 layer)", "prefill_tokens": T, "decode_batch": DECODE_BATCH,
+                   "model": f"{model.name} (1 layer)", "prefill_tokens": T, "decode_batch": DECODE_BATCH,
                    "decode_ctx": DECODE_CTX, "pm": pm, "dm": dm, "decode_steps_per_prefill_layer": n,
                    "parallelism": f"replicas x{world}", "l2": "inputs exceed L2 (weights+KV 1.1 GB/step)"},
         "p50_ttft_us": 1e6 * res.p50(res.prefill_layer_s),

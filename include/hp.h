@@ -208,11 +208,12 @@ int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache, const void
 
 /* Paged decode attention (workload.py:184-188): one query token per
  * sequence over ctx_lens[b] cached positions.  q: [B, Hq*d]; out: [B, Hq*d];
- * block_table: int [B, max_pages]; workspace: fp32, hp_decode_attn_ws_bytes. */
+ * block_table: int [B, max_pages]; workspace: fp32, hp_decode_attn_ws_bytes.
+ * GQA group Hq/Hkv <= 8, or a multiple of 8 (run as Hq/Hkv/8 head blocks). */
 size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits);
 /* Kernel launches hp_decode_attn issues for this shape (2 when the context
  * is split and a log-sum-exp combine follows; bounded by the workspace). */
-int hp_decode_attn_launches(int B, int Hkv, int max_pages, int page, int max_ctas);
+int hp_decode_attn_launches(int B, int Hq, int Hkv, int d, int max_pages, int page, int max_ctas);
 int hp_decode_attn(const void* q, int ldq, const void* kcache, const void* vcache,
                    const int* block_table, int max_pages, const int* ctx_lens, void* out, int ldo,
                    int B, int Hq, int Hkv, int d, int page, int num_blocks, float scale,

@@ -19,7 +19,12 @@
 // so the query group (<= 8 heads) sits in the MMA's N=8 dimension, with an
 // exp2 online softmax and warp-shuffle max/sum; the warps merge (m, l, O) at
 // the unit end and multi-split sequences are merged by log-sum-exp in
-// k_decode_combine.
+// k_decode_combine.  A group of 16 heads at d = 64 (the moe-a22b preset's
+// 64 q / 4 kv heads) uses two N=8 column blocks per K/V fragment (NB = 2:
+// every K and V ldmatrix feeds two MMAs); other groups above 8 run as
+// Gb-head blocks of
+// one unit each, sibling units adjacent in the unit order so the later
+// blocks' K/V reads are L2 hits of the first's (no evict-first hint then).
 //
 // Caches must not hold NaN/Inf in unused slots of partially filled pages
 // (allocate them zeroed): masked probabilities are exactly 0, but 0 * NaN is
@@ -56,17 +61,18 @@ struct DaPlan {
   size_t smem;
 };
 
-inline size_t da_fixed_bytes(int D, int G) {
-  const int cb = G * D + 16;
-  return 1024 + size_t(DA_CONSUMERS) * cb * 4 + size_t(DA_CONSUMERS) * 8 * DA_PROW * 2 +
+// G = heads per unit (Gb), NB = 8-head column blocks (1 or 2)
+inline size_t da_fixed_bytes(int D, int G, int NB) {
+  const int cb = G * D + 16 * NB;
+  return 1024 + size_t(DA_CONSUMERS) * cb * 4 + size_t(DA_CONSUMERS) * NB * 8 * DA_PROW * 2 +
          2 * DA_MAX_RS * 8 + DA_MAX_RS * 4 + 64;
 }
 
-inline DaPlan da_plan(int D, int G) {
+inline DaPlan da_plan(int D, int G, int NB) {
   DaPlan pl;
   pl.hs = uint32_t(DA_TILE) * D * 2;
-  pl.cb = G * D + 16;
-  const size_t fixed = da_fixed_bytes(D, G);
+  pl.cb = G * D + 16 * NB;
+  const size_t fixed = da_fixed_bytes(D, G, NB);
   int rs = int((DA_SMEM_MAX - fixed) / pl.hs);
   rs = std::min(rs, DA_MAX_RS);
   rs -= rs % DA_PRODUCERS;
@@ -86,6 +92,7 @@ struct DecodeParams {
   __nv_bfloat16* out;
   int ldo;
   int B, Hq, Hkv, G, page;
+  int HB, Gb;       // head blocks per kv head, heads per block (min(G, 8))
   int tps;          // tiles per split
   int max_splits;
   int rs;           // ring slots
@@ -95,11 +102,13 @@ struct DecodeParams {
 };
 
 struct UnitId {
-  int b, kvh, s;
+  int b, kvh, s, hb;
 };
 
 __device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
   UnitId id;
+  id.hb = u % p.HB;
+  u /= p.HB;
   id.s = u % p.max_splits;
   const int bh = u / p.max_splits;
   id.kvh = bh % p.Hkv;
@@ -123,18 +132,19 @@ __device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
 // Consumers: DA_CONSUMERS warps take the unit's tiles round-robin.  The K
 // slot is released as soon as the scores are in registers, the V slot after
 // the P.V product, so a slot is held for one MMA chain, not a whole tile.
-template <int D>
+template <int D, int NB>
 __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParams p) {
   pdl_trigger();
   constexpr int KK = D / 16;
   constexpr uint32_t HS = uint32_t(DA_TILE) * D * 2;
+  constexpr int SO = 8 * NB;  // offset of the l (sum) stats after the m stats
   const int RS = p.rs;
-  const int CB = p.G * D + 16;
+  const int CB = p.Gb * D + 2 * SO;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* cbuf = reinterpret_cast<float*>(ring + size_t(RS) * HS);
   __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * CB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + DA_CONSUMERS * 8 * DA_PROW);
+  uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + DA_CONSUMERS * NB * 8 * DA_PROW);
   uint64_t* empty = full + DA_MAX_RS;
   // Consumers can reach a slot more than one phase ahead of its producer
   // (8 warps round-robin over the ring), where a parity wait would be
@@ -155,13 +165,14 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   __syncthreads();
   pdl_wait();  // q, K/V (incl. the token rope_kv_write just stored), block table
 
-  const int total = p.B * p.Hkv * p.max_splits;
+  const int total = p.B * p.Hkv * p.HB * p.max_splits;
   const int page_tiles = p.page / DA_TILE;
 
   if (warp >= DA_CONSUMERS) {
     // ------------------------------------------------------------ producers
     const int pw = warp - DA_CONSUMERS;
-    const uint64_t pol = l2_policy_evict_first();  // KV is read once per step
+    // KV is read once per step -- unless sibling head blocks re-read it from L2
+    const uint64_t pol = p.HB > 1 ? l2_policy_evict_last() : l2_policy_evict_first();
     int win[DA_WREG], winn[DA_WREG];
     auto fetch = [&](int u, int (&w)[DA_WREG]) -> int {  // returns ctx of unit u
       const UnitId id = unit_of(p, u);
@@ -217,21 +228,26 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   const int g8 = lane >> 2;  // MMA group id
   const int t4 = lane & 3;   // thread in group
   const int mat = lane >> 3;
-  __nv_bfloat16* pw = pbuf + warp * 8 * DA_PROW;
+  __nv_bfloat16* pw = pbuf + warp * NB * 8 * DA_PROW;
   float* cw = cbuf + warp * CB;
   uint32_t hbase = 0;
 
-  auto load_q = [&](int u, uint32_t (&qf)[KK][2], int& ctx) {
+  auto load_q = [&](int u, uint32_t (&qf)[NB][KK][2], int& ctx) {
     const UnitId id = unit_of(p, u);
     ctx = p.ctx_lens[id.b];
-    const bool hv = g8 < p.G;
-    const __nv_bfloat16* qrow = p.q + size_t(id.b) * p.ldq + size_t(id.kvh * p.G + (hv ? g8 : 0)) * D;
 #pragma unroll
-    for (int kk = 0; kk < KK; ++kk) {
-      const uint32_t lo = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4);
-      const uint32_t hi = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4 + 8);
-      qf[kk][0] = hv ? lo : 0u;
-      qf[kk][1] = hv ? hi : 0u;
+    for (int nb = 0; nb < NB; ++nb) {
+      const int hl = nb * 8 + g8;  // head within the unit
+      const bool hv = hl < p.Gb;
+      const __nv_bfloat16* qrow =
+          p.q + size_t(id.b) * p.ldq + size_t(id.kvh * p.G + id.hb * p.Gb + (hv ? hl : 0)) * D;
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk) {
+        const uint32_t lo = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4);
+        const uint32_t hi = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t4 + 8);
+        qf[nb][kk][0] = hv ? lo : 0u;
+        qf[nb][kk][1] = hv ? hi : 0u;
+      }
     }
   };
   auto acquire = [&](uint32_t h) -> uint32_t {
@@ -241,13 +257,13 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     return uint32_t(st);
   };
 
-  uint32_t qcur[KK][2];
+  uint32_t qcur[NB][KK][2];
   int ctx_cur = 0;
   if (blockIdx.x < total) load_q(blockIdx.x, qcur, ctx_cur);
 
   for (int u = blockIdx.x; u < total; u += gridDim.x) {
     const UnitId id = unit_of(p, u);
-    uint32_t qnxt[KK][2];
+    uint32_t qnxt[NB][KK][2];
     int ctx_nxt = 0;
     if (u + int(gridDim.x) < total) load_q(u + gridDim.x, qnxt, ctx_nxt);
     const int ctx = ctx_cur;
@@ -256,11 +272,15 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     const int t1 = min(ntiles, t0 + p.tps);
     if (t0 < t1) {
       const int nt = t1 - t0;
-      float o[KK][4];
+      float o[NB][KK][4];
+      float m0[NB], m1[NB], l0[NB], l1[NB];  // per block: heads 2t4, 2t4+1
 #pragma unroll
-      for (int i = 0; i < KK; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-      float m0 = -INFINITY, m1 = -INFINITY;  // running max for heads 2t4, 2t4+1
-      float l0 = 0.f, l1 = 0.f;              // per-lane partial sums
+      for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+        for (int i = 0; i < KK; ++i) o[nb][i][0] = o[nb][i][1] = o[nb][i][2] = o[nb][i][3] = 0.f;
+        m0[nb] = m1[nb] = -INFINITY;
+        l0[nb] = l1[nb] = 0.f;
+      }
 
       for (int i = warp; i < nt; i += DA_CONSUMERS) {
         const uint32_t hk = hbase + 2 * i;
@@ -275,12 +295,14 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           continue;
         }
 #endif
-        // ---- S^T = K . Q^T : four independent 16-token m tiles
+        // ---- S^T = K . Q^T : four independent 16-token m tiles per column block
         const uint32_t sk = acquire(hk);
         const uint32_t kb = smem_u32(ring + size_t(sk) * HS);
-        float sc[4][4];
+        float sc[NB][4][4];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) sc[nb][mt][0] = sc[nb][mt][1] = sc[nb][mt][2] = sc[nb][mt][3] = 0.f;
 #pragma unroll
         for (int kk = 0; kk < KK; ++kk) {
 #pragma unroll
@@ -289,64 +311,72 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
             const uint32_t c = (kk & 3) * 2 + (mat >> 1);
             uint32_t a[4];
             ldmatrix_x4(kb + (kk >> 2) * DA_BOX_BYTES + sw128(r, c), a[0], a[1], a[2], a[3]);
-            mma_bf16_16816(sc[mt], a, qcur[kk]);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) mma_bf16_16816(sc[nb][mt], a, qcur[nb][kk]);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sk]);  // K tile consumed
         // ---- mask, scale, online softmax
         const int tokbase = (t0 + i) * DA_TILE;
-        float tm0 = -INFINITY, tm1 = -INFINITY;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
+        for (int nb = 0; nb < NB; ++nb) {
+          float tm0 = -INFINITY, tm1 = -INFINITY;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const bool valid = tokbase + mt * 16 + g8 + h * 8 < ctx;
-            sc[mt][2 * h] = valid ? sc[mt][2 * h] * p.scale_log2 : -INFINITY;
-            sc[mt][2 * h + 1] = valid ? sc[mt][2 * h + 1] * p.scale_log2 : -INFINITY;
-            tm0 = fmaxf(tm0, sc[mt][2 * h]);
-            tm1 = fmaxf(tm1, sc[mt][2 * h + 1]);
+          for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const bool valid = tokbase + mt * 16 + g8 + h * 8 < ctx;
+              sc[nb][mt][2 * h] = valid ? sc[nb][mt][2 * h] * p.scale_log2 : -INFINITY;
+              sc[nb][mt][2 * h + 1] = valid ? sc[nb][mt][2 * h + 1] * p.scale_log2 : -INFINITY;
+              tm0 = fmaxf(tm0, sc[nb][mt][2 * h]);
+              tm1 = fmaxf(tm1, sc[nb][mt][2 * h + 1]);
+            }
           }
-        }
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
-          tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
-        }
-        const float n0 = fmaxf(m0, tm0), n1 = fmaxf(m1, tm1);
-        const float a0 = exp2f(m0 - n0), a1 = exp2f(m1 - n1);
-        m0 = n0;
-        m1 = n1;
-        l0 *= a0;
-        l1 *= a1;
+          for (int off = 4; off < 32; off <<= 1) {
+            tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
+            tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
+          }
+          const float n0 = fmaxf(m0[nb], tm0), n1 = fmaxf(m1[nb], tm1);
+          const float a0 = exp2f(m0[nb] - n0), a1 = exp2f(m1[nb] - n1);
+          m0[nb] = n0;
+          m1[nb] = n1;
+          l0[nb] *= a0;
+          l1[nb] *= a1;
 #pragma unroll
-        for (int dm = 0; dm < KK; ++dm) {
-          o[dm][0] *= a0;
-          o[dm][2] *= a0;
-          o[dm][1] *= a1;
-          o[dm][3] *= a1;
-        }
+          for (int dm = 0; dm < KK; ++dm) {
+            o[nb][dm][0] *= a0;
+            o[nb][dm][2] *= a0;
+            o[nb][dm][1] *= a1;
+            o[nb][dm][3] *= a1;
+          }
+          __nv_bfloat16* pwb = pw + nb * 8 * DA_PROW;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
+          for (int mt = 0; mt < 4; ++mt) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float p0 = exp2f(sc[mt][2 * h] - n0);
-            const float p1 = exp2f(sc[mt][2 * h + 1] - n1);
-            l0 += p0;
-            l1 += p1;
-            const int tok = mt * 16 + g8 + h * 8;
-            pw[(2 * t4) * DA_PROW + tok] = __float2bfloat16(p0);
-            pw[(2 * t4 + 1) * DA_PROW + tok] = __float2bfloat16(p1);
+            for (int h = 0; h < 2; ++h) {
+              const float p0 = exp2f(sc[nb][mt][2 * h] - n0);
+              const float p1 = exp2f(sc[nb][mt][2 * h + 1] - n1);
+              l0[nb] += p0;
+              l1[nb] += p1;
+              const int tok = mt * 16 + g8 + h * 8;
+              pwb[(2 * t4) * DA_PROW + tok] = __float2bfloat16(p0);
+              pwb[(2 * t4 + 1) * DA_PROW + tok] = __float2bfloat16(p1);
+            }
           }
         }
         __syncwarp();
         // ---- O^T += V^T . P^T
-        uint32_t pf[4][2];
+        uint32_t pf[NB][4][2];
 #pragma unroll
-        for (int kt = 0; kt < 4; ++kt) {
-          pf[kt][0] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4);
-          pf[kt][1] = *reinterpret_cast<const uint32_t*>(pw + g8 * DA_PROW + kt * 16 + 2 * t4 + 8);
-        }
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int kt = 0; kt < 4; ++kt) {
+            const __nv_bfloat16* pr = pw + (nb * 8 + g8) * DA_PROW + kt * 16 + 2 * t4;
+            pf[nb][kt][0] = *reinterpret_cast<const uint32_t*>(pr);
+            pf[nb][kt][1] = *reinterpret_cast<const uint32_t*>(pr + 8);
+          }
         const uint32_t sv = acquire(hk + 1);
         const uint32_t vb = smem_u32(ring + size_t(sv) * HS);
 #pragma unroll
@@ -357,39 +387,44 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
             const uint32_t c = (dm & 3) * 2 + (mat & 1);
             uint32_t a[4];
             ldmatrix_x4_trans(vb + (dm >> 2) * DA_BOX_BYTES + sw128(r, c), a[0], a[1], a[2], a[3]);
-            mma_bf16_16816(o[dm], a, pf[kt]);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) mma_bf16_16816(o[nb][dm], a, pf[nb][kt]);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sv]);  // V tile consumed
       }
-      // ---- merge the consumer warps' (m, l, O) for the G live heads
+      // ---- merge the consumer warps' (m, l, O) for the Gb live heads
+      const int G = p.Gb;
 #pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
-      }
-      const int G = p.G;
-      const bool h0 = 2 * t4 < G, h1 = 2 * t4 + 1 < G;
+      for (int nb = 0; nb < NB; ++nb) {
 #pragma unroll
-      for (int dm = 0; dm < KK; ++dm) {
-        if (h0) {
-          cw[(2 * t4) * D + dm * 16 + g8] = o[dm][0];
-          cw[(2 * t4) * D + dm * 16 + g8 + 8] = o[dm][2];
+        for (int off = 4; off < 32; off <<= 1) {
+          l0[nb] += __shfl_xor_sync(0xffffffffu, l0[nb], off);
+          l1[nb] += __shfl_xor_sync(0xffffffffu, l1[nb], off);
         }
-        if (h1) {
-          cw[(2 * t4 + 1) * D + dm * 16 + g8] = o[dm][1];
-          cw[(2 * t4 + 1) * D + dm * 16 + g8 + 8] = o[dm][3];
+        const int ha = nb * 8 + 2 * t4, hb2 = ha + 1;
+        const bool h0 = ha < G, h1 = hb2 < G;
+#pragma unroll
+        for (int dm = 0; dm < KK; ++dm) {
+          if (h0) {
+            cw[ha * D + dm * 16 + g8] = o[nb][dm][0];
+            cw[ha * D + dm * 16 + g8 + 8] = o[nb][dm][2];
+          }
+          if (h1) {
+            cw[hb2 * D + dm * 16 + g8] = o[nb][dm][1];
+            cw[hb2 * D + dm * 16 + g8 + 8] = o[nb][dm][3];
+          }
         }
-      }
-      if (g8 == 0) {
-        if (h0) {
-          cw[G * D + 2 * t4] = m0;
-          cw[G * D + 8 + 2 * t4] = l0;
-        }
-        if (h1) {
-          cw[G * D + 2 * t4 + 1] = m1;
-          cw[G * D + 8 + 2 * t4 + 1] = l1;
+        if (g8 == 0) {
+          if (h0) {
+            cw[G * D + ha] = m0[nb];
+            cw[G * D + SO + ha] = l0[nb];
+          }
+          if (h1) {
+            cw[G * D + hb2] = m1[nb];
+            cw[G * D + SO + hb2] = l1[nb];
+          }
         }
       }
       named_bar_sync(1, DA_CONSUMERS * 32);
@@ -405,14 +440,14 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
         for (int w = 0; w < nw; ++w) {
           const float* c = cbuf + w * CB;
           const float f = exp2f(c[G * D + h] - M);
-          L += f * c[G * D + 8 + h];
+          L += f * c[G * D + SO + h];
           const float4 v = *reinterpret_cast<const float4*>(c + h * D + d4);
           acc[0] += f * v.x;
           acc[1] += f * v.y;
           acc[2] += f * v.z;
           acc[3] += f * v.w;
         }
-        const int head = id.kvh * G + h;
+        const int head = id.kvh * p.G + id.hb * G + h;
         if (nsplit == 1) {
           const float inv = 1.f / L;
           uint2 w;
@@ -432,10 +467,12 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
       hbase += 2 * nt;
     }
 #pragma unroll
-    for (int kk = 0; kk < KK; ++kk) {
-      qcur[kk][0] = qnxt[kk][0];
-      qcur[kk][1] = qnxt[kk][1];
-    }
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk) {
+        qcur[nb][kk][0] = qnxt[nb][kk][0];
+        qcur[nb][kk][1] = qnxt[nb][kk][1];
+      }
     ctx_cur = ctx_nxt;
   }
 }
@@ -474,19 +511,19 @@ __global__ void k_decode_combine(const DecodeParams p) {
     *reinterpret_cast<uint32_t*>(dst + j) = pack_bf16(acc[j] * inv, acc[j + 1] * inv);
 }
 
-template <int D>
+template <int D, int NB>
 static int launch_decode(DecodeParams& p, int max_ctas, cudaStream_t st) {
-  const DaPlan pl = da_plan(D, p.G);
+  const DaPlan pl = da_plan(D, p.Gb, NB);
   p.rs = pl.rs;
   static bool attr = false;
   if (!attr) {
-    HP_CUDA_TRY(cudaFuncSetAttribute(k_decode_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_decode_attn<D, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(DA_SMEM_MAX)));
     attr = true;
   }
-  const int units = p.B * p.Hkv * p.max_splits;
-  HP_LAUNCH_PDL("k_decode_attn", k_decode_attn<D>, dim3(std::min(units, max_ctas)), dim3(DA_THREADS), pl.smem,
-                st, p);
+  const int units = p.B * p.Hkv * p.HB * p.max_splits;
+  HP_LAUNCH_PDL("k_decode_attn", k_decode_attn<D, NB>, dim3(std::min(units, max_ctas)), dim3(DA_THREADS),
+                pl.smem, st, p);
   if (p.max_splits > 1) {
     const int warps = p.B * p.Hq;
     HP_LAUNCH_PDL("k_decode_combine", k_decode_combine<D>, dim3((warps + 7) / 8), dim3(256), 0, st, p);
@@ -502,19 +539,27 @@ extern "C" size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits) 
   return size_t(B) * Hq * max_splits * (d + 2) * sizeof(float);
 }
 
-// Split count the launch below picks (1 = no combine kernel).
-static int decode_tps(int B, int Hkv, int max_pages, int page, int max_ctas) {
+// 8-head column blocks per unit: two for 16-head groups at d = 64 (at d = 128
+// the doubled O accumulators would spill; those run as 8-head units).
+static int da_nb(int G, int d) { return (G % 16 == 0 && d == 64) ? 2 : 1; }
+
+// Tiles per split the launch below picks: halve until the units cover the
+// grid ~4x, but keep >= 2 (d = 128) / 4 (d = 64) tiles, i.e. >= 32 KB of
+// K+V, per unit so the unit-end merge stays a small share of its time.
+static int decode_tps(int B, int Hq, int Hkv, int d, int max_pages, int page, int max_ctas) {
   const int max_tiles = max_pages * (page / DA_TILE);
-  const int pairs = B * Hkv;
+  const int G = Hq / Hkv;
+  const int units_per_split = B * Hkv * (G / std::min(G, 8 * da_nb(G, d)));  // x head blocks
+  const int min_tps = d == 64 ? 4 : 2;
   int tps = max_tiles;
-  while (tps > 2 && pairs * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
+  while (tps > min_tps && units_per_split * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
   return std::max(1, std::min(tps, (DA_WIN - 1) * (page / DA_TILE)));  // unit pages fit the window
 }
 
-extern "C" int hp_decode_attn_launches(int B, int Hkv, int max_pages, int page, int max_ctas) {
-  if (B < 1 || Hkv < 1 || max_pages < 1 || page < DA_TILE || max_ctas < 1) return 0;
+extern "C" int hp_decode_attn_launches(int B, int Hq, int Hkv, int d, int max_pages, int page, int max_ctas) {
+  if (B < 1 || Hkv < 1 || Hq % Hkv || max_pages < 1 || page < DA_TILE || max_ctas < 1) return 0;
   const int max_tiles = max_pages * (page / DA_TILE);
-  const int tps = decode_tps(B, Hkv, max_pages, page, max_ctas);
+  const int tps = decode_tps(B, Hq, Hkv, d, max_pages, page, max_ctas);
   return (max_tiles + tps - 1) / tps > 1 ? 2 : 1;
 }
 
@@ -526,7 +571,8 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   HP_CHECK_ARG(q && kcache && vcache && block_table && ctx_lens && out, "hp_decode_attn: null pointer");
   HP_CHECK_ARG(d == 64 || d == 128, "hp_decode_attn: head_dim must be 64 or 128");
   HP_CHECK_ARG(page % DA_TILE == 0 && page >= DA_TILE, "hp_decode_attn: page must be a multiple of 64");
-  HP_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0 && Hq / Hkv <= 8, "hp_decode_attn: GQA group must be <= 8");
+  HP_CHECK_ARG(Hkv >= 1 && Hq % Hkv == 0 && (Hq / Hkv <= 8 || (Hq / Hkv) % 8 == 0),
+               "hp_decode_attn: GQA group must be <= 8 or a multiple of 8");
   HP_CHECK_ARG(B >= 1 && max_pages >= 1 && num_blocks >= 1, "hp_decode_attn: empty batch/cache");
   HP_CHECK_ARG(max_ctas >= 1, "hp_decode_attn: max_ctas must be >= 1");
   HP_CHECK_ARG(ldq % 8 == 0 && ldo % 4 == 0, "hp_decode_attn: misaligned strides");
@@ -544,11 +590,14 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
   p.Hq = Hq;
   p.Hkv = Hkv;
   p.G = Hq / Hkv;
+  const int NB = da_nb(p.G, d);
+  p.Gb = std::min(p.G, 8 * NB);
+  p.HB = p.G / p.Gb;
   p.page = page;
   p.scale_log2 = scale * 1.4426950408889634f;
   // split so that the unit count covers the grid ~4x, at least 2 tiles/unit
   const int max_tiles = max_pages * (page / DA_TILE);
-  p.tps = decode_tps(B, Hkv, max_pages, page, max_ctas);
+  p.tps = decode_tps(B, Hq, Hkv, d, max_pages, page, max_ctas);
   p.max_splits = (max_tiles + p.tps - 1) / p.tps;
   if (p.max_splits > 1) {
     HP_CHECK_ARG(workspace != nullptr, "hp_decode_attn: workspace required for split contexts");
@@ -567,5 +616,6 @@ extern "C" int hp_decode_attn(const void* q, int ldq, const void* kcache, const 
                "hp_decode_attn: caches must be 16B aligned");
   (void)num_blocks;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d == 128 ? launch_decode<128>(p, max_ctas, st) : launch_decode<64>(p, max_ctas, st);
+  if (NB == 2) return launch_decode<64, 2>(p, max_ctas, st);
+  return d == 128 ? launch_decode<128, 1>(p, max_ctas, st) : launch_decode<64, 1>(p, max_ctas, st);
 }

@@ -26,7 +26,7 @@ import torch
 
 from ..workload import ModelSpec
 from . import lib
-from .layer import (PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch,
+from .layer import (PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights, PrefillScratch, mlp_width,
                     decode_slots)
 from .partition import DECODE, PREFILL, PartitionPool, PhaseStreams
 
@@ -143,7 +143,8 @@ class CoRunner:
     def launches_per_decode_step(self, sms: int) -> int:
         """Kernels in one decode layer-step on `sms` SMs (the CUDA graph's nodes)."""
         m = self.model
-        return 8 + lib.decode_attn_launches(self.B, m.num_kv_heads, self.block_table.shape[1], PAGE, sms)
+        return 8 + lib.decode_attn_launches(self.B, m.num_heads, m.num_kv_heads, m.head_dim,
+                                            self.block_table.shape[1], PAGE, sms)
 
     # --------------------------------------------------------------- timing
     def isolated(self, phase: int, sms: int, reps: int = 5) -> float:
@@ -394,9 +395,9 @@ class CoRunner:
     def prefill_flops(self) -> float:
         m = self.model
         h = m.hidden
-        gemm = 2.0 * self.T * h * (m.qkv_out_dim + h + 3 * m.intermediate)
+        gemm = 2.0 * self.T * h * (m.qkv_out_dim + h + 3 * mlp_width(m))
         attn = 2.0 * self.T * self.T * h  # causal: 4 T^2 h / 2
         return gemm + attn
 
     def upgate_flops(self) -> float:
-        return 4.0 * self.T * self.model.intermediate * self.model.hidden
+        return 4.0 * self.T * mlp_width(self.model) * self.model.hidden

@@ -46,6 +46,19 @@ from . import lib
 
 PAGE = 64
 EPS = 1e-5
+
+
+def mlp_width(model: ModelSpec) -> int:
+    """MLP rows materialised on the device.  The reference approximates a
+    sparse MoE by scaling the MLP's weights, FLOPs and intermediate
+    activations by `activated_fraction` (workload.py:26-38, 76-79, 196-209);
+    the device realises that as a dense SwiGLU MLP of width
+    intermediate x activated_fraction, rounded to the 128-row weight tile
+    (moe-a22b: 1228.8 -> 1280).  Dense presets: exactly `intermediate`."""
+    f = model.activated_fraction
+    if f == 1.0:
+        return model.intermediate
+    return max(128, int(round(model.intermediate * f / 128)) * 128)
 ROPE_THETA = 500000.0
 
 
@@ -74,7 +87,7 @@ class LayerWeights:
 
     @classmethod
     def random(cls, model: ModelSpec, device, gen: torch.Generator, std: float = 0.02):
-        h, I = model.hidden, model.intermediate
+        h, I = model.hidden, mlp_width(model)
 
         def w(*shape):
             return (torch.randn(*shape, generator=gen, device="cpu") * std).to(torch.bfloat16).to(device)
@@ -89,7 +102,7 @@ class LayerWeights:
     def random_device(cls, model: ModelSpec, device, gen: torch.Generator, std: float = 0.02):
         """Random weights drawn on the GPU (a 32-layer model's 14 GB would take
         minutes through the host generator)."""
-        h, I = model.hidden, model.intermediate
+        h, I = model.hidden, mlp_width(model)
 
         def w(*shape):
             return (torch.randn(*shape, generator=gen, device=device) * std).to(torch.bfloat16)
@@ -144,14 +157,14 @@ class PrefillScratch:
         self.qkv = torch.empty(max_tokens, model.qkv_out_dim, **bf)
         self.attn = torch.empty(max_tokens, h, **bf)
         self.h = torch.empty(max_tokens, h, **bf)
-        self.act = torch.empty(max_tokens, model.intermediate, **bf)
+        self.act = torch.empty(max_tokens, mlp_width(model), **bf)
 
 
 class DecodeScratch:
     """Activation buffers + stream-K workspaces for a decode batch of <= max_batch."""
 
     def __init__(self, model: ModelSpec, max_batch: int, max_pages: int, device, max_ctas: int = 148):
-        h, I = model.hidden, model.intermediate
+        h, I = model.hidden, mlp_width(model)
         bf = dict(dtype=torch.bfloat16, device=device)
         self.max_batch = max_batch
         self.xn = torch.empty(max_batch, h, **bf)
@@ -249,7 +262,7 @@ class DeviceLayer:
                       stream=stream)
         lib.gemm_swap(sc.act[:B], self.W.w_down, y, ws, cnt, lib.EPI_RESID, resid=sc.h[:B],
                       max_ctas=sms, stream=stream)
-        return 8 + lib.decode_attn_launches(B, Hkv, block_table.shape[1], cache.page, sms)
+        return 8 + lib.decode_attn_launches(B, Hq, Hkv, d, block_table.shape[1], cache.page, sms)
 
 
     # --------------------------------------------------------------- hybrid

@@ -53,7 +53,7 @@ SIGNATURES = {
     "hp_prefill_attn_paged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _i, _i, _i, _f,
                                    _i, _p]),
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
-    "hp_decode_attn_launches": (_i, [_i, _i, _i, _i, _i]),
+    "hp_decode_attn_launches": (_i, [_i, _i, _i, _i, _i, _i, _i]),
     "hp_decode_attn": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _f, _p, _sz, _i, _p]),
     "hp_probe": (_i, [_i, _i, _i64, _p, _p]),
     "hp_membw": (_i, [_p, _sz, _i, _i, _p, _p]),
@@ -269,8 +269,8 @@ def prefill_attn_paged(q, kcache, vcache, block_table, cu_seqlens, prior_lens, n
           "hp_prefill_attn_paged")
 
 
-def decode_attn_launches(B: int, Hkv: int, max_pages: int, page: int, max_ctas: int) -> int:
-    return load().hp_decode_attn_launches(B, Hkv, max_pages, page, max_ctas)
+def decode_attn_launches(B: int, Hq: int, Hkv: int, d: int, max_pages: int, page: int, max_ctas: int) -> int:
+    return load().hp_decode_attn_launches(B, Hq, Hkv, d, max_pages, page, max_ctas)
 
 
 def decode_attn_ws_bytes(B: int, Hq: int, d: int, max_splits: int) -> int:

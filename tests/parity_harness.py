@@ -195,19 +195,21 @@ def run_tiny(seed: int = 0, decode_steps: int = 16, device: int = 0) -> dict:
     return out
 
 
-def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, device: int = 0) -> dict:
-    """Config-2 numerics at a CPU-affordable size: one Llama-3-8B layer,
-    prefill of T tokens and one decode step for B sequences of context ctx,
-    device vs oracle."""
+def run_llama_layer(T: int = 512, B: int = 8, ctx: int = 300, seed: int = 0, device: int = 0,
+                    model: str = "llama3-8b") -> dict:
+    """Config-2 numerics at a CPU-affordable size: one layer of a reference
+    preset (default Llama-3-8B; moe-a22b at its activated MLP width), prefill
+    of T tokens and one decode step for B sequences of context ctx, device vs
+    oracle."""
     import torch
 
     from paper_2504_19516_b200.device.layer import (DecodeScratch, DeviceLayer, KVCache,
-                                                    LayerWeights, PrefillScratch, decode_slots)
+                                                    LayerWeights, PrefillScratch, decode_slots, mlp_width)
     from paper_2504_19516_b200.workload import MODEL_PRESETS
 
-    m = MODEL_PRESETS["llama3-8b"]
+    m = MODEL_PRESETS[model]
     rng = np.random.default_rng(seed)
-    h, I, d, Hq, Hkv = m.hidden, m.intermediate, m.head_dim, m.num_heads, m.num_kv_heads
+    h, I, d, Hq, Hkv = m.hidden, mlp_width(m), m.head_dim, m.num_heads, m.num_kv_heads
     W = O.LayerWeights(_bf(rng.normal(0, 0.02, (m.qkv_out_dim, h))), _bf(rng.normal(0, 0.02, (h, h))),
                        _bf(rng.normal(0, 0.02, (I, h))), _bf(rng.normal(0, 0.02, (I, h))),
                        _bf(rng.normal(0, 0.02, (h, I))), _bf(1 + 0.1 * rng.normal(size=h)),

@@ -80,6 +80,18 @@ def test_gemm_tile_planner_is_host_side():
 
 def test_decode_attention_launch_count_is_host_side():
     # one launch while the context is not split, a combine launch otherwise
-    assert lib.decode_attn_launches(32, 8, 32, 64, 8) == 1
-    assert lib.decode_attn_launches(32, 8, 32, 64, 148) == 2
-    assert lib.decode_attn_launches(0, 8, 32, 64, 148) == 0
+    assert lib.decode_attn_launches(32, 32, 8, 128, 32, 64, 8) == 1
+    assert lib.decode_attn_launches(32, 32, 8, 128, 32, 64, 148) == 2
+    assert lib.decode_attn_launches(0, 32, 8, 128, 32, 64, 148) == 0
+    assert lib.decode_attn_launches(32, 64, 4, 64, 32, 64, 148) == 2  # moe-a22b: 2 head blocks
+    assert lib.decode_attn_launches(1, 8, 1, 64, 4, 64, 148) == 1     # 4 tiles: one split of >= 4
+
+
+def test_mlp_width_realises_activated_fraction():
+    from paper_2504_19516_b200.device.layer import mlp_width
+    from paper_2504_19516_b200.workload import MODEL_PRESETS, ModelSpec
+
+    assert mlp_width(MODEL_PRESETS["llama3-8b"]) == 14336
+    assert mlp_width(MODEL_PRESETS["moe-a22b"]) == 1280  # 0.1 x 12288, rounded to the 128-row tile
+    assert mlp_width(ModelSpec("m", 1, 4096, 32, 8, 128, 14336, activated_fraction=0.5)) == 7168
+    assert mlp_width(ModelSpec("m", 1, 4096, 32, 8, 128, 1024, activated_fraction=0.01)) == 128

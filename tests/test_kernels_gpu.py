@@ -196,7 +196,7 @@ def attn_ref(q, k, v, causal, scale):
 
 @pytest.mark.parametrize("lens,Hq,Hkv,d", [([128], 4, 1, 128), ([1000], 8, 2, 128),
                                            ([64, 130, 7], 4, 4, 128), ([2048], 32, 8, 128),
-                                           ([1024], 4, 2, 64), ([5, 300], 4, 2, 64)])
+                                           ([1024], 4, 2, 64), ([5, 300], 4, 2, 64), ([700], 64, 4, 64)])
 def test_prefill_attn(lens, Hq, Hkv, d, gen):
     T = sum(lens)
     qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
@@ -233,7 +233,10 @@ def make_cache(B, ctx, Hkv, d, page, gen, extra_blocks=3):
 @pytest.mark.parametrize("ctx,Hq,Hkv,d", [([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2, 128),
                                           ([2048] * 32, 32, 8, 128), ([1], 8, 1, 128),
                                           ([5000, 33], 64, 8, 128), ([3000] * 3, 32, 8, 128),
-                                          ([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2, 64)])
+                                          ([17, 64, 128, 255, 256, 511, 512, 1000], 4, 2, 64),
+                                          # GQA 16 (moe-a22b: 64 q / 4 kv heads, d 64) and 24: head blocks
+                                          ([2048] * 4 + [100, 7], 64, 4, 64), ([700, 1], 48, 2, 128),
+                                          ([300, 64], 32, 1, 64), ([500], 32, 2, 128)])
 @pytest.mark.parametrize("max_ctas", [8, 148])
 @pytest.mark.parametrize("page", [64, 256])
 def test_decode_attn(ctx, Hq, Hkv, d, max_ctas, page, gen):

@@ -40,6 +40,15 @@ def test_llama3_8b_layer_ragged_prefill_tail():
     assert r["decode_excess"] <= ATOL, r
 
 
+def test_moe_a22b_layer_activated_width():
+    # reference MoE preset (workload.py:76-79): 64 q / 4 kv heads of dim 64
+    # (GQA 16 -> decode attention head blocks), MLP at 0.1 x 12288 -> 1280 rows
+    r = run_llama_layer(T=300, B=5, ctx=200, seed=9, model="moe-a22b")
+    assert r["prefill_excess"] <= ATOL, r
+    assert r["decode_excess"] <= ATOL, r
+    assert r["kv_write_max_abs"] <= 2e-2, r
+
+
 @pytest.mark.parametrize("budget", [512, 200])
 def test_tiny_model_chunked_prefill_hybrid_batches(budget):
     # lockstep hybrid batches (chunks with cached prefixes + decode rows),
