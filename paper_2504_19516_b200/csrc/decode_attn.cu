@@ -34,6 +34,7 @@
 #include "../../include/hp.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 namespace hp {
@@ -543,16 +544,26 @@ extern "C" size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits) 
 // the doubled O accumulators would spill; those run as 8-head units).
 static int da_nb(int G, int d) { return (G % 16 == 0 && d == 64) ? 2 : 1; }
 
-// Tiles per split the launch below picks: halve until the units cover the
-// grid ~4x, but keep >= 2 (d = 128) / 4 (d = 64) tiles, i.e. >= 32 KB of
-// K+V, per unit so the unit-end merge stays a small share of its time.
+// Tiles per split the launch below picks.  Every unit costs ~2 us of
+// fixed work (merge, drain, the combine pass when split), and a lone SM
+// streams ~100 GB/s, so: as few splits as keep >= max_ctas / 2 units
+// (enough streaming SMs to saturate HBM), never below 2 (d = 128) / 4
+// (d = 64) tiles per unit.  Measured (profiles/r01_decode_attn_tps.txt):
+// B=32 ctx 2048 on 148 SMs, no split 44.8 us vs 52.6 at 8 tiles per unit.
 static int decode_tps(int B, int Hq, int Hkv, int d, int max_pages, int page, int max_ctas) {
   const int max_tiles = max_pages * (page / DA_TILE);
   const int G = Hq / Hkv;
   const int units_per_split = B * Hkv * (G / std::min(G, 8 * da_nb(G, d)));  // x head blocks
   const int min_tps = d == 64 ? 4 : 2;
-  int tps = max_tiles;
-  while (tps > min_tps && units_per_split * ((max_tiles + tps - 1) / tps) < 4 * max_ctas) tps = (tps + 1) / 2;
+  static const int forced = [] {  // HP_DA_TPS=n: fixed tiles per split (measurement)
+    const char* e = std::getenv("HP_DA_TPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return std::max(1, std::min({forced, max_tiles, (DA_WIN - 1) * (page / DA_TILE)}));
+  int splits = 1;
+  while (long(units_per_split) * splits < max_ctas / 2 && (max_tiles + 2 * splits - 1) / (2 * splits) >= min_tps)
+    splits *= 2;
+  const int tps = (max_tiles + splits - 1) / splits;
   return std::max(1, std::min(tps, (DA_WIN - 1) * (page / DA_TILE)));  // unit pages fit the window
 }
 

@@ -81,9 +81,10 @@ def test_gemm_tile_planner_is_host_side():
 def test_decode_attention_launch_count_is_host_side():
     # one launch while the context is not split, a combine launch otherwise
     assert lib.decode_attn_launches(32, 32, 8, 128, 32, 64, 8) == 1
-    assert lib.decode_attn_launches(32, 32, 8, 128, 32, 64, 148) == 2
+    assert lib.decode_attn_launches(32, 32, 8, 128, 32, 64, 148) == 1  # 256 units >= 148 / 2: no split
+    assert lib.decode_attn_launches(4, 32, 8, 128, 32, 64, 148) == 2   # 32 units: split + combine
     assert lib.decode_attn_launches(0, 32, 8, 128, 32, 64, 148) == 0
-    assert lib.decode_attn_launches(32, 64, 4, 64, 32, 64, 148) == 2  # moe-a22b: 2 head blocks
+    assert lib.decode_attn_launches(32, 64, 4, 64, 32, 64, 148) == 1  # moe-a22b: 128 units
     assert lib.decode_attn_launches(1, 8, 1, 64, 4, 64, 148) == 1     # 4 tiles: one split of >= 4
 
 
