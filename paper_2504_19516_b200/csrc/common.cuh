@@ -44,6 +44,17 @@ HP_DEVICE uint64_t globaltimer() {
   return r;
 }
 
+// Volatile shared-memory word access by shared-window address (a generic
+// volatile pointer compiles to a slow LD.E.STRONG.SYS).
+HP_DEVICE uint32_t ld_volatile_shared(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+HP_DEVICE void st_volatile_shared(uint32_t addr, uint32_t v) {
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // System-scope release/acquire on a flag another GPU (or process) reads/writes.
 HP_DEVICE void st_release_sys(int* p, int v) {
   asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

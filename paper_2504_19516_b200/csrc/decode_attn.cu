@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   // (8 warps round-robin over the ring), where a parity wait would be
   // ambiguous: they first wait until the slot's tag names their half-tile
   // (written once the producer passed the slot's empty barrier for it).
-  volatile uint32_t* tag = reinterpret_cast<volatile uint32_t*>(empty + DA_MAX_RS);
+  const uint32_t tag = smem_u32(empty + DA_MAX_RS);  // u32 [DA_MAX_RS], volatile shared accesses
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     for (int s = 0; s < RS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      tag[s] = 0xffffffffu;
+      st_volatile_shared(tag + 4u * s, 0xffffffffu);
     }
     fence_barrier_init();
   }
@@ -202,9 +202,14 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
            hh += DA_PRODUCERS) {
         const int t = t0 + (hh >> 1);
         const int pr = t / page_tiles - first;
+        // register select in opaque selp's (a plain select chain becomes an
+        // indexed local-memory load of the whole window)
         int sel = win[0];
+        const int wi = pr >> 5;
 #pragma unroll
-        for (int r = 1; r < DA_WREG; ++r) sel = (pr >> 5) == r ? win[r] : sel;
+        for (int r = 1; r < DA_WREG; ++r)
+          asm("{\n .reg .pred p;\n setp.eq.s32 p, %2, %3;\n selp.b32 %0, %1, %0, p;\n}"
+              : "+r"(sel) : "r"(win[r]), "r"(wi), "r"(r));
         const int blk = __shfl_sync(0xffffffffu, sel, pr & 31);
         const uint32_t h = hbase + hh;
         const int st = int(h % RS);
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           const size_t tile = ((size_t(blk) * p.Hkv + id.kvh) * page_tiles + (t % page_tiles)) * HS;
           mbar_arrive_expect_tx(&full[st], HS);
           bulk_load_hint(ring + size_t(st) * HS, ((hh & 1) ? p.vc : p.kc) + tile, HS, &full[st], pol);
-          tag[st] = h;
+          st_volatile_shared(tag + 4u * st, h);
         }
         __syncwarp();
       }
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   };
   auto acquire = [&](uint32_t h) -> uint32_t {
     const int st = int(h % RS);
-    while (tag[st] != h) __nanosleep(20);
+    while (ld_volatile_shared(tag + 4u * st) != h) __nanosleep(20);
     mbar_wait(&full[st], (h / RS) & 1);
     return uint32_t(st);
   };
