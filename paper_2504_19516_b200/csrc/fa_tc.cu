@@ -120,9 +120,12 @@ __device__ __forceinline__ const __nv_bfloat16* page_tile(const FaParams& p, con
 // tcgen05 ops of one issuing thread execute in order, which is what makes
 // QK_X(j+1) overwriting S_X/P_X after PV_X(j) safe and makes O_X stable
 // whenever s_full_X fires (rescale point).
-// Warps: 0 producer, 1 TMEM alloc + MMA issuer, 2-5 softmax A, 6-9 softmax B.
+// Warps: 0 producer, 1 TMEM alloc + MMA issuer, 2-3 idle (warpgroup 0 gives
+// registers away: setmaxnreg 96), 4-7 softmax A, 8-11 softmax B
+// (setmaxnreg 200: the 128-score row stays in registers without spills).
 // TMEM: S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [256+D, 256+2D).
-constexpr int FA2_THREADS = 320;
+constexpr int FA2_THREADS = 384;
+constexpr int FA2_SOFTMAX_WARP0 = 4;
 
 template <int D>
 struct Fa2Cfg {
@@ -228,7 +231,9 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
   pdl_wait();  // qkv from the QKV GEMM / rope_kv_write; `out` may still be read upstream
   const uint32_t tmem = *tmem_slot;
   const int total = p.nseq * p.n_qt * p.Hq;
-
+  // per SM sub-partition: one warp of each warpgroup, 96 + 200 + 200 <= 3 x 168 (the pool the launch got)
+  if (warp < FA2_SOFTMAX_WARP0) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -356,9 +361,11 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
         ++un;
       }
     }
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
     // ------------------------------------------------------------- softmax
-    const int t = (warp - 2) >> 2;          // tile 0 (A) or 1 (B)
+    const int t = (warp - FA2_SOFTMAX_WARP0) >> 2;  // tile 0 (A) or 1 (B)
     const int q4 = warp & 3;                // TMEM lane quarter
     const int row = q4 * 32 + lane;
     const uint32_t lane_base = uint32_t(q4 * 32) << 16;
