@@ -16,13 +16,16 @@ if which.startswith("swap"):
     T, N, K = 32, 4096, 4096
     if which == "swap_qkv":
         N = 6144
+    epi = lib.EPI_STORE
+    if which == "swap_ug":  # mlp_up_gate, the largest decode GEMM (235 MB of weights)
+        N, epi = 28672, lib.EPI_SILU
     x = torch.randn(T, K, device=DEV).to(torch.bfloat16)
     w = lib.tile_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
     ws = torch.empty(lib.gemm_swap_ws_bytes(T, N, K, sms) // 4, device=DEV)
     cnt = torch.zeros(N // 128, device=DEV, dtype=torch.int32)
     for _ in range(reps):
-        lib.gemm_swap(x, w, y, ws, cnt, lib.EPI_STORE, max_ctas=sms)
+        lib.gemm_swap(x, w, y, ws, cnt, epi, max_ctas=sms)
 elif which == "decode_attn":
     B, ctx, Hq, Hkv, d, page = 32, 2048, 32, 8, 128, 64
     pages = ctx // page
