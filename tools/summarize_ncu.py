@@ -62,11 +62,14 @@ def full(path, out, flops=None):
         unit = units[hdr.index("gpu__time_duration.sum")]
         sec = t * (1e-9 if unit in ("ns", "nsecond") else 1e-6 if unit in ("us", "usecond") else 1e-3)
         txt += f"\nalgorithmic FLOP per launch {float(flops):.4g} -> {float(flops) / sec / 1e12:.1f} TFLOP/s under ncu\n"
-    rd = float(res.get("dram__bytes_read.sum", ["0"])[0].replace(",", ""))
-    wr = float(res.get("dram__bytes_write.sum", ["0"])[0].replace(",", ""))
-    u_rd = units[hdr.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in hdr else "byte"
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u_rd, 1)
-    traffic = (rd + wr) * scale
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def nbytes(k):  # each metric carries its own unit
+        if k not in hdr:
+            return 0.0
+        return float(res[k][0].replace(",", "")) * scale.get(units[hdr.index(k)], 1)
+
+    traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
     txt += f"\nDRAM traffic per launch (read+write): {traffic:.4g} bytes\n"
     open(out, "w").write(txt)
     print(txt)
