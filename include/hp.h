@@ -134,27 +134,33 @@ int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ld
 /* Fused row-parallel GEMM + all-reduce for tensor-parallel decode (config 5,
  * SURVEY.md §8(f)#4; replaces the NCCL all-reduce after o_proj / mlp_down of
  * a Megatron row-parallel layer).  Symmetric buffers: every
- * rank r owns recv_r = bf16 [2][world][T][N] and flags_r = int [2][world][tiles]
- * (tiles = hp_peer_tiles(T, N); flags zero at allocation) and maps every
- * peer's pair (hp_ipc_*).  Call e (epoch e >= 1, +1 per call, all ranks in
- * step) uses half (e & 1) of each buffer:
+ * rank r owns recv_r = bf16 [2][world][T_max][N] and flags_r = int
+ * [2][world][tiles_max] (tiles = hp_peer_tiles(T, N); flags zero at
+ * allocation) and maps every peer's pair (hp_ipc_*).  Call e (epoch e >= 1,
+ * +1 per call, all ranks in step) uses half (e & 1) of each buffer, i.e.
+ * base + (e & 1) * {recv,flags}_half_elems:
  *   hp_gemm_swap_peer: the swap-AB GEMM's epilogue writes this rank's partial
  *     tile straight into slot `rank` of every peer's recv over NVLink, then
- *     raises flags_q[rank][tile] = epoch (system-scope release) -- the
- *     transfer of tile i overlaps the MMA of tile i+1;
- *   hp_peer_reduce: per output tile, wait for every rank's flag >= epoch and
+ *     raises flags_q[rank][tile] = e (system-scope release) -- the transfer of
+ *     tile i overlaps the MMA of tile i+1;
+ *   hp_peer_reduce: per output tile, wait for every rank's flag >= e and
  *     write out = sum_r recv[r] + resid (fp32 sum, bf16 out, rank order).
- * peer_recv / peer_flags: the world pointers of half (e & 1), indexed by rank.
- * Double buffering makes back-to-back calls safe: a rank can reach epoch
- * e + 2 only after every rank's partial for e + 1, i.e. after they all left
- * epoch e's reduce. */
+ * peer_recv / peer_flags: the `world` base pointers, indexed by rank.  Epochs
+ * come from the host (`epoch`) or, with epoch_dev != NULL, from the device:
+ * e = *epoch_dev + 1, and the reduce's last block advances *epoch_dev (`done`:
+ * an int that is zero before the first call) -- the form a CUDA graph can
+ * replay.  Double buffering makes back-to-back calls safe: a rank can reach
+ * epoch e + 2 only after every rank's partial for e + 1, i.e. after they all
+ * left epoch e's reduce. */
 int hp_peer_tiles(int T, int N);
 int hp_gemm_swap_peer(const void* X, int ldx, const void* W, int ldw, int T, int N, int K,
-                      void* const* peer_recv, int* const* peer_flags, int world, int rank, int epoch,
+                      void* const* peer_recv, size_t recv_half_elems, int* const* peer_flags,
+                      size_t flags_half_elems, int world, int rank, int epoch, const int* epoch_dev,
                       void* workspace, size_t ws_bytes, int* counters, int n_counters, int max_ctas,
                       void* stream);
-int hp_peer_reduce(const void* recv, const int* flags, int world, int T, int N, int epoch,
-                   const void* resid, int ldr, void* out, int ldo, void* stream);
+int hp_peer_reduce(const void* recv, size_t recv_half_elems, const int* flags, size_t flags_half_elems,
+                   int world, int T, int N, int epoch, int* epoch_dev, int* done, const void* resid,
+                   int ldr, void* out, int ldo, void* stream);
 /* CUDA IPC for the symmetric buffers: export the handle (HP_IPC_HANDLE_BYTES
  * opaque bytes) of the allocation block holding dev_ptr plus dev_ptr's
  * offset in it; a peer maps the block (hp_ipc_open -> base; its pointer is

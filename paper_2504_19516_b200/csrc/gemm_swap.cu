@@ -72,9 +72,13 @@ struct SwapParams {
   unsigned long long* trace;  // optional [grid][6] globaltimer stamps (hp_set_trace; development aid)
   // HP_EPI_PEER (row-parallel layers under tensor parallelism): the partial
   // tile goes to slot `rank` of every rank's receive buffer [world][T][N]
-  // over peer memory, then flag [rank][tile] := epoch is raised on every rank
+  // over peer memory, then flag [rank][tile] := epoch is raised on every rank.
+  // Buffers are double: half (epoch & 1) at base + half * half_{out,flags};
+  // epoch = *epoch_dev + 1 when epoch_dev is set (graph-replayable), else `epoch`.
   __nv_bfloat16* peer_out[HP_MAX_PEERS];
   int* peer_flags[HP_MAX_PEERS];
+  size_t half_out, half_flags;
+  const int* epoch_dev;
   int world, rank, epoch;
 };
 
@@ -118,7 +122,7 @@ __device__ __forceinline__ void epi_sync() { named_bar_sync(1, 128); }
 // offset c0..c0+31) to the output.  et: 0..127 epilogue thread index.
 template <int BN>
 __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, int mt, int nt,
-                                           int c0, int et) {
+                                           int c0, int et, int ep) {
   const int lane = et & 31, w = et >> 5;
   if (p.epi == HP_EPI_SILU) {
     // 64 outputs per tile: feature r (gate) pairs with r + 64 (up)
@@ -141,7 +145,7 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
         const float* c = V + (g * 8) * VLD + j;
         const uint4 v = make_uint4(pack_bf16(c[0], c[VLD]), pack_bf16(c[2 * VLD], c[3 * VLD]),
                                    pack_bf16(c[4 * VLD], c[5 * VLD]), pack_bf16(c[6 * VLD], c[7 * VLD]));
-        const size_t off = (size_t(p.rank) * p.T + t) * p.N + mt * SBM + g * 8;
+        const size_t off = (ep & 1) * p.half_out + (size_t(p.rank) * p.T + t) * p.N + mt * SBM + g * 8;
         for (int q = 0; q < p.world; ++q) *reinterpret_cast<uint4*>(p.peer_out[q] + off) = v;
       }
     }
@@ -301,15 +305,17 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int et = (warp - SW_MMA - 1) * 32 + lane;
-    // HP_EPI_PEER: once the whole tile sits in every rank's receive buffer,
-    // publish it with a system-scope release on every rank's flag array
+    // HP_EPI_PEER: this call's epoch (after pdl_wait: the previous reduce
+    // advanced *epoch_dev); once the whole tile sits in every rank's receive
+    // buffer, publish it with a system-scope release on every rank's flags
+    const int ep = p.epi != HP_EPI_PEER ? 0 : (p.epoch_dev ? *p.epoch_dev + 1 : p.epoch);
     auto publish = [&](int tile) {
       if (p.epi != HP_EPI_PEER) return;
       epi_sync();
       if (et == 0) {
         __threadfence_system();
-        for (int r = 0; r < p.world; ++r)
-          st_release_sys(p.peer_flags[r] + size_t(p.rank) * (p.m_tiles * p.n_tiles) + tile, p.epoch);
+        const size_t f = (ep & 1) * p.half_flags + size_t(p.rank) * (p.m_tiles * p.n_tiles) + tile;
+        for (int r = 0; r < p.world; ++r) st_release_sys(p.peer_flags[r] + f, ep);
       }
     };
     int acc = 0;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) V[row * VLD + j] = v[j];
           epi_sync();
-          emit_chunk<BN>(p, V, mt, nt, c * 32, et);
+          emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
         }
         publish(s.tile);
       } else {
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
               V[r * VLD + cc + 3] = a[i].w;
             }
             epi_sync();
-            emit_chunk<BN>(p, V, mt, nt, c * 32, et);
+            emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
           }
           if (et == 0) p.counters[s.tile] = 0;
           publish(s.tile);
@@ -466,46 +472,71 @@ extern "C" size_t hp_gemm_swap_ws_bytes(int T, int N, int K, int max_ctas) {
 
 // Receive side of the fused tensor-parallel all-reduce.  Block = 16 tokens x
 // one 128-feature tile column (thread: 8 features, 16-byte loads); it waits
-// until every rank published the tile for `epoch`, then writes
-// out = sum over ranks (rank order, fp32) + resid.
-__global__ void __launch_bounds__(256) k_peer_reduce(const __nv_bfloat16* __restrict__ recv, const int* flags,
-                                                     int world, int T, int N, int m_tiles, int bn, int epoch,
+// until every rank published the tile for this call's epoch, then writes
+// out = sum over ranks (rank order, fp32) + resid.  With epoch_dev, the last
+// block to finish advances *epoch_dev (every block read it before).
+__global__ void __launch_bounds__(256) k_peer_reduce(const __nv_bfloat16* __restrict__ recv, size_t half_recv,
+                                                     const int* flags, size_t half_flags, int world, int T, int N,
+                                                     int m_tiles, int bn, int epoch, int* epoch_dev, int* done,
                                                      const __nv_bfloat16* __restrict__ resid, int ldr,
                                                      __nv_bfloat16* __restrict__ out, int ldo) {
   pdl_trigger();
   pdl_wait();
+  const int ep = epoch_dev ? *reinterpret_cast<volatile int*>(epoch_dev) + 1 : epoch;
+  recv += (ep & 1) * half_recv;
+  flags += (ep & 1) * half_flags;
   const int mt = blockIdx.x, t0 = blockIdx.y * 16;
   const int tile = (t0 / bn) * m_tiles + mt;
   const int ntiles = m_tiles * ((T + bn - 1) / bn);
   if (threadIdx.x < world) {
     const int* f = flags + size_t(threadIdx.x) * ntiles + tile;
-    while (ld_acquire_sys(f) < epoch) __nanosleep(32);
+    while (ld_acquire_sys(f) < ep) __nanosleep(32);
   }
   __syncthreads();
   const int t = t0 + (threadIdx.x >> 4);
-  if (t >= T) return;
-  const int o = mt * SBM + (threadIdx.x & 15) * 8;
-  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  auto add = [&](uint4 v) {
-    a[0] += bf16lo(v.x); a[1] += bf16hi(v.x); a[2] += bf16lo(v.y); a[3] += bf16hi(v.y);
-    a[4] += bf16lo(v.z); a[5] += bf16hi(v.z); a[6] += bf16lo(v.w); a[7] += bf16hi(v.w);
-  };
-  uint4 v[HP_MAX_PEERS];
+  if (t < T) {
+    const int o = mt * SBM + (threadIdx.x & 15) * 8;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    auto add = [&](uint4 v) {
+      a[0] += bf16lo(v.x); a[1] += bf16hi(v.x); a[2] += bf16lo(v.y); a[3] += bf16hi(v.y);
+      a[4] += bf16lo(v.z); a[5] += bf16hi(v.z); a[6] += bf16lo(v.w); a[7] += bf16hi(v.w);
+    };
+    uint4 v[HP_MAX_PEERS];
 #pragma unroll
-  for (int r = 0; r < HP_MAX_PEERS; ++r)
-    if (r < world) v[r] = __ldcg(reinterpret_cast<const uint4*>(recv + (size_t(r) * T + t) * N + o));
+    for (int r = 0; r < HP_MAX_PEERS; ++r)
+      if (r < world) v[r] = __ldcg(reinterpret_cast<const uint4*>(recv + (size_t(r) * T + t) * N + o));
 #pragma unroll
-  for (int r = 0; r < HP_MAX_PEERS; ++r)
-    if (r < world) add(v[r]);
-  if (resid) add(*reinterpret_cast<const uint4*>(resid + size_t(t) * ldr + o));
-  *reinterpret_cast<uint4*>(out + size_t(t) * ldo + o) =
-      make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+    for (int r = 0; r < HP_MAX_PEERS; ++r)
+      if (r < world) add(v[r]);
+    if (resid) add(*reinterpret_cast<const uint4*>(resid + size_t(t) * ldr + o));
+    *reinterpret_cast<uint4*>(out + size_t(t) * ldo + o) =
+        make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+  }
+  if (epoch_dev) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int nblk = int(gridDim.x * gridDim.y);
+      if (atomicAdd(done, 1) == nblk - 1) {
+        *done = 0;
+        __threadfence();
+        atomicAdd(epoch_dev, 1);
+      }
+    }
+  }
 }
+
+struct PeerArgs {
+  void* const* recv;
+  size_t half_recv;
+  int* const* flags;
+  size_t half_flags;
+  int world, rank, epoch;
+  const int* epoch_dev;
+};
 
 static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
                           int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes, int* counters,
-                          int n_counters, int max_ctas, void* stream, void* const* peer_recv,
-                          int* const* peer_flags, int world, int rank, int epoch);
+                          int n_counters, int max_ctas, void* stream, const PeerArgs* peer);
 
 extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                             const void* R, int ldr, int T, int N, int K, int epilogue,
@@ -514,32 +545,36 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
   HP_CHECK_ARG(Y, "hp_gemm_swap: null pointer");
   HP_CHECK_ARG(epilogue >= HP_EPI_STORE && epilogue <= HP_EPI_SILU, "hp_gemm_swap: bad epilogue");
   return gemm_swap_impl(X, ldx, W, ldw, Y, ldy, R, ldr, T, N, K, epilogue, workspace, ws_bytes, counters,
-                        n_counters, max_ctas, stream, nullptr, nullptr, 0, 0, 0);
+                        n_counters, max_ctas, stream, nullptr);
 }
 
 extern "C" int hp_gemm_swap_peer(const void* X, int ldx, const void* W, int ldw, int T, int N, int K,
-                                 void* const* peer_recv, int* const* peer_flags, int world, int rank, int epoch,
+                                 void* const* peer_recv, size_t recv_half_elems, int* const* peer_flags,
+                                 size_t flags_half_elems, int world, int rank, int epoch, const int* epoch_dev,
                                  void* workspace, size_t ws_bytes, int* counters, int n_counters, int max_ctas,
                                  void* stream) {
   HP_CHECK_ARG(peer_recv && peer_flags && world >= 1 && world <= HP_MAX_PEERS && rank >= 0 && rank < world,
                "hp_gemm_swap_peer: bad peer arguments");
-  HP_CHECK_ARG(epoch >= 1, "hp_gemm_swap_peer: epoch must be >= 1 and increase per call");
+  HP_CHECK_ARG(epoch_dev || epoch >= 1, "hp_gemm_swap_peer: host epochs start at 1 and increase per call");
   for (int q = 0; q < world; ++q)
     HP_CHECK_ARG(peer_recv[q] && peer_flags[q], "hp_gemm_swap_peer: null peer buffer");
+  const PeerArgs pa{peer_recv, recv_half_elems, peer_flags, flags_half_elems, world, rank, epoch, epoch_dev};
   return gemm_swap_impl(X, ldx, W, ldw, nullptr, 0, nullptr, 0, T, N, K, HP_EPI_PEER, workspace, ws_bytes,
-                        counters, n_counters, max_ctas, stream, peer_recv, peer_flags, world, rank, epoch);
+                        counters, n_counters, max_ctas, stream, &pa);
 }
 
-extern "C" int hp_peer_reduce(const void* recv, const int* flags, int world, int T, int N, int epoch,
-                              const void* resid, int ldr, void* out, int ldo, void* stream) {
+extern "C" int hp_peer_reduce(const void* recv, size_t recv_half_elems, const int* flags, size_t flags_half_elems,
+                              int world, int T, int N, int epoch, int* epoch_dev, int* done, const void* resid,
+                              int ldr, void* out, int ldo, void* stream) {
   HP_CHECK_ARG(recv && flags && out && world >= 1 && world <= HP_MAX_PEERS, "hp_peer_reduce: bad arguments");
   HP_CHECK_ARG(T >= 1 && T <= 256 && N % SBM == 0, "hp_peer_reduce: T in [1, 256], N a multiple of 128");
   HP_CHECK_ARG(ldo % 8 == 0 && (resid == nullptr || ldr % 8 == 0), "hp_peer_reduce: pitch not 16-byte aligned");
+  HP_CHECK_ARG(epoch_dev ? done != nullptr : epoch >= 1, "hp_peer_reduce: device epochs need a zeroed `done` word");
   const int m_tiles = N / SBM;
   HP_LAUNCH_PDL("k_peer_reduce", k_peer_reduce, dim3(m_tiles, (T + 15) / 16), dim3(256), 0,
-                static_cast<cudaStream_t>(stream), static_cast<const __nv_bfloat16*>(recv), flags, world, T, N,
-                m_tiles, swap_bn(T), epoch, static_cast<const __nv_bfloat16*>(resid), ldr,
-                static_cast<__nv_bfloat16*>(out), ldo);
+                static_cast<cudaStream_t>(stream), static_cast<const __nv_bfloat16*>(recv), recv_half_elems, flags,
+                flags_half_elems, world, T, N, m_tiles, swap_bn(T), epoch, epoch_dev, done,
+                static_cast<const __nv_bfloat16*>(resid), ldr, static_cast<__nv_bfloat16*>(out), ldo);
   HP_LAUNCH_CHECK("k_peer_reduce");
   return HP_OK;
 }
@@ -552,8 +587,7 @@ extern "C" int hp_peer_tiles(int T, int N) {
 
 static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
                           int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes, int* counters,
-                          int n_counters, int max_ctas, void* stream, void* const* peer_recv,
-                          int* const* peer_flags, int world, int rank, int epoch) {
+                          int n_counters, int max_ctas, void* stream, const PeerArgs* peer) {
   HP_CHECK_ARG(X && W, "hp_gemm_swap: null pointer");
   HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
   HP_CHECK_ARG(N % 128 == 0, "hp_gemm_swap: N must be a multiple of 128 (tiled weight layout)");
@@ -583,13 +617,18 @@ static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* 
   p.counters = counters;
   p.epi = epilogue;
   p.trace = static_cast<unsigned long long*>(trace_buf(TRACE_SWAP));
-  for (int q = 0; q < world; ++q) {
-    p.peer_out[q] = static_cast<__nv_bfloat16*>(peer_recv[q]);
-    p.peer_flags[q] = peer_flags[q];
+  if (peer) {
+    for (int q = 0; q < peer->world; ++q) {
+      p.peer_out[q] = static_cast<__nv_bfloat16*>(peer->recv[q]);
+      p.peer_flags[q] = peer->flags[q];
+    }
+    p.half_out = peer->half_recv;
+    p.half_flags = peer->half_flags;
+    p.epoch_dev = peer->epoch_dev;
+    p.world = peer->world;
+    p.rank = peer->rank;
+    p.epoch = peer->epoch;
   }
-  p.world = world;
-  p.rank = rank;
-  p.epoch = epoch;
   const bool any_split = p.ipc % p.num_kb != 0 || p.ipc < p.num_kb;
   if (any_split) {
     HP_CHECK_ARG(workspace && counters, "hp_gemm_swap: split tiles need workspace and counters");

@@ -42,8 +42,9 @@ SIGNATURES = {
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_peer_tiles": (_i, [_i, _i]),
-    "hp_gemm_swap_peer": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _p, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
-    "hp_peer_reduce": (_i, [_p, _p, _i, _i, _i, _i, _p, _i, _p, _i, _p]),
+    "hp_gemm_swap_peer": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, _p, _sz, _i, _i, _i, _p, _p, _sz, _p, _i, _i,
+                               _p]),
+    "hp_peer_reduce": (_i, [_p, _sz, _p, _sz, _i, _i, _i, _i, _p, _p, _p, _i, _p, _i, _p]),
     "hp_ipc_handle": (_i, [_p, _p, C.POINTER(_sz)]),
     "hp_ipc_open": (_i, [_p, C.POINTER(_p)]),
     "hp_ipc_close": (_i, [_p]),
@@ -188,23 +189,25 @@ def peer_tiles(T: int, N: int) -> int:
     return n
 
 
-def gemm_swap_peer(x, w, peer_recv, peer_flags, world: int, rank: int, epoch: int, ws, counters,
-                   max_ctas: int = 148, stream=None) -> None:
+def gemm_swap_peer(x, w, peer_recv, recv_half: int, peer_flags, flags_half: int, world: int, rank: int,
+                   epoch: int, epoch_dev, ws, counters, max_ctas: int = 148, stream=None) -> None:
     """Row-parallel decode GEMM whose epilogue scatters this rank's partial
     into every rank's receive buffer; peer_recv / peer_flags: ctypes arrays
-    of `world` device pointers (see include/hp.h hp_gemm_swap_peer)."""
+    of `world` base device pointers (see include/hp.h hp_gemm_swap_peer);
+    epoch_dev: device int tensor (device epochs) or None (host `epoch`)."""
     T, K = x.shape
     N = w.shape[0]
-    check(load().hp_gemm_swap_peer(_ptr(x), x.stride(0), _ptr(w), w.stride(0), T, N, K, peer_recv, peer_flags,
-                                   world, rank, epoch, _ptr(ws), ws.numel() * ws.element_size(), _ptr(counters),
-                                   counters.numel(), max_ctas, _stream(stream)), "hp_gemm_swap_peer")
+    check(load().hp_gemm_swap_peer(_ptr(x), x.stride(0), _ptr(w), w.stride(0), T, N, K, peer_recv, recv_half,
+                                   peer_flags, flags_half, world, rank, epoch, _ptr(epoch_dev), _ptr(ws),
+                                   ws.numel() * ws.element_size(), _ptr(counters), counters.numel(), max_ctas,
+                                   _stream(stream)), "hp_gemm_swap_peer")
 
 
-def peer_reduce(recv_ptr: int, flags_ptr: int, world: int, T: int, N: int, epoch: int, out, resid=None,
-                stream=None) -> None:
-    check(load().hp_peer_reduce(recv_ptr, flags_ptr, world, T, N, epoch, _ptr(resid),
-                                resid.stride(0) if resid is not None else 0, _ptr(out), out.stride(0),
-                                _stream(stream)), "hp_peer_reduce")
+def peer_reduce(recv_ptr: int, recv_half: int, flags_ptr: int, flags_half: int, world: int, T: int, N: int,
+                epoch: int, out, resid=None, epoch_dev=None, done=None, stream=None) -> None:
+    check(load().hp_peer_reduce(recv_ptr, recv_half, flags_ptr, flags_half, world, T, N, epoch, _ptr(epoch_dev),
+                                _ptr(done), _ptr(resid), resid.stride(0) if resid is not None else 0, _ptr(out),
+                                out.stride(0), _stream(stream)), "hp_peer_reduce")
 
 
 def ipc_handle(t) -> tuple[bytes, int]:

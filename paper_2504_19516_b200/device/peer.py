@@ -15,7 +15,10 @@ Symmetric memory (one set per rank, mapped by every peer with CUDA IPC):
     recv  bf16 [2][world][T_max][N]     half (epoch & 1) per call
     flags int  [2][world][tiles_max]    zero at allocation; values = epoch
 Epochs start at 1 and advance by one per call on every rank, so ranks stay in
-step without a host barrier (include/hp.h, hp_gemm_swap_peer).
+step without a host barrier (include/hp.h, hp_gemm_swap_peer).  With
+`device_epoch=True` the epoch lives in device memory (read by the GEMM and the
+reduce, advanced by the reduce's last block), so a captured CUDA graph of the
+layer replays correctly; the default host epochs suit eager launches.
 
 `PeerAllReduce.local_group` builds `world` instances inside ONE process on
 one GPU (all buffers local): the same kernels and flag protocol, used by the
@@ -35,7 +38,8 @@ from . import lib
 
 class PeerAllReduce:
     def __init__(self, world: int, rank: int, T_max: int, N: int, recv: torch.Tensor | None,
-                 flags: torch.Tensor | None, peer_recv: list[int], peer_flags: list[int], device):
+                 flags: torch.Tensor | None, peer_recv: list[int], peer_flags: list[int], device,
+                 device_epoch: bool = False):
         if not 1 <= world <= lib.MAX_PEERS:
             raise ValueError(f"world {world} outside [1, {lib.MAX_PEERS}]")
         if not 1 <= T_max <= 256 or N % 128:
@@ -43,14 +47,17 @@ class PeerAllReduce:
         self.world, self.rank, self.T_max, self.N = world, rank, T_max, N
         self.recv, self.flags = recv, flags          # this rank's own buffers (kept alive)
         self.dev = device
-        self.half_recv = world * T_max * N * 2       # bytes
-        self.half_flags = world * lib.peer_tiles(T_max, N) * 4
+        self.half_recv = world * T_max * N           # elements (bf16)
+        self.half_flags = world * lib.peer_tiles(T_max, N)  # elements (int32)
         self._peer_recv = peer_recv
         self._peer_flags = peer_flags
-        self._ptr_arrays = {}
+        self._rv = (C.c_void_p * world)(*peer_recv)
+        self._fl = (C.c_void_p * world)(*peer_flags)
         self._opened: list[int] = []
         self.epoch = 0
         self._ws = None
+        # device epoch + the reduce's block counter (both start at zero)
+        self.epoch_dev = torch.zeros(2, dtype=torch.int32, device=device) if device_epoch else None
 
     # ---------------------------------------------------------- construction
     @staticmethod
@@ -60,17 +67,19 @@ class PeerAllReduce:
         return recv, flags
 
     @classmethod
-    def local_group(cls, world: int, T_max: int, N: int, device=None) -> list["PeerAllReduce"]:
+    def local_group(cls, world: int, T_max: int, N: int, device=None,
+                    device_epoch: bool = False) -> list["PeerAllReduce"]:
         """`world` ranks emulated in one process: every rank's buffers live on
         this GPU and the 'peer' pointers are plain device pointers."""
         device = device or torch.device("cuda", torch.cuda.current_device())
         bufs = [cls._alloc(world, T_max, N, device) for _ in range(world)]
         pr = [r.data_ptr() for r, _ in bufs]
         pf = [f.data_ptr() for _, f in bufs]
-        return [cls(world, q, T_max, N, bufs[q][0], bufs[q][1], pr, pf, device) for q in range(world)]
+        return [cls(world, q, T_max, N, bufs[q][0], bufs[q][1], pr, pf, device, device_epoch)
+                for q in range(world)]
 
     @classmethod
-    def create(cls, group, T_max: int, N: int, device=None) -> "PeerAllReduce":
+    def create(cls, group, T_max: int, N: int, device=None, device_epoch: bool = False) -> "PeerAllReduce":
         """One rank of a multi-process TP group: allocate this rank's buffers,
         exchange CUDA IPC handles over `group`, map every peer's buffers."""
         import torch.distributed as dist
@@ -92,7 +101,7 @@ class PeerAllReduce:
                 if h not in opened:  # recv and flags may share one allocation block
                     opened[h] = lib.ipc_open(h)
                 dst.append(opened[h] + off)
-        self = cls(world, rank, T_max, N, recv, flags, pr, pf, device)
+        self = cls(world, rank, T_max, N, recv, flags, pr, pf, device, device_epoch)
         self._opened = list(opened.values())
         dist.barrier(group=group)
         return self
@@ -103,14 +112,6 @@ class PeerAllReduce:
         self._opened = []
 
     # ------------------------------------------------------------------ call
-    def _arrays(self, half: int):
-        a = self._ptr_arrays.get(half)
-        if a is None:
-            rv = (C.c_void_p * self.world)(*[p + half * self.half_recv for p in self._peer_recv])
-            fl = (C.c_void_p * self.world)(*[p + half * self.half_flags for p in self._peer_flags])
-            a = self._ptr_arrays[half] = (rv, fl)
-        return a
-
     def workspace(self, K: int, max_ctas: int):
         nb = lib.gemm_swap_ws_bytes(256, self.N, K, max_ctas)
         if self._ws is None or self._ws[0].numel() * 4 < nb:
@@ -123,18 +124,21 @@ class PeerAllReduce:
         T = x.shape[0]
         if T > self.T_max or w.shape[0] != self.N:
             raise ValueError(f"fused all-reduce sized for T <= {self.T_max}, N = {self.N}")
-        rv, fl = self._arrays(epoch & 1)
         ws, cnt = self.workspace(x.shape[1], max_ctas)
-        lib.gemm_swap_peer(x, w, C.cast(rv, C.c_void_p), C.cast(fl, C.c_void_p), self.world, self.rank, epoch,
-                           ws, cnt, max_ctas=max_ctas, stream=stream)
+        lib.gemm_swap_peer(x, w, C.cast(self._rv, C.c_void_p), self.half_recv, C.cast(self._fl, C.c_void_p),
+                           self.half_flags, self.world, self.rank, epoch, self._edev(), ws, cnt,
+                           max_ctas=max_ctas, stream=stream)
 
     def reduce(self, out, epoch: int, resid=None, stream=None) -> None:
         """Receive half: out = sum over ranks of the partials (+ resid)."""
         T = out.shape[0]
-        half = epoch & 1
-        lib.peer_reduce(self._peer_recv[self.rank] + half * self.half_recv,
-                        self._peer_flags[self.rank] + half * self.half_flags, self.world, T, self.N, epoch,
-                        out, resid=resid, stream=stream)
+        e = self._edev()
+        lib.peer_reduce(self._peer_recv[self.rank], self.half_recv, self._peer_flags[self.rank], self.half_flags,
+                        self.world, T, self.N, epoch, out, resid=resid, epoch_dev=e,
+                        done=None if e is None else self.epoch_dev[1:], stream=stream)
+
+    def _edev(self):
+        return None if self.epoch_dev is None else self.epoch_dev[:1]
 
     def linear(self, x, w, out, resid=None, max_ctas: int = 148, stream=None) -> None:
         """out = all_reduce(x @ w^T) + resid, fused (one process per rank)."""

@@ -94,3 +94,49 @@ def test_fused_allreduce_rejects_bad_shapes():
     w = lib.tile_weight(torch.zeros(1024, 256, dtype=torch.bfloat16, device=DEV))
     with pytest.raises(ValueError):
         pr.gemm(x, w, 1)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_allreduce_device_epochs_replay_in_a_cuda_graph(world):
+    """device_epoch=True: the epoch lives on the device, so one captured graph
+    of every rank's GEMM + reduce replays call after call (alternating buffer
+    halves) and stays bit-identical to the unfused path."""
+    N, K, T = 1024, 512, 48
+    g = torch.Generator(device="cpu").manual_seed(77 + world)
+    ranks = PeerAllReduce.local_group(world, 64, N, DEV, device_epoch=True)
+    ws_t = [lib.tile_weight((torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16).to(DEV))
+            for _ in range(world)]
+    xs = [torch.empty(T, K, dtype=torch.bfloat16, device=DEV) for _ in range(world)]
+    resid = torch.empty(T, N, dtype=torch.bfloat16, device=DEV)
+    outs = [torch.empty(T, N, dtype=torch.bfloat16, device=DEV) for _ in range(world)]
+
+    def step():
+        for r in range(world):
+            ranks[r].gemm(xs[r], ws_t[r], 0, max_ctas=32)
+        for r in range(world):
+            ranks[r].reduce(outs[r], 0, resid=resid)
+
+    def fill():
+        for x in xs:
+            x.copy_(torch.randn(T, K, generator=g).to(torch.bfloat16))
+        resid.copy_(torch.randn(T, N, generator=g).to(torch.bfloat16))
+
+    fill()
+    step()  # eager call 1 (also sizes the workspaces before capture)
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, _unfused(xs, ws_t, resid, 32)) for o in outs)
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s), torch.cuda.graph(graph, stream=s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    for call in range(4):  # replays = epochs 2..5 (both halves, twice)
+        fill()
+        graph.replay()
+        torch.cuda.synchronize()
+        ref = _unfused(xs, ws_t, resid, 32)
+        for r in range(world):
+            assert torch.equal(outs[r], ref), (call, r)
+    for pr in ranks:
+        assert pr.epoch_dev[0].item() == 5 and pr.epoch_dev[1].item() == 0
