@@ -26,6 +26,7 @@
 #include "../../include/hp.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace hp {
 
@@ -57,7 +58,8 @@ struct SwapCfg {
 
 struct SwapParams {
   int N, T, K;
-  int m_tiles, n_tiles, num_kb;
+  int m_tiles, n_tiles, num_kb;  // m_tiles: 128-feature tiles
+  int m_walk;       // feature tiles of the stream-K walk (m_tiles, or m_tiles / 2 for CTA pairs)
   int ipc;          // k-block iterations per CTA
   int total_iters;  // m_tiles * n_tiles * num_kb
   int max_contrib;
@@ -166,6 +168,154 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
         *reinterpret_cast<uint32_t*>(p.out + size_t(t) * p.ldo + o) = pack_bf16(v0, v1);
       }
     }
+  }
+}
+
+// Epilogue warps of the decode GEMM (both kernels): per stream-K segment,
+// whole tiles go TMEM -> smem transpose -> output; split tiles leave fp32
+// partials and the last contributor sums them.  cid: this CTA's (or pair's)
+// contributor index in the walk; PAIR: rank = CTA in the pair, TMEM release
+// goes to the leader's `tempty` (both CTAs' epilogue warps arrive).
+template <int BN, int NCH, bool PAIR>
+__device__ __forceinline__ void swap_epilogue(const SwapParams& p, float* V, uint64_t* tfull, uint64_t* tempty,
+                                              int* last_flag, uint32_t tmem_base, int begin, int end, int cid,
+                                              uint32_t rank) {
+  const uint32_t ltempty = PAIR ? mapa_shared(tempty, 0) : 0u;
+  auto release = [&](int acc) {
+    if (PAIR)
+      mbar_arrive_cluster_relaxed(ltempty + 8u * acc);
+    else
+      mbar_arrive(&tempty[acc]);
+  };
+pdl_wait();  // residual, workspace and output are shared with the stream predecessor
+const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+const int q = warp & 3;
+  const int row = q * 32 + lane;
+  const int et = (warp - SW_MMA - 1) * 32 + lane;
+  // HP_EPI_PEER: this call's epoch (after pdl_wait: the previous reduce
+  // advanced *epoch_dev); once the whole tile sits in every rank's receive
+  // buffer, publish it with a system-scope release on every rank's flags
+  const int ep = p.epi != HP_EPI_PEER ? 0 : (p.epoch_dev ? *p.epoch_dev + 1 : p.epoch);
+  auto publish = [&](int tile) {
+    if (p.epi != HP_EPI_PEER) return;
+    epi_sync();
+    if (et == 0) {
+      __threadfence_system();
+      const size_t f = (ep & 1) * p.half_flags + size_t(p.rank) * (p.m_tiles * p.n_tiles) + tile;
+      for (int r = 0; r < p.world; ++r) st_release_sys(p.peer_flags[r] + f, ep);
+    }
+  };
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  int it = begin;
+  Seg s;
+  while (next_seg(p, it, end, s)) {
+    const int mw = s.tile % p.m_walk, nt = s.tile / p.m_walk;
+    const int mt = PAIR ? 2 * mw + int(rank) : mw;  // this CTA's 128-feature tile
+    const int t128 = nt * p.m_tiles + mt;           // its workspace / counter / flag slot
+    const int first = (s.tile * p.num_kb) / p.ipc;
+    const int last = ((s.tile + 1) * p.num_kb - 1) / p.ipc;
+    const bool single = first == last;
+    mbar_wait(&tfull[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * (NCH * BN);
+    if (single) {
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        load_acc<BN, NCH>(taddr + c * 32, v);
+        if (c == BN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) release(acc);
+        }
+        epi_sync();  // previous chunk's readers are done with V
+#pragma unroll
+        for (int j = 0; j < 32; ++j) V[row * VLD + j] = v[j];
+        epi_sync();
+        emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
+      }
+      publish(t128);
+    } else {
+      float* mine = p.ws + (size_t(t128) * p.max_contrib + (cid - first)) * (SBM * BN) +
+                    size_t(row) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        load_acc<BN, NCH>(taddr + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(mine + c * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) release(acc);
+      __threadfence();
+      epi_sync();
+      if (et == 0) {
+        const int prev = atomicAdd(p.counters + t128, 1);
+        *last_flag = (prev == last - first) ? 1 : 0;
+      }
+      epi_sync();
+      if (*last_flag) {
+        __threadfence();
+        const int ncontrib = last - first + 1;
+        const float* base = p.ws + size_t(t128) * p.max_contrib * (SBM * BN);
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          // 128 rows x 32 cols chunk: 1024 float4, 8 per thread
+          float4 a[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          // two contributors per round with all 16 loads in flight (the
+          // partials are L2 hits; a one-at-a-time loop paid one L2 round
+          // trip per contributor on the GEMM's critical tail)
+          auto ld = [&](int k, int i) {
+            const int f = i * 128 + et;            // float4 index within the chunk
+            const int r = f >> 3, cc = (f & 7) * 4;
+            return __ldcg(reinterpret_cast<const float4*>(base + size_t(k) * (SBM * BN) + size_t(r) * BN +
+                                                          c * 32 + cc));
+          };
+          int k = 0;
+          for (; k + 1 < ncontrib; k += 2) {
+            float4 x0[8], x1[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              x0[i] = ld(k, i);
+              x1[i] = ld(k + 1, i);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              a[i].x += x0[i].x; a[i].y += x0[i].y; a[i].z += x0[i].z; a[i].w += x0[i].w;
+              a[i].x += x1[i].x; a[i].y += x1[i].y; a[i].z += x1[i].z; a[i].w += x1[i].w;
+            }
+          }
+          if (k < ncontrib) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 x = ld(k, i);
+              a[i].x += x.x; a[i].y += x.y; a[i].z += x.z; a[i].w += x.w;
+            }
+          }
+          epi_sync();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int f = i * 128 + et;
+            const int r = f >> 3, cc = (f & 7) * 4;
+            V[r * VLD + cc] = a[i].x;
+            V[r * VLD + cc + 1] = a[i].y;
+            V[r * VLD + cc + 2] = a[i].z;
+            V[r * VLD + cc + 3] = a[i].w;
+          }
+          epi_sync();
+          emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
+        }
+        if (et == 0) p.counters[t128] = 0;
+        publish(t128);
+      }
+    }
+    acc ^= 1;
+    if (acc == 0) acc_phase ^= 1;
   }
 }
 
@@ -301,133 +451,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     }
     if (tr && lane == 0) tr[3] = globaltimer();
   } else {
-    pdl_wait();  // residual, workspace and output are shared with the stream predecessor
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const int et = (warp - SW_MMA - 1) * 32 + lane;
-    // HP_EPI_PEER: this call's epoch (after pdl_wait: the previous reduce
-    // advanced *epoch_dev); once the whole tile sits in every rank's receive
-    // buffer, publish it with a system-scope release on every rank's flags
-    const int ep = p.epi != HP_EPI_PEER ? 0 : (p.epoch_dev ? *p.epoch_dev + 1 : p.epoch);
-    auto publish = [&](int tile) {
-      if (p.epi != HP_EPI_PEER) return;
-      epi_sync();
-      if (et == 0) {
-        __threadfence_system();
-        const size_t f = (ep & 1) * p.half_flags + size_t(p.rank) * (p.m_tiles * p.n_tiles) + tile;
-        for (int r = 0; r < p.world; ++r) st_release_sys(p.peer_flags[r] + f, ep);
-      }
-    };
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int it = begin;
-    Seg s;
-    while (next_seg(p, it, end, s)) {
-      const int mt = s.tile % p.m_tiles, nt = s.tile / p.m_tiles;
-      const int first = (s.tile * p.num_kb) / p.ipc;
-      const int last = ((s.tile + 1) * p.num_kb - 1) / p.ipc;
-      const bool single = first == last;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * C::ACC_COLS;
-      if (single) {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          load_acc<BN, C::NCH>(taddr + c * 32, v);
-          if (c == BN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          epi_sync();  // previous chunk's readers are done with V
-#pragma unroll
-          for (int j = 0; j < 32; ++j) V[row * VLD + j] = v[j];
-          epi_sync();
-          emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
-        }
-        publish(s.tile);
-      } else {
-        float* mine = p.ws + (size_t(s.tile) * p.max_contrib + (blockIdx.x - first)) * (SBM * BN) +
-                      size_t(row) * BN;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          load_acc<BN, C::NCH>(taddr + c * 32, v);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(mine + c * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        __threadfence();
-        epi_sync();
-        if (et == 0) {
-          const int prev = atomicAdd(p.counters + s.tile, 1);
-          *last_flag = (prev == last - first) ? 1 : 0;
-        }
-        epi_sync();
-        if (*last_flag) {
-          __threadfence();
-          const int ncontrib = last - first + 1;
-          const float* base = p.ws + size_t(s.tile) * p.max_contrib * (SBM * BN);
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            // 128 rows x 32 cols chunk: 1024 float4, 8 per thread
-            float4 a[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            // two contributors per round with all 16 loads in flight (the
-            // partials are L2 hits; a one-at-a-time loop paid one L2 round
-            // trip per contributor on the GEMM's critical tail)
-            auto ld = [&](int k, int i) {
-              const int f = i * 128 + et;            // float4 index within the chunk
-              const int r = f >> 3, cc = (f & 7) * 4;
-              return __ldcg(reinterpret_cast<const float4*>(base + size_t(k) * (SBM * BN) + size_t(r) * BN +
-                                                            c * 32 + cc));
-            };
-            int k = 0;
-            for (; k + 1 < ncontrib; k += 2) {
-              float4 x0[8], x1[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                x0[i] = ld(k, i);
-                x1[i] = ld(k + 1, i);
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                a[i].x += x0[i].x; a[i].y += x0[i].y; a[i].z += x0[i].z; a[i].w += x0[i].w;
-                a[i].x += x1[i].x; a[i].y += x1[i].y; a[i].z += x1[i].z; a[i].w += x1[i].w;
-              }
-            }
-            if (k < ncontrib) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float4 x = ld(k, i);
-                a[i].x += x.x; a[i].y += x.y; a[i].z += x.z; a[i].w += x.w;
-              }
-            }
-            epi_sync();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int f = i * 128 + et;
-              const int r = f >> 3, cc = (f & 7) * 4;
-              V[r * VLD + cc] = a[i].x;
-              V[r * VLD + cc + 1] = a[i].y;
-              V[r * VLD + cc + 2] = a[i].z;
-              V[r * VLD + cc + 3] = a[i].w;
-            }
-            epi_sync();
-            emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
-          }
-          if (et == 0) p.counters[s.tile] = 0;
-          publish(s.tile);
-        }
-      }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-    }
+    swap_epilogue<BN, C::NCH, false>(p, V, tfull, tempty, last_flag, tmem_base, begin, end, blockIdx.x, 0);
   }
   if (tr && threadIdx.x == (SW_MMA + 1) * 32) tr[4] = globaltimer();
   tc_fence_before();
@@ -437,6 +461,180 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
   if (tr && threadIdx.x == 0) tr[5] = globaltimer();
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant: a 2-CTA cluster owns 256 output features; the leader
+// issues tcgen05.mma.cta_group::2 (M = 256) with each CTA's 128 weight rows
+// and half of the BN tokens in its own smem.  At N = BN = 32 one pair MMA
+// runs at 41 % of the pair's MAC rate where the 1-CTA form manages 18 %
+// (profiles/r01_umma_rates.md), which is what caps a small decode partition:
+// 8 MMAs per 32 KB weight stage take ~710 cycles on one SM (~107 GB/s).
+// Both CTAs' stage copies (TMA, .cta_group::2) complete on the leader's
+// `full`; the leader's commits free both CTAs' stages (multicast).
+template <int BN>
+struct SwapPairCfg {
+  static constexpr uint32_t A_BYTES = SBM * SBK * 2;       // this CTA's 128 weight rows
+  static constexpr uint32_t B_BYTES = (BN / 2) * SBK * 2;  // this CTA's BN/2 tokens
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t VBUF = size_t(SBM) * VLD * 4;
+  static constexpr int STAGES_FIT = int((227 * 1024 - 1024 - VBUF - 256) / STAGE_BYTES);
+  static constexpr int STAGES = STAGES_FIT < 6 ? STAGES_FIT : 6;
+  static constexpr int PL = STAGES < SW_PRODUCERS ? STAGES : SW_PRODUCERS;
+  static constexpr int NCH = SwapCfg<BN>::NCH;
+  static constexpr uint32_t ACC_COLS = NCH * BN;
+  static constexpr uint32_t TMEM_COLS = SwapCfg<BN>::TMEM_COLS;
+  static constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + VBUF + 256;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SW_THREADS, 1)
+    k_gemm_swap_pair(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                     const SwapParams p) {
+  using C = SwapPairCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  float* V = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(V) + C::VBUF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // on the leader: 4 epilogue warps per CTA
+    }
+    fence_barrier_init();
+  }
+  if (warp == SW_MMA) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int begin = pair * p.ipc;
+  const int end = min(begin + p.ipc, p.total_iters);
+
+  if (warp < SW_PRODUCERS) {
+    constexpr int PL = C::PL;
+    const uint32_t lfull = mapa_shared(full, 0);
+    // weights (constant across the layer chain) for the first ring before the
+    // programmatic-dependency wait, activations after it
+    for (int pass = 0; pass < 2; ++pass) {
+      uint32_t g = 0;
+      int it = begin;
+      Seg s;
+      while (next_seg(p, it, end, s)) {
+        const int mw = s.tile % p.m_walk, nt = s.tile / p.m_walk;
+        for (int kb = s.kb0; kb < s.kb1; ++kb, ++g) {
+          const bool pre = g < uint32_t(STAGES);
+          if (int(g % PL) != warp || (pass == 0 && !pre)) continue;
+          const int stage = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          const uint32_t bar = lfull + 8u * stage;
+          if (pass == 0 || !pre) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (elect_one()) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+              // this CTA's 128 x 128 weight block: one 32 KB run of the tiled layout
+              const int wrow = int(wtile_offset((2 * mw + int(rank)) * SBM, 2 * kb, p.K) / 128);
+              tma_load_2d_pair(sA + stage * C::A_BYTES, &tmW, bar, 0, wrow);
+            }
+          }
+          if (pass == 1 && elect_one()) {
+            const int t0 = nt * BN + int(rank) * (BN / 2);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmX, bar, kb * SBK, t0);
+            tma_load_2d_pair(sB + stage * C::B_BYTES + (BN / 2) * 128, &tmX, bar, kb * SBK + 64, t0);
+          }
+          __syncwarp();
+        }
+        if (pass == 0 && g >= uint32_t(STAGES)) break;
+      }
+      if (pass == 0) pdl_wait();
+    }
+  } else if (warp == SW_MMA) {
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * SBM, BN);
+      const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA));
+      const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sB));
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int it = begin;
+      Seg s;
+      while (next_seg(p, it, end, s)) {
+        mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+        for (int kb = s.kb0; kb < s.kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = adesc0 + uint64_t((stage * C::A_BYTES) >> 4);
+          const uint64_t bd = bdesc0 + uint64_t((stage * C::B_BYTES) >> 4);
+          const bool first = kb == s.kb0;
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < SBK / 16; ++k)
+              umma_bf16_pair(d_tmem + (k % C::NCH) * BN, ad + (k >> 2) * (128 * 128 >> 4) + 2 * (k & 3),
+                             bd + (k >> 2) * ((BN / 2) * 128 >> 4) + 2 * (k & 3), idesc,
+                             (!first || k >= C::NCH) ? 1u : 0u);
+            umma_commit_pair(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) umma_commit_pair(&tfull[acc]);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    swap_epilogue<BN, C::NCH, true>(p, V, tfull, tempty, last_flag, tmem_base, begin, end, pair, rank);
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == SW_MMA) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN>
+static int launch_swap_pair(const CUtensorMap& tx, const SwapParams& p, int grid, cudaStream_t st) {
+  using C = SwapPairCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_gemm_swap_pair<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(C::SMEM)));
+    attr_set = true;
+  }
+  // the tiled weights as a [N*K/64, 64] bf16 tensor: one 256-row box is one
+  // CTA's contiguous 32 KB stage (two pre-swizzled [128][64] halves, verbatim)
+  CUtensorMap tw;
+  int rc = cached_tmap_bf16(&tw, p.w, uint64_t(p.N) * p.K / 64, 64, 64, 256, 64, false);
+  if (rc) return rc;
+  HP_LAUNCH_PDL("k_gemm_swap_pair", k_gemm_swap_pair<BN>, dim3(grid), dim3(SW_THREADS), C::SMEM, st, tx, tw, p);
+  HP_LAUNCH_CHECK("k_gemm_swap_pair");
+  return HP_OK;
 }
 
 template <int BN>
@@ -604,8 +802,20 @@ static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* 
   p.m_tiles = N / SBM;
   p.n_tiles = (T + BN - 1) / BN;
   p.num_kb = K / SBK;
-  p.total_iters = p.m_tiles * p.n_tiles * p.num_kb;
-  const int grid = std::min(max_ctas, p.total_iters);
+  // CTA pairs (M = 256 MMAs) on small partitions (2..16 SMs), where one SM's
+  // MMA issue rate at N = 32 is the limit (8 SMs: 105 -> 113 GB/s per SM,
+  // tools/swap_sms.py); on the full GPU the 1-CTA walk is faster (2.89 vs
+  // 2.57 TB/s: half as many independent streams).  HP_SWAP_PAIR=0/1 forces.
+  static const int pair_env = [] {
+    const char* e = std::getenv("HP_SWAP_PAIR");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool pair_ok = N % 256 == 0 && max_ctas >= 2;
+  const bool pair = pair_ok && (pair_env >= 0 ? pair_env == 1 : max_ctas <= 16);
+  p.m_walk = pair ? p.m_tiles / 2 : p.m_tiles;
+  p.total_iters = p.m_walk * p.n_tiles * p.num_kb;
+  const int units = pair ? max_ctas / 2 : max_ctas;
+  const int grid = std::min(units, p.total_iters);
   p.ipc = (p.total_iters + grid - 1) / grid;
   p.max_contrib = (p.num_kb + p.ipc - 1) / p.ipc + 1;
   p.out = static_cast<__nv_bfloat16*>(Y);
@@ -636,10 +846,19 @@ static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* 
     HP_CHECK_ARG(n_counters >= p.m_tiles * p.n_tiles, "hp_gemm_swap: too few counters");
   }
   CUtensorMap tx;
-  int rc = cached_tmap_bf16(&tx, X, T, K, ldx, BN, 64, true);  // two 64-k boxes per stage
+  // two 64-k boxes per stage; a pair CTA loads its BN/2 tokens
+  int rc = cached_tmap_bf16(&tx, X, T, K, ldx, pair ? BN / 2 : BN, 64, true);
   if (rc) return rc;
   const int g = (p.total_iters + p.ipc - 1) / p.ipc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pair) {
+    switch (BN) {
+      case 32: return launch_swap_pair<32>(tx, p, 2 * g, st);
+      case 64: return launch_swap_pair<64>(tx, p, 2 * g, st);
+      case 128: return launch_swap_pair<128>(tx, p, 2 * g, st);
+      default: return launch_swap_pair<256>(tx, p, 2 * g, st);
+    }
+  }
   switch (BN) {
     case 32: return launch_swap<32>(tx, p, g, st);
     case 64: return launch_swap<64>(tx, p, g, st);

@@ -102,7 +102,11 @@ def _ws(N, T, K, ctas):
 
 @pytest.mark.parametrize("T,N,K,ctas", [(1, 256, 256, 1), (8, 6144, 4096, 148), (32, 4096, 4096, 64),
                                         (32, 4096, 4096, 32), (33, 1024, 1024, 7), (100, 512, 2048, 148),
-                                        (256, 256, 512, 3), (32, 28672, 4096, 148)])
+                                        (256, 256, 512, 3), (32, 28672, 4096, 148),
+                                        # CTA-pair kernel (N % 256 == 0 on <= 16 SMs): BN 32 / 64 / 128 /
+                                        # 256, split and whole tiles, tokens past T zero-filled
+                                        (32, 4096, 4096, 8), (20, 6144, 4096, 16), (64, 512, 2048, 2),
+                                        (100, 1024, 1024, 6), (256, 512, 512, 4), (9, 28672, 4096, 8)])
 def test_gemm_swap_store(T, N, K, ctas, gen):
     x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
     y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
@@ -117,7 +121,7 @@ def test_gemm_swap_store(T, N, K, ctas, gen):
     assert rel_err(y, x.float() @ w.float().T) < 1e-2
 
 
-@pytest.mark.parametrize("ctas", [32, 148])
+@pytest.mark.parametrize("ctas", [32, 148, 8, 2])
 def test_gemm_swap_resid_silu(ctas, gen):
     T, K = 32, 1024
     x, r = bf((T, K), gen=gen), bf((T, 4096), gen=gen)
