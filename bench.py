@@ -297,9 +297,12 @@ def main(argv=None) -> int:
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         rid = torch.cuda.nvtx.range_start("timed")  # process-wide range (ncu --nvtx-include "timed]")
-        res = cr.corun(pm, dm, args.steps, n, time_upgate=True)
+        res = cr.corun(pm, dm, args.steps, n, time_upgate=True)  # events around mlp_up_gate only
         torch.cuda.nvtx.range_end(rid)
     torch.cuda.synchronize()
+    # per-group breakdown from a second, fully instrumented co-run (diagnostic:
+    # events between every kernel group cost their programmatic-launch overlap)
+    groups = cr.corun(pm, dm, args.steps, n, time_groups=True)
     span, tokens = job_totals(dist, res.span_s, res.tokens, "cuda")
     if dist is not None:
         dist.barrier()
@@ -336,7 +339,7 @@ def main(argv=None) -> int:
              (("qkv", wl.w_qkv), ("o_proj", wl.w_o), ("mlp_up_gate", wl.w_ug), ("mlp_down", wl.w_down))}
     units = {g: (pl[1], pm // pl[2]) for g, pl in plans.items()}  # (tiles, concurrent tile slots)
     units["attn"] = (-(-T // 256) * model.num_heads, pm)          # k_fa2: 256-query units, one per CTA
-    g_s = res.group_s
+    g_s = groups.group_s
     wave_idle = sum(g_s[g] * wave_stats(u, 1, n).idle_ratio for g, (u, n) in units.items()) / sum(g_s.values())
 
     # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
@@ -394,7 +397,9 @@ def main(argv=None) -> int:
         },
         "chunked_baseline": chunked,
         "sm_idle_pct": {"partition": 100 * res.partition_idle(N), "wave_model_prefill_layer": 100 * wave_idle,
-                        "prefill_group_us": {g: 1e6 * v for g, v in g_s.items()}},
+                        "prefill_group_us": {g: 1e6 * v for g, v in g_s.items()},
+                        "prefill_group_note": "per-group events from a second co-run of the same split (the timed "
+                                              "region records events around mlp_up_gate only)"},
         "prefill_gemms": {"tflops": gemm_flops / gemm_s / 1e12, "frac_of_partition_peak": gemm_flops / gemm_s / 1e12 / peak,
                           "frac_of_partition_sustained_peak": gemm_flops / gemm_s / 1e12 / (tf_sus * pm / N),
                           "flops_per_layer": gemm_flops,

@@ -168,15 +168,19 @@ class CoRunner:
         return ms[len(ms) // 2] * 1e-3
 
     def corun(self, pm: int, dm: int, steps: int, decode_per_step: int, time_upgate: bool = False,
-              copy_in=None, copy_out=None) -> CoRunResult:
+              copy_in=None, copy_out=None, time_groups: bool = False) -> CoRunResult:
         """`steps` prefill layers on pm SMs co-executed with
-        steps * decode_per_step decode layer-steps on dm SMs."""
+        steps * decode_per_step decode layer-steps on dm SMs.  time_upgate:
+        events around the mlp_up_gate GEMM only (the roofline kernel);
+        time_groups: around every kernel group (diagnostic: the extra events
+        between launches cost their programmatic-launch overlap)."""
         ps, ds = self.pool.split(pm, dm)
         g = self.decode_graph(ds)
         ctrl = torch.cuda.current_stream(self.dev)
         start, end_p, end_d = _ev(), _ev(), _ev()
         p_ev = [(_ev(), _ev()) for _ in range(steps)]
-        ug_ev = ([{g: (_ev(), _ev()) for g in GROUPS} for _ in range(steps)] if time_upgate else None)
+        timed = GROUPS if time_groups else (("mlp_up_gate",) if time_upgate else ())
+        ug_ev = [{g: (_ev(), _ev()) for g in timed} for _ in range(steps)] if timed else None
         d_ev = [(_ev(), _ev()) for _ in range(steps * decode_per_step)]
         torch.cuda._sleep(400_000)
         start.record(ctrl)
@@ -214,7 +218,7 @@ class CoRunner:
         if ug_ev:
             res.upgate_s = [a.elapsed_time(b) * 1e-3 for a, b in (e["mlp_up_gate"] for e in ug_ev)]
             res.group_s = {g: statistics.median(e[g][0].elapsed_time(e[g][1]) * 1e-3 for e in ug_ev)
-                           for g in GROUPS}
+                           for g in timed}
         return res
 
     def corun_e2e(self, pm: int, dm: int, steps: int, decode_per_step: int, host_px, host_py,
