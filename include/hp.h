@@ -156,11 +156,27 @@ int hp_peer_tiles(int T, int N);
 int hp_gemm_swap_peer(const void* X, int ldx, const void* W, int ldw, int T, int N, int K,
                       void* const* peer_recv, size_t recv_half_elems, int* const* peer_flags,
                       size_t flags_half_elems, int world, int rank, int epoch, const int* epoch_dev,
-                      void* workspace, size_t ws_bytes, int* counters, int n_counters, int max_ctas,
-                      void* stream);
+                      int two_shot, void* workspace, size_t ws_bytes, int* counters, int n_counters,
+                      int max_ctas, void* stream);
 int hp_peer_reduce(const void* recv, size_t recv_half_elems, const int* flags, size_t flags_half_elems,
                    int world, int T, int N, int epoch, int* epoch_dev, int* done, const void* resid,
                    int ldr, void* out, int ldo, void* stream);
+/* Two-shot form (two_shot = 1 in hp_gemm_swap_peer): feature tile mt belongs
+ * to rank mt % world and the GEMM sends it only there, (world-1)/world of
+ * the message per rank instead of (world-1) x.  hp_peer_rs (owner: wait for
+ * the tile's partials, sum + resid, broadcast the bf16 result into every
+ * rank's gather buffer gather_r = bf16 [2][T_max][N], raise gflags_r =
+ * int [2][ceil(T_max/16)][N/128] on every rank), then hp_peer_ag (every
+ * rank: wait for each (16-row block, feature tile) flag, copy to out; with
+ * epoch_dev it advances the device epoch).  Bytes moved per rank over
+ * NVLink: 2 (world-1)/world T N 2 -- the bandwidth-optimal all-reduce for
+ * large decode batches; one-shot has one fewer hop for small ones. */
+int hp_peer_rs(const void* recv, size_t recv_half_elems, const int* flags, size_t flags_half_elems,
+               void* const* peer_gather, size_t gather_half_elems, int* const* peer_gflags,
+               size_t gflags_half_elems, int world, int rank, int T, int N, int epoch, const int* epoch_dev,
+               const void* resid, int ldr, void* stream);
+int hp_peer_ag(const void* gather, size_t gather_half_elems, const int* gflags, size_t gflags_half_elems,
+               int T, int N, int epoch, int* epoch_dev, int* done, void* out, int ldo, void* stream);
 /* CUDA IPC for the symmetric buffers: export the handle (HP_IPC_HANDLE_BYTES
  * opaque bytes) of the allocation block holding dev_ptr plus dev_ptr's
  * offset in it; a peer maps the block (hp_ipc_open -> base; its pointer is

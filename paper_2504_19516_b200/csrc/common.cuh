@@ -56,6 +56,11 @@ HP_DEVICE void st_volatile_shared(uint32_t addr, uint32_t v) {
 }
 
 // System-scope release/acquire on a flag another GPU (or process) reads/writes.
+// Relaxed system-scope store: after one __threadfence_system() (fence.sc.sys)
+// a batch of these publishes like release stores without a fence each.
+HP_DEVICE void st_relaxed_sys(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 HP_DEVICE void st_release_sys(int* p, int v) {
   asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

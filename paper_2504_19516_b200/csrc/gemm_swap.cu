@@ -82,6 +82,7 @@ struct SwapParams {
   size_t half_out, half_flags;
   const int* epoch_dev;
   int world, rank, epoch;
+  int two_shot;     // 1: a tile goes only to its owner rank (feature tile mt % world)
 };
 
 struct Seg {
@@ -148,7 +149,10 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
         const uint4 v = make_uint4(pack_bf16(c[0], c[VLD]), pack_bf16(c[2 * VLD], c[3 * VLD]),
                                    pack_bf16(c[4 * VLD], c[5 * VLD]), pack_bf16(c[6 * VLD], c[7 * VLD]));
         const size_t off = (ep & 1) * p.half_out + (size_t(p.rank) * p.T + t) * p.N + mt * SBM + g * 8;
-        for (int q = 0; q < p.world; ++q) *reinterpret_cast<uint4*>(p.peer_out[q] + off) = v;
+        if (p.two_shot)
+          *reinterpret_cast<uint4*>(p.peer_out[mt % p.world] + off) = v;
+        else
+          for (int q = 0; q < p.world; ++q) *reinterpret_cast<uint4*>(p.peer_out[q] + off) = v;
       }
     }
   } else {
@@ -202,7 +206,10 @@ const int q = warp & 3;
     if (et == 0) {
       __threadfence_system();
       const size_t f = (ep & 1) * p.half_flags + size_t(p.rank) * (p.m_tiles * p.n_tiles) + tile;
-      for (int r = 0; r < p.world; ++r) st_release_sys(p.peer_flags[r] + f, ep);
+      if (p.two_shot)
+        st_relaxed_sys(p.peer_flags[(tile % p.m_tiles) % p.world] + f, ep);
+      else
+        for (int r = 0; r < p.world; ++r) st_relaxed_sys(p.peer_flags[r] + f, ep);  // fenced above
     }
   };
   int acc = 0;
@@ -723,6 +730,98 @@ __global__ void __launch_bounds__(256) k_peer_reduce(const __nv_bfloat16* __rest
   }
 }
 
+// Two-shot receive side, step 1 (reduce-scatter): this rank owns the
+// feature tiles mt with mt % world == rank; per owned tile and 16-token row
+// block, wait for every rank's partial, sum (+ resid) and broadcast the bf16
+// result into every rank's gather buffer, then raise gather flag
+// [row block][mt] = epoch on every rank.
+struct PeerPtrs {  // per-rank device pointers, passed by value in the kernel parameters
+  __nv_bfloat16* buf[HP_MAX_PEERS];
+  int* flag[HP_MAX_PEERS];
+};
+
+__global__ void __launch_bounds__(256) k_peer_rs(const __nv_bfloat16* __restrict__ recv, size_t half_recv,
+                                                 const int* flags, size_t half_flags, const PeerPtrs g,
+                                                 size_t half_gather, size_t half_gflags, int world, int rank,
+                                                 int T, int N, int m_tiles, int bn, int epoch, const int* epoch_dev,
+                                                 const __nv_bfloat16* __restrict__ resid, int ldr) {
+  pdl_trigger();
+  pdl_wait();
+  const int ep = epoch_dev ? *reinterpret_cast<const volatile int*>(epoch_dev) + 1 : epoch;
+  recv += (ep & 1) * half_recv;
+  flags += (ep & 1) * half_flags;
+  const int mt = rank + int(blockIdx.x) * world, t0 = blockIdx.y * 16;
+  const int tile = (t0 / bn) * m_tiles + mt;
+  const int ntiles = m_tiles * ((T + bn - 1) / bn);
+  if (threadIdx.x < world) {
+    const int* f = flags + size_t(threadIdx.x) * ntiles + tile;
+    while (ld_acquire_sys(f) < ep) __nanosleep(32);
+  }
+  __syncthreads();
+  const int t = t0 + (threadIdx.x >> 4);
+  if (t < T) {
+    const int o = mt * SBM + (threadIdx.x & 15) * 8;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    auto add = [&](uint4 v) {
+      a[0] += bf16lo(v.x); a[1] += bf16hi(v.x); a[2] += bf16lo(v.y); a[3] += bf16hi(v.y);
+      a[4] += bf16lo(v.z); a[5] += bf16hi(v.z); a[6] += bf16lo(v.w); a[7] += bf16hi(v.w);
+    };
+    uint4 v[HP_MAX_PEERS];
+#pragma unroll
+    for (int r = 0; r < HP_MAX_PEERS; ++r)
+      if (r < world) v[r] = __ldcg(reinterpret_cast<const uint4*>(recv + (size_t(r) * T + t) * N + o));
+#pragma unroll
+    for (int r = 0; r < HP_MAX_PEERS; ++r)
+      if (r < world) add(v[r]);
+    if (resid) add(*reinterpret_cast<const uint4*>(resid + size_t(t) * ldr + o));
+    const uint4 w =
+        make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+    const size_t off = (ep & 1) * half_gather + size_t(t) * N + o;
+    for (int q = 0; q < world; ++q) *reinterpret_cast<uint4*>(g.buf[q] + off) = w;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const size_t f = (ep & 1) * half_gflags + size_t(blockIdx.y) * m_tiles + mt;
+    for (int q = 0; q < world; ++q) st_relaxed_sys(g.flag[q] + f, ep);  // fenced above
+  }
+}
+
+// Two-shot step 2 (all-gather, local): wait for the owner's flag of every
+// (row block, feature tile) and copy the reduced tile to `out`.  With
+// epoch_dev, the last block advances *epoch_dev.
+__global__ void __launch_bounds__(256) k_peer_ag(const __nv_bfloat16* __restrict__ gather, size_t half_gather,
+                                                 const int* gflags, size_t half_gflags, int T, int N, int m_tiles,
+                                                 int epoch, int* epoch_dev, int* done,
+                                                 __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_trigger();
+  pdl_wait();
+  const int ep = epoch_dev ? *reinterpret_cast<volatile int*>(epoch_dev) + 1 : epoch;
+  const int mt = blockIdx.x, t0 = blockIdx.y * 16;
+  if (threadIdx.x == 0) {
+    const int* f = gflags + (ep & 1) * half_gflags + size_t(blockIdx.y) * m_tiles + mt;
+    while (ld_acquire_sys(f) < ep) __nanosleep(32);
+  }
+  __syncthreads();
+  const int t = t0 + (threadIdx.x >> 4);
+  if (t < T) {
+    const int o = mt * SBM + (threadIdx.x & 15) * 8;
+    *reinterpret_cast<uint4*>(out + size_t(t) * ldo + o) =
+        __ldcg(reinterpret_cast<const uint4*>(gather + (ep & 1) * half_gather + size_t(t) * N + o));
+  }
+  if (epoch_dev) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int nblk = int(gridDim.x * gridDim.y);
+      if (atomicAdd(done, 1) == nblk - 1) {
+        *done = 0;
+        __threadfence();
+        atomicAdd(epoch_dev, 1);
+      }
+    }
+  }
+}
+
 struct PeerArgs {
   void* const* recv;
   size_t half_recv;
@@ -730,6 +829,7 @@ struct PeerArgs {
   size_t half_flags;
   int world, rank, epoch;
   const int* epoch_dev;
+  int two_shot;
 };
 
 static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
@@ -749,14 +849,15 @@ extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void
 extern "C" int hp_gemm_swap_peer(const void* X, int ldx, const void* W, int ldw, int T, int N, int K,
                                  void* const* peer_recv, size_t recv_half_elems, int* const* peer_flags,
                                  size_t flags_half_elems, int world, int rank, int epoch, const int* epoch_dev,
-                                 void* workspace, size_t ws_bytes, int* counters, int n_counters, int max_ctas,
-                                 void* stream) {
+                                 int two_shot, void* workspace, size_t ws_bytes, int* counters, int n_counters,
+                                 int max_ctas, void* stream) {
   HP_CHECK_ARG(peer_recv && peer_flags && world >= 1 && world <= HP_MAX_PEERS && rank >= 0 && rank < world,
                "hp_gemm_swap_peer: bad peer arguments");
   HP_CHECK_ARG(epoch_dev || epoch >= 1, "hp_gemm_swap_peer: host epochs start at 1 and increase per call");
   for (int q = 0; q < world; ++q)
     HP_CHECK_ARG(peer_recv[q] && peer_flags[q], "hp_gemm_swap_peer: null peer buffer");
-  const PeerArgs pa{peer_recv, recv_half_elems, peer_flags, flags_half_elems, world, rank, epoch, epoch_dev};
+  const PeerArgs pa{peer_recv, recv_half_elems, peer_flags, flags_half_elems, world, rank, epoch, epoch_dev,
+                    two_shot ? 1 : 0};
   return gemm_swap_impl(X, ldx, W, ldw, nullptr, 0, nullptr, 0, T, N, K, HP_EPI_PEER, workspace, ws_bytes,
                         counters, n_counters, max_ctas, stream, &pa);
 }
@@ -774,6 +875,45 @@ extern "C" int hp_peer_reduce(const void* recv, size_t recv_half_elems, const in
                 flags_half_elems, world, T, N, m_tiles, swap_bn(T), epoch, epoch_dev, done,
                 static_cast<const __nv_bfloat16*>(resid), ldr, static_cast<__nv_bfloat16*>(out), ldo);
   HP_LAUNCH_CHECK("k_peer_reduce");
+  return HP_OK;
+}
+
+extern "C" int hp_peer_rs(const void* recv, size_t recv_half_elems, const int* flags, size_t flags_half_elems,
+                          void* const* peer_gather, size_t gather_half_elems, int* const* peer_gflags,
+                          size_t gflags_half_elems, int world, int rank, int T, int N, int epoch,
+                          const int* epoch_dev, const void* resid, int ldr, void* stream) {
+  HP_CHECK_ARG(recv && flags && peer_gather && peer_gflags && world >= 1 && world <= HP_MAX_PEERS && rank >= 0 &&
+                   rank < world, "hp_peer_rs: bad arguments");
+  HP_CHECK_ARG(T >= 1 && T <= 256 && N % SBM == 0, "hp_peer_rs: T in [1, 256], N a multiple of 128");
+  HP_CHECK_ARG(resid == nullptr || ldr % 8 == 0, "hp_peer_rs: residual pitch not 16-byte aligned");
+  HP_CHECK_ARG(epoch_dev || epoch >= 1, "hp_peer_rs: host epochs start at 1");
+  const int m_tiles = N / SBM;
+  const int owned = (m_tiles - rank + world - 1) / world;  // feature tiles rank, rank + world, ...
+  if (owned == 0) return HP_OK;
+  PeerPtrs g{};
+  for (int q = 0; q < world; ++q) {
+    HP_CHECK_ARG(peer_gather[q] && peer_gflags[q], "hp_peer_rs: null peer buffer");
+    g.buf[q] = static_cast<__nv_bfloat16*>(peer_gather[q]);
+    g.flag[q] = peer_gflags[q];
+  }
+  HP_LAUNCH_PDL("k_peer_rs", k_peer_rs, dim3(owned, (T + 15) / 16), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const __nv_bfloat16*>(recv), recv_half_elems, flags, flags_half_elems, g,
+                gather_half_elems, gflags_half_elems, world, rank, T, N, m_tiles, swap_bn(T), epoch, epoch_dev,
+                static_cast<const __nv_bfloat16*>(resid), ldr);
+  HP_LAUNCH_CHECK("k_peer_rs");
+  return HP_OK;
+}
+
+extern "C" int hp_peer_ag(const void* gather, size_t gather_half_elems, const int* gflags, size_t gflags_half_elems,
+                          int T, int N, int epoch, int* epoch_dev, int* done, void* out, int ldo, void* stream) {
+  HP_CHECK_ARG(gather && gflags && out, "hp_peer_ag: null pointer");
+  HP_CHECK_ARG(T >= 1 && T <= 256 && N % SBM == 0 && ldo % 8 == 0, "hp_peer_ag: bad shape");
+  HP_CHECK_ARG(epoch_dev ? done != nullptr : epoch >= 1, "hp_peer_ag: device epochs need a zeroed `done` word");
+  const int m_tiles = N / SBM;
+  HP_LAUNCH_PDL("k_peer_ag", k_peer_ag, dim3(m_tiles, (T + 15) / 16), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const __nv_bfloat16*>(gather), gather_half_elems, gflags, gflags_half_elems, T, N,
+                m_tiles, epoch, epoch_dev, done, static_cast<__nv_bfloat16*>(out), ldo);
+  HP_LAUNCH_CHECK("k_peer_ag");
   return HP_OK;
 }
 
@@ -838,6 +978,7 @@ static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* 
     p.world = peer->world;
     p.rank = peer->rank;
     p.epoch = peer->epoch;
+    p.two_shot = peer->two_shot;
   }
   const bool any_split = p.ipc % p.num_kb != 0 || p.ipc < p.num_kb;
   if (any_split) {

@@ -42,8 +42,10 @@ SIGNATURES = {
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_peer_tiles": (_i, [_i, _i]),
-    "hp_gemm_swap_peer": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, _p, _sz, _i, _i, _i, _p, _p, _sz, _p, _i, _i,
-                               _p]),
+    "hp_gemm_swap_peer": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, _p, _sz, _i, _i, _i, _p, _i, _p, _sz, _p, _i,
+                               _i, _p]),
+    "hp_peer_rs": (_i, [_p, _sz, _p, _sz, _p, _sz, _p, _sz, _i, _i, _i, _i, _i, _p, _p, _i, _p]),
+    "hp_peer_ag": (_i, [_p, _sz, _p, _sz, _i, _i, _i, _p, _p, _p, _i, _p]),
     "hp_peer_reduce": (_i, [_p, _sz, _p, _sz, _i, _i, _i, _i, _p, _p, _p, _i, _p, _i, _p]),
     "hp_ipc_handle": (_i, [_p, _p, C.POINTER(_sz)]),
     "hp_ipc_open": (_i, [_p, C.POINTER(_p)]),
@@ -190,7 +192,8 @@ def peer_tiles(T: int, N: int) -> int:
 
 
 def gemm_swap_peer(x, w, peer_recv, recv_half: int, peer_flags, flags_half: int, world: int, rank: int,
-                   epoch: int, epoch_dev, ws, counters, max_ctas: int = 148, stream=None) -> None:
+                   epoch: int, epoch_dev, ws, counters, max_ctas: int = 148, stream=None,
+                   two_shot: bool = False) -> None:
     """Row-parallel decode GEMM whose epilogue scatters this rank's partial
     into every rank's receive buffer; peer_recv / peer_flags: ctypes arrays
     of `world` base device pointers (see include/hp.h hp_gemm_swap_peer);
@@ -198,7 +201,8 @@ def gemm_swap_peer(x, w, peer_recv, recv_half: int, peer_flags, flags_half: int,
     T, K = x.shape
     N = w.shape[0]
     check(load().hp_gemm_swap_peer(_ptr(x), x.stride(0), _ptr(w), w.stride(0), T, N, K, peer_recv, recv_half,
-                                   peer_flags, flags_half, world, rank, epoch, _ptr(epoch_dev), _ptr(ws),
+                                   peer_flags, flags_half, world, rank, epoch, _ptr(epoch_dev), int(two_shot),
+                                   _ptr(ws),
                                    ws.numel() * ws.element_size(), _ptr(counters), counters.numel(), max_ctas,
                                    _stream(stream)), "hp_gemm_swap_peer")
 
@@ -208,6 +212,20 @@ def peer_reduce(recv_ptr: int, recv_half: int, flags_ptr: int, flags_half: int, 
     check(load().hp_peer_reduce(recv_ptr, recv_half, flags_ptr, flags_half, world, T, N, epoch, _ptr(epoch_dev),
                                 _ptr(done), _ptr(resid), resid.stride(0) if resid is not None else 0, _ptr(out),
                                 out.stride(0), _stream(stream)), "hp_peer_reduce")
+
+
+def peer_rs(recv_ptr: int, recv_half: int, flags_ptr: int, flags_half: int, peer_gather, gather_half: int,
+            peer_gflags, gflags_half: int, world: int, rank: int, T: int, N: int, epoch: int, epoch_dev=None,
+            resid=None, stream=None) -> None:
+    check(load().hp_peer_rs(recv_ptr, recv_half, flags_ptr, flags_half, peer_gather, gather_half, peer_gflags,
+                            gflags_half, world, rank, T, N, epoch, _ptr(epoch_dev), _ptr(resid),
+                            resid.stride(0) if resid is not None else 0, _stream(stream)), "hp_peer_rs")
+
+
+def peer_ag(gather_ptr: int, gather_half: int, gflags_ptr: int, gflags_half: int, T: int, N: int, epoch: int,
+            out, epoch_dev=None, done=None, stream=None) -> None:
+    check(load().hp_peer_ag(gather_ptr, gather_half, gflags_ptr, gflags_half, T, N, epoch, _ptr(epoch_dev),
+                            _ptr(done), _ptr(out), out.stride(0), _stream(stream)), "hp_peer_ag")
 
 
 def ipc_handle(t) -> tuple[bytes, int]:

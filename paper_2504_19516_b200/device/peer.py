@@ -20,6 +20,14 @@ step without a host barrier (include/hp.h, hp_gemm_swap_peer).  With
 reduce, advanced by the reduce's last block), so a captured CUDA graph of the
 layer replays correctly; the default host epochs suit eager launches.
 
+`two_shot=True` switches to the bandwidth-optimal form for large batches:
+the GEMM sends each 128-feature tile only to its owner rank (mt % world),
+the owner reduces it and broadcasts the result into every rank's gather
+buffer (hp_peer_rs), and every rank copies the gathered tiles out
+(hp_peer_ag): 2 (world-1)/world of the message per rank instead of
+(world-1) x, one extra hop.  Extra symmetric buffers:
+    gather  bf16 [2][T_max][N]             gflags int [2][ceil(T_max/16)][N/128]
+
 `PeerAllReduce.local_group` builds `world` instances inside ONE process on
 one GPU (all buffers local): the same kernels and flag protocol, used by the
 single-GPU tests and to measure the epilogue's cost; `PeerAllReduce.create`
@@ -39,7 +47,7 @@ from . import lib
 class PeerAllReduce:
     def __init__(self, world: int, rank: int, T_max: int, N: int, recv: torch.Tensor | None,
                  flags: torch.Tensor | None, peer_recv: list[int], peer_flags: list[int], device,
-                 device_epoch: bool = False):
+                 device_epoch: bool = False, gather=None, peer_gather=None, peer_gflags=None):
         if not 1 <= world <= lib.MAX_PEERS:
             raise ValueError(f"world {world} outside [1, {lib.MAX_PEERS}]")
         if not 1 <= T_max <= 256 or N % 128:
@@ -58,6 +66,14 @@ class PeerAllReduce:
         self._ws = None
         # device epoch + the reduce's block counter (both start at zero)
         self.epoch_dev = torch.zeros(2, dtype=torch.int32, device=device) if device_epoch else None
+        self.two_shot = peer_gather is not None
+        if self.two_shot:
+            self.gather = gather  # this rank's (gather, gflags), kept alive
+            self.half_gather = T_max * N
+            self.half_gflags = -(-T_max // 16) * (N // 128)
+            self._peer_gather, self._peer_gflags = peer_gather, peer_gflags
+            self._gv = (C.c_void_p * world)(*peer_gather)
+            self._gf = (C.c_void_p * world)(*peer_gflags)
 
     # ---------------------------------------------------------- construction
     @staticmethod
@@ -66,20 +82,33 @@ class PeerAllReduce:
         flags = torch.zeros(2 * world * lib.peer_tiles(T_max, N), dtype=torch.int32, device=device)
         return recv, flags
 
+    @staticmethod
+    def _alloc_gather(T_max, N, device):
+        gather = torch.empty(2 * T_max * N, dtype=torch.bfloat16, device=device)
+        gflags = torch.zeros(2 * -(-T_max // 16) * (N // 128), dtype=torch.int32, device=device)
+        return gather, gflags
+
     @classmethod
-    def local_group(cls, world: int, T_max: int, N: int, device=None,
-                    device_epoch: bool = False) -> list["PeerAllReduce"]:
+    def local_group(cls, world: int, T_max: int, N: int, device=None, device_epoch: bool = False,
+                    two_shot: bool = False) -> list["PeerAllReduce"]:
         """`world` ranks emulated in one process: every rank's buffers live on
         this GPU and the 'peer' pointers are plain device pointers."""
         device = device or torch.device("cuda", torch.cuda.current_device())
         bufs = [cls._alloc(world, T_max, N, device) for _ in range(world)]
         pr = [r.data_ptr() for r, _ in bufs]
         pf = [f.data_ptr() for _, f in bufs]
-        return [cls(world, q, T_max, N, bufs[q][0], bufs[q][1], pr, pf, device, device_epoch)
-                for q in range(world)]
+        gat = [cls._alloc_gather(T_max, N, device) for _ in range(world)] if two_shot else None
+        pg = [g.data_ptr() for g, _ in gat] if two_shot else None
+        pgf = [f.data_ptr() for _, f in gat] if two_shot else None
+        ranks = [cls(world, q, T_max, N, bufs[q][0], bufs[q][1], pr, pf, device, device_epoch,
+                     gat[q] if two_shot else None, pg, pgf) for q in range(world)]
+        for r in ranks:  # every rank's buffers stay alive as long as any rank's view does
+            r._group_buffers = (bufs, gat)
+        return ranks
 
     @classmethod
-    def create(cls, group, T_max: int, N: int, device=None, device_epoch: bool = False) -> "PeerAllReduce":
+    def create(cls, group, T_max: int, N: int, device=None, device_epoch: bool = False,
+               two_shot: bool = False) -> "PeerAllReduce":
         """One rank of a multi-process TP group: allocate this rank's buffers,
         exchange CUDA IPC handles over `group`, map every peer's buffers."""
         import torch.distributed as dist
@@ -87,21 +116,27 @@ class PeerAllReduce:
         device = device or torch.device("cuda", torch.cuda.current_device())
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         recv, flags = cls._alloc(world, T_max, N, device)
+        own = [recv, flags]
+        gat = cls._alloc_gather(T_max, N, device) if two_shot else None
+        if two_shot:
+            own += list(gat)
         torch.cuda.synchronize(device)
-        mine = (lib.ipc_handle(recv), lib.ipc_handle(flags))
+        mine = tuple(lib.ipc_handle(t) for t in own)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
-        pr, pf, opened = [], [], {}
+        ptrs = [[] for _ in own]  # per buffer kind: one pointer per rank
+        opened = {}
         for q in range(world):
-            if q == rank:
-                pr.append(recv.data_ptr())
-                pf.append(flags.data_ptr())
-                continue
-            for (h, off), dst in zip(allh[q], (pr, pf)):
-                if h not in opened:  # recv and flags may share one allocation block
+            for k, (h, off) in enumerate(allh[q]):
+                if q == rank:
+                    ptrs[k].append(own[k].data_ptr())
+                    continue
+                if h not in opened:  # buffers may share one allocation block
                     opened[h] = lib.ipc_open(h)
-                dst.append(opened[h] + off)
-        self = cls(world, rank, T_max, N, recv, flags, pr, pf, device, device_epoch)
+                ptrs[k].append(opened[h] + off)
+        pr, pf = ptrs[0], ptrs[1]
+        self = cls(world, rank, T_max, N, recv, flags, pr, pf, device, device_epoch, gat,
+                   ptrs[2] if two_shot else None, ptrs[3] if two_shot else None)
         self._opened = list(opened.values())
         dist.barrier(group=group)
         return self
@@ -127,15 +162,31 @@ class PeerAllReduce:
         ws, cnt = self.workspace(x.shape[1], max_ctas)
         lib.gemm_swap_peer(x, w, C.cast(self._rv, C.c_void_p), self.half_recv, C.cast(self._fl, C.c_void_p),
                            self.half_flags, self.world, self.rank, epoch, self._edev(), ws, cnt,
-                           max_ctas=max_ctas, stream=stream)
+                           max_ctas=max_ctas, stream=stream, two_shot=self.two_shot)
 
     def reduce(self, out, epoch: int, resid=None, stream=None) -> None:
-        """Receive half: out = sum over ranks of the partials (+ resid)."""
+        """Receive half: out = sum over ranks of the partials (+ resid).
+        Two-shot: reduce_scatter() then all_gather() (separate launches)."""
+        if self.two_shot:
+            self.reduce_scatter(out.shape[0], epoch, resid, stream)
+            self.all_gather(out, epoch, stream)
+            return
         T = out.shape[0]
         e = self._edev()
         lib.peer_reduce(self._peer_recv[self.rank], self.half_recv, self._peer_flags[self.rank], self.half_flags,
                         self.world, T, self.N, epoch, out, resid=resid, epoch_dev=e,
                         done=None if e is None else self.epoch_dev[1:], stream=stream)
+
+    def reduce_scatter(self, T: int, epoch: int, resid=None, stream=None) -> None:
+        lib.peer_rs(self._peer_recv[self.rank], self.half_recv, self._peer_flags[self.rank], self.half_flags,
+                    C.cast(self._gv, C.c_void_p), self.half_gather, C.cast(self._gf, C.c_void_p), self.half_gflags,
+                    self.world, self.rank, T, self.N, epoch, epoch_dev=self._edev(), resid=resid, stream=stream)
+
+    def all_gather(self, out, epoch: int, stream=None) -> None:
+        e = self._edev()
+        lib.peer_ag(self._peer_gather[self.rank], self.half_gather, self._peer_gflags[self.rank], self.half_gflags,
+                    out.shape[0], self.N, epoch, out, epoch_dev=e, done=None if e is None else self.epoch_dev[1:],
+                    stream=stream)
 
     def _edev(self):
         return None if self.epoch_dev is None else self.epoch_dev[:1]

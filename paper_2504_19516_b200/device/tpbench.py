@@ -40,6 +40,7 @@ def main(argv=None) -> int:
     ap.add_argument("--fused", action="store_true",
                     help="decode all-reduces fused into the o_proj/mlp_down epilogues (device/peer.py); on 1 GPU "
                          "the tp ranks' receive buffers are emulated locally and peers' flags pre-raised")
+    ap.add_argument("--two-shot", action="store_true", help="with --fused: reduce-scatter + all-gather form")
     a = ap.parse_args(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -70,10 +71,12 @@ def main(argv=None) -> int:
         from .peer import PeerAllReduce
 
         if world > 1:
-            dl.peer = PeerAllReduce.create(groups[1], B, s.hidden, dev)
+            dl.peer = PeerAllReduce.create(groups[1], B, s.hidden, dev, device_epoch=True, two_shot=a.two_shot)
         else:  # rank 0's view of a tp-rank group: scatter to tp local buffers, peers' flags pre-raised
-            dl.peer = PeerAllReduce.local_group(tp, B, s.hidden, dev)[0]
+            dl.peer = PeerAllReduce.local_group(tp, B, s.hidden, dev, device_epoch=True, two_shot=a.two_shot)[0]
             dl.peer.flags.fill_(2 ** 31 - 1)
+            if a.two_shot:
+                dl.peer.gather[1].fill_(2 ** 31 - 1)
     bf = dict(dtype=torch.bfloat16, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
     px, py = torch.randn(T, s.hidden, **bf), torch.empty(T, s.hidden, **bf)
@@ -95,8 +98,23 @@ def main(argv=None) -> int:
     def run_p(st):
         pl.prefill(px, py, cu, 1, T, ppos, ppos, kc, vc, st.sms, st.torch_stream)
 
+    graphs = {}
+
     def run_d(st):
-        dl.decode(dx, dy, ctx, dpos, dslots, bt, kc, vc, st.sms, st.torch_stream, ws=ws)
+        """One decode layer-step, replayed from a CUDA graph captured on the
+        phase's stream (eager launches of ~12 kernels are host-bound; the
+        fused all-reduce uses device epochs so its graph replays)."""
+        key = (st.stream, st.sms)
+        if key not in graphs:
+            with torch.cuda.stream(st.torch_stream):
+                dl.decode(dx, dy, ctx, dpos, dslots, bt, kc, vc, st.sms, st.torch_stream, ws=ws)  # warm
+                st.torch_stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st.torch_stream):
+                    dl.decode(dx, dy, ctx, dpos, dslots, bt, kc, vc, st.sms, st.torch_stream, ws=ws)
+            torch.cuda.synchronize()
+            graphs[key] = g
+        graphs[key].replay()
 
     def timed(fn, st):
         with torch.cuda.stream(st.torch_stream):
@@ -137,7 +155,8 @@ def main(argv=None) -> int:
         print(json.dumps({
             "config": f"llama3-70b layer TP={tp}: chunked prefill {T} + decode batch {B} ctx {C}",
             "world": world,
-            "collective": ("decode: fused GEMM-epilogue peer all-reduce x2 per layer; prefill: " if a.fused else "")
+            "collective": (f"decode: fused GEMM-epilogue peer all-reduce ({'two' if a.two_shot else 'one'}-shot) x2 "
+                           "per layer; prefill: " if a.fused else "")
             + ("nccl all-reduce x2 per layer" if world > 1 else
                "none (1 GPU: rank-0 shard compute only" + (", fused epilogue scatter to tp local buffers)"
                                                            if a.fused else ")")),

@@ -39,13 +39,27 @@ def _unfused(xs, ws_t, resid, sms):
     return acc.to(torch.bfloat16)
 
 
+def _receive(ranks, outs, epoch, resid):
+    """Every rank's receive side, in an order one stream can run: two-shot
+    needs every owner's reduce-scatter before any rank's all-gather."""
+    if ranks[0].two_shot:
+        for r, pr in enumerate(ranks):
+            pr.reduce_scatter(outs[r].shape[0], epoch, resid=resid)
+        for r, pr in enumerate(ranks):
+            pr.all_gather(outs[r], epoch)
+    else:
+        for r, pr in enumerate(ranks):
+            pr.reduce(outs[r], epoch, resid=resid)
+
+
 @pytest.mark.parametrize("world", [2, 8])
 @pytest.mark.parametrize("T", [1, 32, 100, 256])
 @pytest.mark.parametrize("sms", [8, 148])
-def test_fused_allreduce_matches_unfused(world, T, sms):
+@pytest.mark.parametrize("two_shot", [False, True], ids=["one_shot", "two_shot"])
+def test_fused_allreduce_matches_unfused(world, T, sms, two_shot):
     N, K = 1024, 512
     g = torch.Generator(device="cpu").manual_seed(world * 1000 + T + sms)
-    ranks = PeerAllReduce.local_group(world, 256, N, DEV)
+    ranks = PeerAllReduce.local_group(world, 256, N, DEV, two_shot=two_shot)
     for call in range(3):  # both buffer halves, epochs 1..3
         xs = [torch.randn(T, K, generator=g).to(torch.bfloat16).to(DEV) for _ in range(world)]
         wd = [(torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16) for _ in range(world)]
@@ -53,10 +67,9 @@ def test_fused_allreduce_matches_unfused(world, T, sms):
         resid = torch.randn(T, N, generator=g).to(torch.bfloat16).to(DEV) if call != 1 else None
         outs = [torch.full((T, N), float("nan"), dtype=torch.bfloat16, device=DEV) for _ in range(world)]
         epoch = call + 1
-        for r in range(world):  # every rank's GEMM, then every rank's reduce (one stream)
+        for r in range(world):  # every rank's GEMM, then every rank's receive side (one stream)
             ranks[r].gemm(xs[r], ws_t[r], epoch, max_ctas=sms)
-        for r in range(world):
-            ranks[r].reduce(outs[r], epoch, resid=resid)
+        _receive(ranks, outs, epoch, resid)
         torch.cuda.synchronize()
         ref = _unfused(xs, ws_t, resid, sms)
         for r in range(world):
@@ -97,13 +110,14 @@ def test_fused_allreduce_rejects_bad_shapes():
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_fused_allreduce_device_epochs_replay_in_a_cuda_graph(world):
+@pytest.mark.parametrize("two_shot", [False, True], ids=["one_shot", "two_shot"])
+def test_fused_allreduce_device_epochs_replay_in_a_cuda_graph(world, two_shot):
     """device_epoch=True: the epoch lives on the device, so one captured graph
     of every rank's GEMM + reduce replays call after call (alternating buffer
     halves) and stays bit-identical to the unfused path."""
     N, K, T = 1024, 512, 48
     g = torch.Generator(device="cpu").manual_seed(77 + world)
-    ranks = PeerAllReduce.local_group(world, 64, N, DEV, device_epoch=True)
+    ranks = PeerAllReduce.local_group(world, 64, N, DEV, device_epoch=True, two_shot=two_shot)
     ws_t = [lib.tile_weight((torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16).to(DEV))
             for _ in range(world)]
     xs = [torch.empty(T, K, dtype=torch.bfloat16, device=DEV) for _ in range(world)]
@@ -113,8 +127,7 @@ def test_fused_allreduce_device_epochs_replay_in_a_cuda_graph(world):
     def step():
         for r in range(world):
             ranks[r].gemm(xs[r], ws_t[r], 0, max_ctas=32)
-        for r in range(world):
-            ranks[r].reduce(outs[r], 0, resid=resid)
+        _receive(ranks, outs, 0, resid)
 
     def fill():
         for x in xs:

@@ -49,6 +49,7 @@ def _free_port():
 
 
 def _rank(rank, world, port, q, fused=False):
+    two_shot = fused == "two_shot"
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2504_19516_b200.device import lib
@@ -74,7 +75,7 @@ def _rank(rank, world, port, q, fused=False):
     if fused:  # decode all-reduces through the GEMM epilogue over CUDA IPC peer memory
         from paper_2504_19516_b200.device.peer import PeerAllReduce
 
-        lyr.peer = PeerAllReduce.create(dist.group.WORLD, B, H, dev)
+        lyr.peer = PeerAllReduce.create(dist.group.WORLD, B, H, dev, two_shot=two_shot)
     kvh = HKV // world
     pages = -(-T // 64)
     kc = torch.zeros(pages + B * 4, kvh, 64, D, dtype=torch.bfloat16, device=dev)
@@ -104,7 +105,7 @@ def _rank(rank, world, port, q, fused=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fused", [False, True], ids=["nccl_style", "fused_peer"])
+@pytest.mark.parametrize("fused", [False, True, "two_shot"], ids=["nccl_style", "fused_peer", "fused_two_shot"])
 def test_tp2_layer_on_device_matches_oracle(fused):
     world = 2
     ctx = mp.get_context("spawn")
