@@ -1,5 +1,7 @@
 """Fused TP all-reduce microbench: rank 0 of an emulated `world`-rank group (peers' flags pre-raised),
 one linear replayed from a CUDA graph vs the plain gemm_swap.  args: world T N K sms [reps]"""
+import sys
+
 import torch
 sys.path.insert(0, ".")
 from paper_2504_19516_b200.device import lib
