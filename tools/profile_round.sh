@@ -27,4 +27,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fa
     -o $OUT/prefill_attn python tools/one_kernel.py attn4096 $PM 3 > $OUT/ncu_fa.out 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_swap -s 2 -c 1 \
     -o $OUT/swap_o python tools/one_kernel.py swap 148 4 > $OUT/ncu_swap.out 2>&1
+# the decode partition's view: CTA-pair decode GEMM (mlp_up_gate) and decode attention on 8 SMs
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_swap -s 2 -c 1 \
+    -o $OUT/swap_ug8 python tools/one_kernel.py swap_ug 8 4 > $OUT/ncu_swap8.out 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_decode_attn -s 2 -c 1 \
+    -o $OUT/decode_attn8 python tools/one_kernel.py decode_attn 8 4 > $OUT/ncu_dattn8.out 2>&1
 ls -la $OUT
