@@ -96,3 +96,24 @@ def test_mlp_width_realises_activated_fraction():
     assert mlp_width(MODEL_PRESETS["moe-a22b"]) == 1280  # 0.1 x 12288, rounded to the 128-row tile
     assert mlp_width(ModelSpec("m", 1, 4096, 32, 8, 128, 14336, activated_fraction=0.5)) == 7168
     assert mlp_width(ModelSpec("m", 1, 4096, 32, 8, 128, 1024, activated_fraction=0.01)) == 128
+
+
+def test_header_is_plain_c_and_cxx(tmp_path):
+    """include/hp.h is the drop-in boundary: it must compile as C99 (a cgo /
+    ctypes consumer) and as C++17, with no torch or CUDA types."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    src = tmp_path / "use_hp.c"
+    src.write_text('#include "hp.h"\nint main(void) { return hp_abi_version() == HP_ABI_VERSION ? 0 : 1; }\n')
+    for cc, args in (("gcc", ["-std=c99"]), ("g++", ["-std=c++17", "-x", "c++"])):
+        if shutil.which(cc) is None:
+            continue
+        r = subprocess.run([cc, *args, "-fsyntax-only", "-Wall", "-Werror", f"-I{root / 'include'}", str(src)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+    code = [ln for ln in (root / "include" / "hp.h").read_text().splitlines()
+            if ln.strip() and not ln.strip().startswith(("/*", "*", "//"))]
+    assert not any("torch" in ln or "#include <cuda" in ln for ln in code)
