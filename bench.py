@@ -243,12 +243,22 @@ def main(argv=None) -> int:
 
     import torch
 
+    # HP_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 with gloo
+    # collectives, to exercise the N > 1 path on a one-GPU box; the numbers of
+    # such a run mean nothing (the ranks share one GPU)
+    shared = os.environ.get("HP_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+    coll = "cpu" if shared else "cuda"
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
 
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist_mod.init_process_group("gloo")
+        else:
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
 
     from paper_2504_19516_b200.device.corun import CoRunner
@@ -284,7 +294,7 @@ def main(argv=None) -> int:
     ok = [c for c in candidates if c["slo_ok"]] or candidates
     best = max(ok, key=lambda c: c["tokens_per_s"])
     if dist is not None:  # identical split on every replica (rank 0 decides)
-        dmv, nv = agree_split(dist, best["dm"], best["n"], "cuda")
+        dmv, nv = agree_split(dist, best["dm"], best["n"], coll)
         best = next((c for c in candidates if c["dm"] == dmv and c["n"] == nv),
                     dict(best, dm=dmv, pm=N - dmv, n=nv))
     pm, dm, n = best["pm"], best["dm"], best["n"]
@@ -307,7 +317,7 @@ def main(argv=None) -> int:
         res = cr.corun(pm, dm, args.steps, n, time_upgate=True)  # events around mlp_up_gate only
         torch.cuda.nvtx.range_end(rid)
     torch.cuda.synchronize()
-    span, tokens = job_totals(dist, res.span_s, res.tokens, "cuda")
+    span, tokens = job_totals(dist, res.span_s, res.tokens, coll)
     if dist is not None:
         dist.barrier()
     value = tokens / span
@@ -322,7 +332,7 @@ def main(argv=None) -> int:
     pin_dx.copy_(cr.dx.cpu())
 
     e2e_res = cr.corun_e2e(pm, dm, args.steps, n, pin_px, pin_py, pin_dx, pin_dy)
-    e2e_span, e2e_tokens = job_totals(dist, e2e_res.span_s, e2e_res.tokens, "cuda")
+    e2e_span, e2e_tokens = job_totals(dist, e2e_res.span_s, e2e_res.tokens, coll)
     h2d = T * h * 2 + n * DECODE_BATCH * h * 2
     d2h = h2d
 
