@@ -231,7 +231,10 @@ int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache, const void
 /* Paged decode attention (workload.py:184-188): one query token per
  * sequence over ctx_lens[b] cached positions.  q: [B, Hq*d]; out: [B, Hq*d];
  * block_table: int [B, max_pages]; workspace: fp32, hp_decode_attn_ws_bytes.
- * GQA group Hq/Hkv <= 8, or a multiple of 8 (run as Hq/Hkv/8 head blocks). */
+ * GQA group Hq/Hkv <= 8, or a multiple of 8 (run as Hq/Hkv/8 head blocks).
+ * Precondition: 1 <= ctx_lens[b] <= max_pages * page (the row's pages must
+ * hold the context); the kernels clamp a longer ctx_lens[b] to that bound
+ * rather than read past the block-table row or the split workspace. */
 size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits);
 /* Kernel launches hp_decode_attn issues for this shape (2 when the context
  * is split and a log-sum-exp combine follows; bounded by the workspace). */

@@ -148,10 +148,12 @@ class LayerWeights:
 
 
 def layer_prefill(x: np.ndarray, W: LayerWeights, Hq: int, Hkv: int, d: int, pos: np.ndarray,
-                  table: np.ndarray, bf16_boundaries: bool = True):
+                  table: np.ndarray, bf16_boundaries: bool = True, trace: dict | None = None):
     """One prefill layer over a single sequence's new span (no cached prefix).
 
-    Returns (y, k_rot, v): the layer output and the K/V rows written to cache."""
+    Returns (y, k_rot, v): the layer output and the K/V rows written to cache.
+    `trace`: if a dict, receives the stored intermediates q (roped), attn,
+    h (residual after o_proj) and act (SwiGLU output) for per-tensor parity."""
     rb = bf16_boundaries
     T = x.shape[0]
     qkv = _b(_b(rmsnorm(x, W.attn_norm), rb) @ W.w_qkv.T, rb)
@@ -165,15 +167,17 @@ def layer_prefill(x: np.ndarray, W: LayerWeights, Hq: int, Hkv: int, d: int, pos
     n2 = _b(rmsnorm(h, W.mlp_norm), rb)
     act = _b(silu(n2 @ W.w_gate.T) * (n2 @ W.w_up.T), rb)
     y = _b(h + act @ W.w_down.T, rb)
+    if trace is not None:
+        trace.update(q=q.reshape(T, Hq * d), attn=a, h=h, act=act)
     return y, k, v
 
 
 def layer_decode(x: np.ndarray, W: LayerWeights, Hq: int, Hkv: int, d: int, ctx_lens: np.ndarray,
                  table: np.ndarray, kcache: np.ndarray, vcache: np.ndarray, block_table: np.ndarray,
-                 bf16_boundaries: bool = True) -> np.ndarray:
+                 bf16_boundaries: bool = True, trace: dict | None = None) -> np.ndarray:
     """One decode layer step for B sequences: the new token of sequence b sits
     at position ctx_lens[b]-1; its K/V are written into the (mutated) caches
-    before attention over ctx_lens[b] positions."""
+    before attention over ctx_lens[b] positions.  `trace`: as layer_prefill."""
     rb = bf16_boundaries
     B = x.shape[0]
     page = kcache.shape[2]
@@ -191,6 +195,8 @@ def layer_decode(x: np.ndarray, W: LayerWeights, Hq: int, Hkv: int, d: int, ctx_
     h = _b(x + a @ W.w_o.T, rb)
     n2 = _b(rmsnorm(h, W.mlp_norm), rb)
     act = _b(silu(n2 @ W.w_gate.T) * (n2 @ W.w_up.T), rb)
+    if trace is not None:
+        trace.update(q=q.reshape(B, Hq * d), attn=a, h=h, act=act)
     return _b(h + act @ W.w_down.T, rb)
 
 

@@ -102,6 +102,13 @@ struct DecodeParams {
   float* ws_ml;     // [B, Hq, max_splits, 2]
 };
 
+// Context length of sequence b, clamped to what its block-table row can
+// address (max_pages * page): a longer ctx_lens[b] (a caller bug, see hp.h)
+// must not index split slots past max_splits or pages past the row.
+__device__ __forceinline__ int da_ctx(const DecodeParams& p, int b) {
+  return max(0, min(p.ctx_lens[b], p.max_pages * p.page));
+}
+
 struct UnitId {
   int b, kvh, s, hb;
 };
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
         const int j = first + r * 32 + lane;
         w[r] = j < last ? row[j] : 0;
       }
-      return p.ctx_lens[id.b];
+      return da_ctx(p, id.b);
     };
     uint32_t hbase = 0;
     int u = blockIdx.x;
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
 
   auto load_q = [&](int u, uint32_t (&qf)[NB][KK][2], int& ctx) {
     const UnitId id = unit_of(p, u);
-    ctx = p.ctx_lens[id.b];
+    ctx = da_ctx(p, id.b);
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
       const int hl = nb * 8 + g8;  // head within the unit
@@ -493,7 +500,7 @@ __global__ void k_decode_combine(const DecodeParams p) {
   if (warp_global >= p.B * p.Hq) return;
   const int b = warp_global / p.Hq;
   const int head = warp_global % p.Hq;
-  const int ntiles = (p.ctx_lens[b] + DA_TILE - 1) / DA_TILE;
+  const int ntiles = (da_ctx(p, b) + DA_TILE - 1) / DA_TILE;
   const int nsplit = (ntiles + p.tps - 1) / p.tps;
   if (nsplit <= 1) return;  // written directly by the main kernel
   const size_t base = (size_t(b) * p.Hq + head) * p.max_splits;

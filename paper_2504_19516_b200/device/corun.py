@@ -51,6 +51,17 @@ class CoRunResult:
     decode_layer_s: list = field(default_factory=list)    # per decode layer-step
     upgate_s: list = field(default_factory=list)          # dominant kernel launches
     group_s: dict = field(default_factory=dict)           # median seconds per prefill kernel group
+    prefill_window_s: list = field(default_factory=list)  # (start, end) of each prefill layer from t0
+    decode_window_s: list = field(default_factory=list)   # (start, end) of each decode layer-step
+
+    def overlap_s(self) -> float:
+        """Seconds during which a decode step ran while a prefill layer was
+        running (the co-execution actually happened on the device)."""
+        tot = 0.0
+        for a0, a1 in self.prefill_window_s:
+            for b0, b1 in self.decode_window_s:
+                tot += max(0.0, min(a1, b1) - max(a0, b0))
+        return tot
 
     def partition_idle(self, n: int) -> float:
         """SM idle fraction of the co-run: 1 - (pm * prefill busy + dm *
@@ -72,7 +83,8 @@ class CoRunResult:
 
 class CoRunner:
     def __init__(self, model: ModelSpec, prefill_tokens: int, decode_batch: int, decode_ctx: int,
-                 device: int = 0, seed: int = 0, pool: PartitionPool | None = None):
+                 device: int = 0, seed: int = 0, pool: PartitionPool | None = None,
+                 weights: LayerWeights | None = None):
         self.model = model
         self.dev = torch.device("cuda", device)
         self.T = prefill_tokens
@@ -80,8 +92,9 @@ class CoRunner:
         self.C = decode_ctx
         gen = torch.Generator(device="cpu")
         gen.manual_seed(seed)
-        self.layer = DeviceLayer(model, LayerWeights.random(model, self.dev, gen), self.dev,
-                                 max_pos=max(prefill_tokens, decode_ctx) + 1)
+        if weights is None:
+            weights = LayerWeights.random(model, self.dev, gen)
+        self.layer = DeviceLayer(model, weights, self.dev, max_pos=max(prefill_tokens, decode_ctx) + 1)
         self.pool = pool or PartitionPool(device)
         self.n = self.pool.n
         h = model.hidden
@@ -112,6 +125,26 @@ class CoRunner:
         self.dy = torch.empty(self.B, h, **bf)
         self.dsc = DecodeScratch(model, self.B, pages, self.dev, max_ctas=self.n)
         self._graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
+        torch.cuda.synchronize()
+
+    def load(self, px=None, dx=None, kcache=None, vcache=None, block_table=None) -> None:
+        """Overwrite workload inputs in place (captured decode graphs keep
+        their pointers): prefill input [T, h], decode input [B, h], logical
+        K/V caches [blocks, Hkv, page, d] (packed here into the device page
+        layout) and the decode block table [B, pages]."""
+        if px is not None:
+            self.px.copy_(px)
+        if dx is not None:
+            self.dx.copy_(dx)
+        if kcache is not None:
+            self.dcache.k[: kcache.shape[0]].copy_(lib.kv_pack(kcache))
+        if vcache is not None:
+            self.dcache.v[: vcache.shape[0]].copy_(lib.kv_pack(vcache))
+        if block_table is not None:
+            self.block_table.copy_(block_table)
+            pos, slots = decode_slots(self.block_table, self.ctx)
+            self.d_pos.copy_(pos)
+            self.d_slots.copy_(slots)
         torch.cuda.synchronize()
 
     # ------------------------------------------------------------- launches
@@ -215,6 +248,8 @@ class CoRunner:
                           steps * decode_per_step * self.B)
         res.prefill_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in p_ev]
         res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
+        res.prefill_window_s = [(start.elapsed_time(a) * 1e-3, start.elapsed_time(b) * 1e-3) for a, b in p_ev]
+        res.decode_window_s = [(start.elapsed_time(a) * 1e-3, start.elapsed_time(b) * 1e-3) for a, b in d_ev]
         if ug_ev:
             res.upgate_s = [a.elapsed_time(b) * 1e-3 for a, b in (e["mlp_up_gate"] for e in ug_ev)]
             res.group_s = {g: statistics.median(e[g][0].elapsed_time(e[g][1]) * 1e-3 for e in ug_ev)

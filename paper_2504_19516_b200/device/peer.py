@@ -64,6 +64,7 @@ class PeerAllReduce:
         self._opened: list[int] = []
         self.epoch = 0
         self._ws = None
+        self._ws_retired: list = []  # outgrown workspaces, kept alive for captured graphs
         # device epoch + the reduce's block counter (both start at zero)
         self.epoch_dev = torch.zeros(2, dtype=torch.int32, device=device) if device_epoch else None
         self.two_shot = peer_gather is not None
@@ -111,8 +112,16 @@ class PeerAllReduce:
                two_shot: bool = False) -> "PeerAllReduce":
         """One rank of a multi-process TP group: allocate this rank's buffers,
         exchange CUDA IPC handles over `group`, map every peer's buffers."""
+        import os
+
         import torch.distributed as dist
 
+        conf = os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "") + "," + os.environ.get("PYTORCH_ALLOC_CONF", "")
+        if "expandable_segments:true" in conf.replace(" ", "").lower():
+            # expandable segments are cuMemCreate (VMM) allocations, which
+            # legacy cudaIpcGetMemHandle cannot export
+            raise RuntimeError("PeerAllReduce.create: CUDA IPC of caching-allocator blocks does not work "
+                               "with PYTORCH_CUDA_ALLOC_CONF=expandable_segments:True; unset it")
         device = device or torch.device("cuda", torch.cuda.current_device())
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         recv, flags = cls._alloc(world, T_max, N, device)
@@ -148,10 +157,19 @@ class PeerAllReduce:
 
     # ------------------------------------------------------------------ call
     def workspace(self, K: int, max_ctas: int):
-        nb = lib.gemm_swap_ws_bytes(256, self.N, K, max_ctas)
+        """Stream-K workspace + arrival counters for a K-deep GEMM.  Sized for
+        148 CTAs (any partition) and grown only for a deeper K; a replaced
+        workspace is retained, never freed, because CUDA graphs captured
+        earlier (e.g. on a smaller partition) keep its pointers.  A new
+        workspace's zeroed counters are made visible to every stream before
+        first use (the GEMM may run on a green-context stream)."""
+        nb = lib.gemm_swap_ws_bytes(256, self.N, K, max(max_ctas, 148))
         if self._ws is None or self._ws[0].numel() * 4 < nb:
+            if self._ws is not None:
+                self._ws_retired.append(self._ws)
             self._ws = (torch.empty(nb // 4 + 1, dtype=torch.float32, device=self.dev),
                         torch.zeros(self.N // 128 * 8, dtype=torch.int32, device=self.dev))
+            torch.cuda.synchronize(self.dev)
         return self._ws
 
     def gemm(self, x, w, epoch: int, max_ctas: int = 148, stream=None) -> None:
