@@ -1,18 +1,28 @@
 """Benchmark: co-executed prefill + decode on SM partitions of one B200
-(BASELINE.json config 2, Llama-3-8B single layer, bf16).
+(BASELINE.json config 2: Llama-3-8B single layer, bf16, prefill chunk sweep
+1024/2048/4096/16384 co-run with decode batch 32 at context 2048).
 
-One STEP = one prefill layer over a T-token chunk (default 4096) on a
-green-context partition of pm SMs, co-executed with n decode layer-steps
-(batch 32, context 2048, paged KV) on the remaining dm SMs.  n is the number
-of decode steps that fit in one prefill layer at that split.  The split
-(pm, dm) is chosen during warm-up on the 8-SM green-context grid: the
-highest tokens/s whose p50 TTFT/TPOT proxies are no worse than the
-time-sliced baseline's (same kernels, one full-GPU stream, prefill layer and
-decode step alternating).
+One STEP = one prefill layer over a T-token chunk on a green-context
+partition of pm SMs, co-executed with the decode layer-steps (batch 32,
+context 2048, paged KV, one CUDA graph per step) that run continuously on
+the other dm SMs meanwhile (r decode steps per prefill layer on average,
+r = measured co-run prefill-layer / decode-step time).
 
-Metric: tokens/s = (T + 32 n) per step / device time (layer-tokens; divide by
-32 layers for model-equivalent tokens).  Inputs (weights 436 MB + KV 269 MB
-+ activations per step) exceed the 126 MB L2, so no explicit flush.
+The split (pm, dm) is chosen by the reference's estimator and Algorithm 1
+(device/split.py: `min_decode_sms`, else `set_balanced_sm`, on the B200
+calibration tables), with SLO targets = the time-sliced baseline's
+latencies; a brute-force sweep over the 8-SM grid is reported beside it as a
+regret check.  Time-sliced baseline: the same kernels and the same work on
+one full-GPU stream (prefill layer, then its decode steps).  Chunked
+baseline: lockstep hybrid batches at chunk 1024 / 2048 (SGLang-style).
+
+Metric: layer-tokens/s = (prefill tokens + 32 x decode steps) / device time
+for ONE layer (a Llama-3-8B model has 32: model-equivalent tokens/s =
+value / 32, also reported).  TTFT / TPOT are per layer: mean prefill
+progress per layer and mean time per decode layer-step.  Every config-2 T is
+measured (`per_T`); the headline is T = 4096 (--prefill-tokens).  Inputs
+(weights 436 MB + KV 269 MB + activations per step) exceed the 126 MB L2,
+so no explicit flush.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -26,6 +36,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -37,8 +48,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "tokens/sec with co-executed prefill+decode per B200; p50 TTFT/TPOT; SM idle %"
-UNIT = "tokens/s"
+UNIT = "layer-tokens/s"
 DECODE_BATCH, DECODE_CTX = 32, 2048
+SWEEP_T = (1024, 2048, 4096, 16384)
 
 
 def _peaks():
@@ -47,6 +59,15 @@ def _peaks():
         d = json.loads(p.read_text())
         return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
     return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def config_of(model_name: str, T: int, world: int) -> dict:
+    """The workload both arms (GPU and reference CPU) run: identical dicts."""
+    return {"workload": f"{model_name} 1 layer: prefill chunk {T} tok co-run with decode batch "
+                        f"{DECODE_BATCH} ctx {DECODE_CTX}",
+            "model": f"{model_name} (1 layer)", "prefill_tokens": T, "decode_batch": DECODE_BATCH,
+            "decode_ctx": DECODE_CTX, "parallelism": f"replicas x{world}",
+            "l2": "inputs exceed L2 (weights+KV 1.1 GB/step), no flush"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -117,17 +138,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+
 # ------------------------------------------------------------- CPU oracle
-def cpu_reference_step(T: int, B: int, C: int, seed: int = 0, model: str = "llama3-8b"):
-    """Time one bounded sample of the workload with the numpy CPU oracle:
-    one Llama-3-8B prefill layer over T tokens + one decode layer-step for
-    B sequences of context C.  Returns (seconds, tokens)."""
+def cpu_reference_step(T: int, B: int, C: int, seed: int = 0, model: str = "llama3-8b",
+                       decode_steps: int = 1):
+    """Time one sample of the workload with the numpy CPU oracle (the
+    reference path's CPU implementation; the reference itself has no
+    numerics): one prefill layer over T tokens + `decode_steps` decode
+    layer-steps for B sequences of context C.  Returns (seconds, tokens)."""
     import numpy as np
 
     from oracle import numerics as O
-    from paper_2504_19516_b200.workload import MODEL_PRESETS
-
     from paper_2504_19516_b200.device.layer import mlp_width
+    from paper_2504_19516_b200.workload import MODEL_PRESETS
 
     m = MODEL_PRESETS[model]
     rng = np.random.default_rng(seed)
@@ -148,8 +171,9 @@ def cpu_reference_step(T: int, B: int, C: int, seed: int = 0, model: str = "llam
     xd = rng.standard_normal((B, h), dtype=np.float32)
     t0 = time.perf_counter()
     O.layer_prefill(x, W, Hq, Hkv, d, np.arange(T), table, bf16_boundaries=False)
-    O.layer_decode(xd, W, Hq, Hkv, d, ctx, table, kc, vc, bt, bf16_boundaries=False)
-    return time.perf_counter() - t0, T + B
+    for _ in range(decode_steps):
+        O.layer_decode(xd, W, Hq, Hkv, d, ctx, table, kc, vc, bt, bf16_boundaries=False)
+    return time.perf_counter() - t0, T + decode_steps * B
 
 
 def cpu_threads() -> int:
@@ -163,46 +187,116 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-CPU_SAMPLE_T = 512
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=5).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def control_plane_timings(model_name: str = "llama3-8b") -> dict:
+    """the reference control plane on ONE core (pure
+    Python; this package's restatement is decision-identical to the
+    reference, tests/test_golden_parity.py): estimate_latency /
+    schedule_prefill / set_balanced_sm / min_decode_sms us per call at N =
+    148, sm_step 8 on the config-2 state, and the serving simulator's wall
+    time (engine.run, synthetic oracle) on the config-1 and config-4 traces."""
+    from paper_2504_19516_b200 import engine as E
+    from paper_2504_19516_b200 import scheduler as S
+    from paper_2504_19516_b200.device.split import b200_gpu, b200_store, corun_state
+    from paper_2504_19516_b200.perf_model import ExecutionState, PerfEstimator, estimate_latency
+    from paper_2504_19516_b200.workload import (MODEL_PRESETS, TINY_MODEL, LengthDist, Request, TRACE_PRESETS,
+                                               gen_poisson_trace)
+
+    m = MODEL_PRESETS[model_name]
+    gpu, store = b200_gpu(), b200_store()
+    est = PerfEstimator(m, gpu, store)
+    slo = S.SloSpec(norm_ttft_s_per_token=1.5e-3, tpot_s=0.2)
+    cfg = S.SchedulerConfig(sm_step=8)
+    es = ExecutionState(prefill_lens=(4096,), prefill_sms=116, decode_ctx_lens=(2048,) * 32, decode_sms=32)
+
+    def per_call(fn, reps):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        return 1e6 * (time.perf_counter() - t0) / reps
+
+    st = corun_state(4096, [2048] * 32, gpu.num_sms, dm0=32)
+    st.tpot_window = tuple([0.05] * 64)
+    out = {"estimate_latency_us": per_call(lambda: estimate_latency(es, m, gpu, store), 300),
+           "schedule_prefill_us": per_call(lambda: S.schedule_prefill(st, slo, est, cfg), 50),
+           "set_balanced_sm_us": per_call(lambda: S.set_balanced_sm(st, slo, est, cfg), 50),
+           "min_decode_sms_us": per_call(lambda: S.min_decode_sms(st, slo, est, cfg), 100),
+           "state": "N=148, sm_step 8, prefill 4096 tok in flight, decode 32 x ctx 2048"}
+    sim = {}
+    c1 = [Request(0, 0.0, 1024, 16)] + [Request(i + 1, 0.0, c, 16) for i, c in
+                                        enumerate((17, 64, 128, 255, 256, 511, 512, 1000))]
+    c4 = gen_poisson_trace(4.0, 20.0, LengthDist("uniform", lo=512, hi=8192),
+                           TRACE_PRESETS["sharegpt-like"][1], seed=0)
+    for name, mod, trace in (("config1", TINY_MODEL, c1), ("config4", m, c4)):
+        for pol in ("bullet", "nopartition", "chunked"):
+            scfg = E.SimConfig(gpu=gpu, model=mod, slo=slo, sched=cfg, policy=E.PolicySpec(pol, chunk_size=1024),
+                               seed=0)
+            t0 = time.perf_counter()
+            E.run(scfg, trace)
+            sim[f"{name}_{pol}_s"] = time.perf_counter() - t0
+    sim["traces"] = {"config1": "9 requests (1024 + 8 short prompts) x 16 tokens, tiny model",
+                     "config4": f"{len(c4)} requests, Poisson 4 rps x 20 s, prompts U[512, 8192], llama3-8b"}
+    out["simulator_wall"] = sim
+    return out
+
+
+REF_TIME_BUDGET_S = 150.0
 
 
 def run_reference(args, rank: int, world: int) -> None:
     """--impl reference: the reference path's CPU implementation (the numpy
-    oracle port; the reference itself has no numerics) on the host cores."""
+    oracle port; the reference itself has no numerics) on the host cores,
+    on the SAME workload as the GPU arm's headline (T = --prefill-tokens):
+    each step = 1 prefill layer over T tokens + 1 decode layer-step (B = 32,
+    ctx 2048).  Steps stop early once REF_TIME_BUDGET_S of CPU time is spent
+    (reported in `steps`), so the run ends within a few minutes."""
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX)
-    secs, toks = 0.0, 0
+    T = args.prefill_tokens
+    for _ in range(args.warmup):  # warm BLAS threads / page in, on a small sample
+        cpu_reference_step(512, DECODE_BATCH, DECODE_CTX, model=args.model)
+    secs, toks, done = 0.0, 0, 0
     for _ in range(args.steps):
-        s, t = cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX)
+        s, t = cpu_reference_step(T, DECODE_BATCH, DECODE_CTX, model=args.model)
         secs += s
         toks += t
+        done += 1
+        if secs >= REF_TIME_BUDGET_S:
+            break
     v = toks / secs
-    sample = f"1 prefill layer x {CPU_SAMPLE_T} tokens + 1 decode step (B={DECODE_BATCH}, ctx {DECODE_CTX}), Llama-3-8B layer, numpy fp32"
+    sample = (f"1 prefill layer x {T} tokens + 1 decode layer-step (B={DECODE_BATCH}, ctx {DECODE_CTX}), "
+              f"{args.model} layer, numpy fp32, {done} step(s) timed")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * secs / done,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "llama3-8b 1 layer: prefill chunk + decode batch 32 ctx 2048 (CPU sample)",
-                       "prefill_tokens": CPU_SAMPLE_T, "decode_batch": DECODE_BATCH,
-                       "decode_ctx": DECODE_CTX, "parallelism": "replicas"},
+            "data": "synthetic", "config": config_of(args.model, T, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------- replica plumbing
-def agree_split(dist, dm: int, n: int, device) -> tuple[int, int]:
-    """Every replica runs rank 0's (dm, n) so the job measures one config."""
+def bcast(dist, vals, device):
+    """Rank 0's values on every replica (one config measured by the job)."""
     if dist is None:
-        return dm, n
+        return vals
     import torch
 
-    t = torch.tensor([dm, n], device=device)
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
     dist.broadcast(t, 0)
-    return int(t[0]), int(t[1])
+    return [x for x in t.tolist()]
 
 
 def job_totals(dist, span_s: float, tokens: int, device) -> tuple[float, int]:
@@ -218,6 +312,76 @@ def job_totals(dist, span_s: float, tokens: int, device) -> tuple[float, int]:
     return float(t.item()), int(tk.item())
 
 
+# ------------------------------------------------------------ per-T study
+def lat(r) -> dict:
+    return {"tokens_per_s": r.tokens_per_s, "ttft_layer_us": 1e6 * r.ttft_layer_s,
+            "tpot_layer_us": 1e6 * r.tpot_layer_s, "p50_prefill_layer_us": 1e6 * r.p50(r.prefill_layer_s),
+            "p50_decode_step_us": 1e6 * r.p50(r.decode_layer_s), "decode_steps_per_prefill_layer":
+                r.decode_steps / r.steps}
+
+
+def study_T(cr, gpu, store, steps: int, dist, coll, sweep: bool = True) -> dict:
+    """Config 2 at one chunk size: estimator split, co-run vs time-sliced vs
+    chunked on the same kernels, and the brute-force regret check."""
+    import torch
+
+    from paper_2504_19516_b200.device.partition import DECODE, PREFILL
+    from paper_2504_19516_b200.device.split import estimator_split
+    from paper_2504_19516_b200.scheduler import SloSpec
+
+    m, T, N = cr.model, cr.T, cr.n
+    L = m.num_layers
+    t_p_full = cr.isolated(PREFILL, N)
+    t_d_full = cr.isolated(DECODE, N)
+    # SLO targets = the time-sliced baseline's latencies at layer interleave
+    # (every decode step waits one prefill layer): whole-model units
+    ts = t_p_full + t_d_full
+    slo = SloSpec(norm_ttft_s_per_token=L * ts / T, tpot_s=L * ts)
+    split = estimator_split(m, T, [cr.C] * cr.B, slo, gpu, store)
+    pm, dm = (int(v) for v in bcast(dist, [split["pm"], split["dm"]], coll))
+    split.update(pm=pm, dm=dm)
+
+    def cadence(pm_, dm_):
+        """Decode steps per prefill layer that keep the decode side busy:
+        measured co-run prefill-layer / decode-step time."""
+        t_p = cr.isolated(PREFILL, pm_, reps=3)
+        t_d = cr.isolated(DECODE, dm_, reps=3)
+        r0 = cr.corun(pm_, dm_, 3, max(1.0, t_p / t_d))
+        return max(1.0, r0.p50(r0.prefill_layer_s) / r0.p50(r0.decode_layer_s))
+
+    ratio = bcast(dist, [cadence(pm, dm)], coll)[0]
+    co = cr.corun(pm, dm, steps, ratio)
+    tsl = cr.time_sliced(steps, ratio)
+    torch.cuda.synchronize()
+    out = {"T": T, "split": split, "decode_steps_per_prefill_layer": ratio,
+           "corun": lat(co), "time_sliced": lat(tsl),
+           "time_sliced_alternating_us": {"ttft_layer": 1e6 * ts, "tpot_layer": 1e6 * ts,
+                                          "prefill_layer_full_gpu": 1e6 * t_p_full,
+                                          "decode_step_full_gpu": 1e6 * t_d_full}}
+    out["corun_vs_time_sliced"] = {
+        "tokens_per_s_ratio": co.tokens_per_s / tsl.tokens_per_s,
+        "ttft_ratio": co.ttft_layer_s / tsl.ttft_layer_s, "tpot_ratio": co.tpot_layer_s / tsl.tpot_layer_s,
+        "wins": bool(co.tokens_per_s >= tsl.tokens_per_s and co.ttft_layer_s <= tsl.ttft_layer_s
+                     and co.tpot_layer_s <= tsl.tpot_layer_s)}
+    out["chunked"] = [cr.chunked(c, reps=2) for c in (1024, 2048)]
+    if sweep:
+        cands = []
+        for d in range(8, 72, 8):
+            r = cr.corun(N - d, d, 4, cadence(N - d, d))
+            cands.append({"pm": N - d, "dm": d, "tokens_per_s": r.tokens_per_s,
+                          "ttft_layer_us": 1e6 * r.ttft_layer_s, "tpot_layer_us": 1e6 * r.tpot_layer_s,
+                          "beats_time_sliced_latency": bool(r.ttft_layer_s <= tsl.ttft_layer_s
+                                                            and r.tpot_layer_s <= tsl.tpot_layer_s)})
+        ok = [c for c in cands if c["beats_time_sliced_latency"]]
+        best = max(ok or cands, key=lambda c: c["tokens_per_s"])
+        mine = next((c for c in cands if c["dm"] == dm), None)
+        out["regret_sweep"] = {"candidates": cands, "best_measured": best,
+                               "best_is_latency_ok": bool(ok),
+                               "estimator_regret": (best["tokens_per_s"] / mine["tokens_per_s"] - 1.0)
+                               if mine else None}
+    return out
+
+
 # ------------------------------------------------------------------ main
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
@@ -225,11 +389,14 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--prefill-tokens", type=int, default=4096)
+    ap.add_argument("--prefill-tokens", type=int, default=4096, help="headline chunk size")
+    ap.add_argument("--sweep", default=",".join(map(str, SWEEP_T)),
+                    help="config-2 chunk sizes measured into per_T ('' = headline only)")
     ap.add_argument("--model", default="llama3-8b", choices=["llama3-8b", "llama3-70b", "moe-a22b"],
                     help="reference preset (workload.py:70-80); moe-a22b runs its MLP at the activated width")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--split", default=None, help="pm,dm,n: skip the warm-up split sweep (profiling)")
+    ap.add_argument("--no-regret-sweep", action="store_true")
+    ap.add_argument("--split", default=None, help="pm,dm: override the estimator's split (profiling)")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
 
@@ -261,50 +428,51 @@ def main(argv=None) -> int:
             dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
 
+    from paper_2504_19516_b200.device import lib as hplib
     from paper_2504_19516_b200.device.corun import CoRunner
-    from paper_2504_19516_b200.device.partition import DECODE, PREFILL
+    from paper_2504_19516_b200.device.layer import LayerWeights, mlp_width
+    from paper_2504_19516_b200.device.partition import PartitionPool
+    from paper_2504_19516_b200.device.split import b200_gpu, b200_store
+    from paper_2504_19516_b200.perf_model import wave_stats
     from paper_2504_19516_b200.workload import MODEL_PRESETS
 
     hbm_gbs, tf_burst, tf_sus, peak_src = _peaks()
     model = MODEL_PRESETS[args.model]
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    weights = LayerWeights.random_device(model, dev, g)  # one layer, shared by every chunk size
+    pool = PartitionPool(local)
+    pool.warm()
+    N = pool.n
+    gpu, store = b200_gpu(), b200_store()
     T = args.prefill_tokens
-    cr = CoRunner(model, T, DECODE_BATCH, DECODE_CTX, device=local, seed=1234 + rank)
-    N = cr.n
+    sweep_T = [int(x) for x in args.sweep.split(",") if x] if args.sweep else []
+    per_T = []
+    for t in [x for x in sweep_T if x != T]:
+        cr_t = CoRunner(model, t, DECODE_BATCH, DECODE_CTX, device=local, seed=1234 + rank, pool=pool,
+                        weights=weights)
+        per_T.append(study_T(cr_t, gpu, store, min(args.steps, 10), dist, coll,
+                             sweep=not args.no_regret_sweep))
+        del cr_t
+        torch.cuda.empty_cache()
 
-    # ---- warm-up: isolated latencies, baseline, split selection
-    t_p_full = cr.isolated(PREFILL, N)
-    t_d_full = cr.isolated(DECODE, N)
-    ts_ttft = ts_tpot = t_p_full + t_d_full  # alternating: every decode step waits one prefill layer
-    ts_alt = cr.time_sliced(args.warmup, 1)
-    candidates = []
-    fixed = [int(v) for v in args.split.split(",")] if args.split else None
-    for dm in ([fixed[1]] if fixed else range(8, 72, 8)):
-        pm = N - dm
-        t_d = cr.isolated(DECODE, dm, reps=3)
-        t_p = cr.isolated(PREFILL, pm, reps=3)
-        # decode steps per prefill layer around t_p / t_d (isolated times;
-        # co-running decode is slower, so one fewer step may fit)
-        nf = max(1, math.floor(t_p / t_d))
-        for n in ([fixed[2]] if fixed else sorted({max(1, nf - 1), nf, nf + 1})):
-            r = cr.corun(pm, dm, 2, n)
-            ok = r.p50(r.decode_layer_s) <= ts_tpot and r.p50(r.prefill_layer_s) <= ts_ttft
-            candidates.append({"pm": pm, "dm": dm, "n": n, "tokens_per_s": r.tokens_per_s,
-                               "ttft_p50_us": 1e6 * r.p50(r.prefill_layer_s),
-                               "tpot_p50_us": 1e6 * r.p50(r.decode_layer_s), "slo_ok": ok})
-    ok = [c for c in candidates if c["slo_ok"]] or candidates
-    best = max(ok, key=lambda c: c["tokens_per_s"])
-    if dist is not None:  # identical split on every replica (rank 0 decides)
-        dmv, nv = agree_split(dist, best["dm"], best["n"], coll)
-        best = next((c for c in candidates if c["dm"] == dmv and c["n"] == nv),
-                    dict(best, dm=dmv, pm=N - dmv, n=nv))
-    pm, dm, n = best["pm"], best["dm"], best["n"]
+    # ---- headline chunk size: study (warm-up), then the timed region
+    cr = CoRunner(model, T, DECODE_BATCH, DECODE_CTX, device=local, seed=1234 + rank, pool=pool, weights=weights)
+    head = study_T(cr, gpu, store, min(args.steps, 10), dist, coll, sweep=not args.no_regret_sweep)
+    per_T.append(head)
+    per_T.sort(key=lambda e: e["T"])
+    pm, dm = head["split"]["pm"], head["split"]["dm"]
+    if args.split:
+        pm, dm = (int(v) for v in args.split.split(","))
+    ratio = head["decode_steps_per_prefill_layer"]
     for _ in range(args.warmup):
-        cr.corun(pm, dm, 1, n)
+        cr.corun(pm, dm, 2, ratio)
     # per-group breakdown from a separate, fully instrumented co-run of the
     # same split (diagnostic: events between every kernel group cost their
     # programmatic-launch overlap), then a pause so the timed region starts
     # from the same power state
-    groups = cr.corun(pm, dm, args.steps, n, time_groups=True)
+    groups = cr.corun(pm, dm, args.steps, ratio, time_groups=True)
     torch.cuda.synchronize()
     time.sleep(1.0)
 
@@ -314,7 +482,7 @@ def main(argv=None) -> int:
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         rid = torch.cuda.nvtx.range_start("timed")  # process-wide range (ncu --nvtx-include "timed]")
-        res = cr.corun(pm, dm, args.steps, n, time_upgate=True)  # events around mlp_up_gate only
+        res = cr.corun(pm, dm, args.steps, ratio, time_upgate=True)  # events around mlp_up_gate only
         torch.cuda.nvtx.range_end(rid)
     torch.cuda.synchronize()
     span, tokens = job_totals(dist, res.span_s, res.tokens, coll)
@@ -330,45 +498,35 @@ def main(argv=None) -> int:
     pin_dy = torch.empty(DECODE_BATCH, h, dtype=torch.bfloat16, pin_memory=True)
     pin_px.copy_(cr.px.cpu())
     pin_dx.copy_(cr.dx.cpu())
-
-    e2e_res = cr.corun_e2e(pm, dm, args.steps, n, pin_px, pin_py, pin_dx, pin_dy)
+    e2e_res = cr.corun_e2e(pm, dm, args.steps, ratio, pin_px, pin_py, pin_dx, pin_dy)
     e2e_span, e2e_tokens = job_totals(dist, e2e_res.span_s, e2e_res.tokens, coll)
-    h2d = T * h * 2 + n * DECODE_BATCH * h * 2
+    h2d = (T * h * 2 * args.steps + e2e_res.decode_steps * DECODE_BATCH * h * 2) // args.steps
     d2h = h2d
 
-    # ---- time-sliced baseline (same kernels, full GPU, alternating)
-    ts_eq = cr.time_sliced(args.steps, n)  # equal work
-
-    # ---- chunked-prefill baseline (lockstep hybrid batches, SGLang-1024/2048
-    # analogue; reference _ChunkedSim engine.py:741-800) on the same kernels
-    chunked = [cr.chunked(c, reps=max(1, min(3, args.steps))) for c in (1024, 2048)]
+    # ---- time-sliced baseline on the timed region's exact work
+    ts_eq = cr.time_sliced(args.steps, ratio)
 
     # ---- SM idle: partition-level (SM-time with no work in either partition)
     # and the wave model's intra-kernel idle of the prefill layer on pm SMs
-    from paper_2504_19516_b200.device import lib as hplib
-    from paper_2504_19516_b200.perf_model import wave_stats
-
     wl = cr.layer.W
-    plans = {g: hplib.gemm_plan(T, w.shape[0], pm) for g, w in
+    plans = {gname: hplib.gemm_plan(T, w.shape[0], pm) for gname, w in
              (("qkv", wl.w_qkv), ("o_proj", wl.w_o), ("mlp_up_gate", wl.w_ug), ("mlp_down", wl.w_down))}
-    units = {g: (pl[1], pm // pl[2]) for g, pl in plans.items()}  # (tiles, concurrent tile slots)
-    units["attn"] = (-(-T // 256) * model.num_heads, pm)          # k_fa2: 256-query units, one per CTA
+    units = {gname: (pl[1], pm // pl[2]) for gname, pl in plans.items()}  # (tiles, concurrent tile slots)
+    units["attn"] = (-(-T // 256) * model.num_heads, pm)                   # k_fa2: 256-query units, one per CTA
     g_s = groups.group_s
-    wave_idle = sum(g_s[g] * wave_stats(u, 1, n).idle_ratio for g, (u, n) in units.items()) / sum(g_s.values())
+    wave_idle = sum(g_s[k] * wave_stats(u, 1, n).idle_ratio for k, (u, n) in units.items()) / sum(g_s.values())
 
     # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
     dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}
 
     # ---- all four prefill GEMMs together (north-star target: >= 85 % of the partition's tensor peak)
-    from paper_2504_19516_b200.device.layer import mlp_width
-
     gemm_flops = 2.0 * T * model.hidden * (model.qkv_out_dim + model.hidden + 3 * mlp_width(model))
-    gemm_s = sum(g_s[g] for g in ("qkv", "o_proj", "mlp_up_gate", "mlp_down"))
+    gemm_s = sum(g_s[k] for k in ("qkv", "o_proj", "mlp_up_gate", "mlp_down"))
 
     # ---- roofline of the dominant kernel (mlp_up_gate GEMM, tensor-bound)
     ug = statistics.mean(res.upgate_s)
     achieved = cr.upgate_flops() / ug / 1e12
-    # the timed region is ~10-20 ms, far from the 4 s power-capped run behind
+    # the timed region is ~50 ms, far from the 4 s power-capped run behind
     # the sustained figure, so the burst peak (scaled to the partition) applies
     peak = tf_burst * pm / N
     traffic = None
@@ -379,39 +537,38 @@ def main(argv=None) -> int:
         except Exception:
             traffic = None
 
-    # ---- CPU baseline (rank 0, N = 1 only)
+    # ---- CPU baseline (rank 0, N = 1 only): the same workload on the host
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        secs, toks = 0.0, 0
-        for _ in range(2):
-            s, t = cpu_reference_step(CPU_SAMPLE_T, DECODE_BATCH, DECODE_CTX, model=args.model)
-            secs += s
-            toks += t
-        cpu = {"value": toks / secs, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-               "sample": f"numpy oracle: 1 prefill layer x {CPU_SAMPLE_T} tokens + 1 decode step "
-                         f"(B={DECODE_BATCH}, ctx {DECODE_CTX}), x2"}
+        s_cpu, t_cpu = cpu_reference_step(T, DECODE_BATCH, DECODE_CTX, model=args.model)
+        cpu = {"value": t_cpu / s_cpu, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+               "cpu_model": cpu_model(),
+               "sample": f"numpy oracle: 1 prefill layer x {T} tokens + 1 decode layer-step "
+                         f"(B={DECODE_BATCH}, ctx {DECODE_CTX}), the headline workload, all BLAS threads",
+               "control_plane_1core": control_plane_timings(args.model)}
 
-    per_step_launches = 7 + n * cr.launches_per_decode_step(dm)  # prefill layer: 7 kernels
+    per_step_launches = 7 + (res.decode_steps / args.steps) * cr.launches_per_decode_step(dm)
+    cfg = config_of(model.name, T, world)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * span / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": f"synthetic (random-init {model.name} layer weights, N(0,1) activations and KV)",
-        "config": {"workload": f"{model.name} 1 layer: prefill chunk {T} tok on {pm} SMs || decode batch "
-                               f"{DECODE_BATCH} ctx {DECODE_CTX} on {dm} SMs (green contexts)",
-                   "model": f"{model.name} (1 layer)", "prefill_tokens": T, "decode_batch": DECODE_BATCH,
-                   "decode_ctx": DECODE_CTX, "pm": pm, "dm": dm, "decode_steps_per_prefill_layer": n,
-                   "parallelism": f"replicas x{world}", "l2": "inputs exceed L2 (weights+KV 1.1 GB/step)"},
-        "p50_ttft_us": 1e6 * res.p50(res.prefill_layer_s),
-        "p50_tpot_us": 1e6 * res.p50(res.decode_layer_s),
-        "time_sliced": {
-            "alternating": {"tokens_per_s": ts_alt.tokens_per_s, "p50_ttft_us": 1e6 * ts_ttft,
-                            "p50_tpot_us": 1e6 * ts_tpot},
-            "equal_work": {"tokens_per_s": ts_eq.tokens_per_s, "span_ratio": ts_eq.span_s / res.span_s},
-        },
-        "chunked_baseline": chunked,
+        "config": cfg,
+        "split": {"pm": pm, "dm": dm, "split_source": "override" if args.split else "estimator",
+                  "decode_steps_per_prefill_layer": res.decode_steps / args.steps,
+                  "estimator": head["split"], "green_contexts": True},
+        "model_equivalent_tokens_per_s": value / model.num_layers,
+        "ttft_layer_us": 1e6 * res.ttft_layer_s, "tpot_layer_us": 1e6 * res.tpot_layer_s,
+        "p50_ttft_layer_us": 1e6 * res.p50(res.prefill_layer_s),
+        "p50_tpot_layer_us": 1e6 * res.p50(res.decode_layer_s),
+        "latency_note": "per layer: TTFT = mean prefill progress per layer, TPOT = mean time per decode "
+                        "layer-step; x32 for a Llama-3-8B model",
+        "time_sliced": dict(lat(ts_eq), note="same kernels and work, one full-GPU stream, prefill layer then "
+                                             "its decode steps"),
+        "per_T": per_T,
         "sm_idle_pct": {"partition": 100 * res.partition_idle(N), "wave_model_prefill_layer": 100 * wave_idle,
-                        "prefill_group_us": {g: 1e6 * v for g, v in g_s.items()},
+                        "prefill_group_us": {k: 1e6 * v for k, v in g_s.items()},
                         "prefill_group_note": "per-group events from a separate co-run of the same split just "
                                               "before the timed region (which records events around "
                                               "mlp_up_gate only)"},
@@ -420,7 +577,6 @@ def main(argv=None) -> int:
                           "flops_per_layer": gemm_flops,
                           "note": "all four prefill GEMMs of the layer (qkv, o_proj, mlp_up_gate, mlp_down), "
                                   "median per-group CUDA-event times during the co-run"},
-        "split_sweep": candidates,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "mlp_up_gate (tcgen05 GEMM + SiLU)",
                      "peak_basis": f"bf16_tflops burst ({peak_src}) x pm/N = {tf_burst} x {pm}/{N}",
@@ -431,7 +587,7 @@ def main(argv=None) -> int:
         "clocks": clk.summary(),
         "e2e": {"value": e2e_tokens / e2e_span, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps * per_step_launches,
+        "gpu_launches": int(round(args.steps * per_step_launches)),
         "cpu_baseline": cpu,
     }
     if rank == 0:

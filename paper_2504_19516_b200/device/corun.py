@@ -38,6 +38,27 @@ def _ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+def decode_schedule(steps: int, per_step) -> list[int]:
+    """Decode layer-steps issued beside each of `steps` prefill layers:
+    an int n (n each), a list (as given), or a float ratio r (Bresenham
+    spread: r decode steps per prefill layer on average, at least 1 each --
+    the decode side then runs continuously through the prefill layers)."""
+    if isinstance(per_step, (list, tuple)):
+        if len(per_step) != steps:
+            raise ValueError("decode schedule length != steps")
+        return [int(n) for n in per_step]
+    if isinstance(per_step, int):
+        return [per_step] * steps
+    r = max(1.0, float(per_step))
+    out, acc = [], 0.0
+    for _ in range(steps):
+        acc += r
+        n = int(acc + 1e-9)
+        out.append(n)
+        acc -= n
+    return out
+
+
 @dataclass
 class CoRunResult:
     pm: int
@@ -79,6 +100,19 @@ class CoRunResult:
 
     def p50(self, xs) -> float:
         return statistics.median(xs) if xs else 0.0
+
+    @property
+    def ttft_layer_s(self) -> float:
+        """Mean prefill progress per layer: completion of the last prefill
+        layer / prefill layers (a prompt's TTFT is num_layers x this)."""
+        return max(e for _, e in self.prefill_window_s) / self.steps
+
+    @property
+    def tpot_layer_s(self) -> float:
+        """Mean time per decode layer-step: completion of the last decode
+        step / decode steps (the mean inter-token time of a decoding
+        request, per layer -- the paper's TPOT)."""
+        return max(e for _, e in self.decode_window_s) / self.decode_steps
 
 
 class CoRunner:
@@ -200,10 +234,10 @@ class CoRunner:
         ms = sorted(x.elapsed_time(y) for x, y in times[1:])
         return ms[len(ms) // 2] * 1e-3
 
-    def corun(self, pm: int, dm: int, steps: int, decode_per_step: int, time_upgate: bool = False,
+    def corun(self, pm: int, dm: int, steps: int, decode_per_step, time_upgate: bool = False,
               copy_in=None, copy_out=None, time_groups: bool = False) -> CoRunResult:
         """`steps` prefill layers on pm SMs co-executed with
-        steps * decode_per_step decode layer-steps on dm SMs.  time_upgate:
+        decode layer-steps on dm SMs (`decode_schedule`).  time_upgate:
         events around the mlp_up_gate GEMM only (the roofline kernel);
         time_groups: around every kernel group (diagnostic: the extra events
         between launches cost their programmatic-launch overlap)."""
@@ -214,7 +248,9 @@ class CoRunner:
         p_ev = [(_ev(), _ev()) for _ in range(steps)]
         timed = GROUPS if time_groups else (("mlp_up_gate",) if time_upgate else ())
         ug_ev = [{g: (_ev(), _ev()) for g in timed} for _ in range(steps)] if timed else None
-        d_ev = [(_ev(), _ev()) for _ in range(steps * decode_per_step)]
+        sched = decode_schedule(steps, decode_per_step)
+        D = sum(sched)
+        d_ev = [(_ev(), _ev()) for _ in range(D)]
         torch.cuda._sleep(400_000)
         start.record(ctrl)
         ps.torch_stream.wait_event(start)
@@ -231,7 +267,7 @@ class CoRunner:
                 if copy_out is not None:
                     copy_out(PREFILL, ps.torch_stream)
             with torch.cuda.stream(ds.torch_stream):
-                for _ in range(decode_per_step):
+                for _ in range(sched[s]):
                     if copy_in is not None:
                         copy_in(DECODE, ds.torch_stream)
                     d_ev[di][0].record(ds.torch_stream)
@@ -244,8 +280,7 @@ class CoRunner:
         end_d.record(ds.torch_stream)
         torch.cuda.synchronize()
         span = max(start.elapsed_time(end_p), start.elapsed_time(end_d)) * 1e-3
-        res = CoRunResult(pm, dm, steps, steps * decode_per_step, span, steps * self.T,
-                          steps * decode_per_step * self.B)
+        res = CoRunResult(pm, dm, steps, D, span, steps * self.T, D * self.B)
         res.prefill_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in p_ev]
         res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
         res.prefill_window_s = [(start.elapsed_time(a) * 1e-3, start.elapsed_time(b) * 1e-3) for a, b in p_ev]
@@ -256,7 +291,7 @@ class CoRunner:
                            for g in timed}
         return res
 
-    def corun_e2e(self, pm: int, dm: int, steps: int, decode_per_step: int, host_px, host_py,
+    def corun_e2e(self, pm: int, dm: int, steps: int, decode_per_step, host_px, host_py,
                   host_dx, host_dy) -> CoRunResult:
         """`corun` end to end from pinned host memory: every prefill layer's
         input is copied host->device and its output device->host, every
@@ -266,6 +301,7 @@ class CoRunner:
         pipeline); decode copies (B x hidden) stay in-stream."""
         ps, ds = self.pool.split(pm, dm)
         g = self.decode_graph(ds)
+        sched = decode_schedule(steps, decode_per_step)
         ctrl = torch.cuda.current_stream(self.dev)
         h2d, d2h = torch.cuda.Stream(self.dev), torch.cuda.Stream(self.dev)
         xs = [self.px, torch.empty_like(self.px)]
@@ -301,7 +337,7 @@ class CoRunner:
                 host_py.copy_(ys[s % 2], non_blocking=True)
                 out_done[s].record(d2h)
             with torch.cuda.stream(ds.torch_stream):
-                for _ in range(decode_per_step):
+                for _ in range(sched[s]):
                     self.dx.copy_(host_dx, non_blocking=True)
                     g.replay()
                     host_dy.copy_(self.dy, non_blocking=True)
@@ -310,16 +346,17 @@ class CoRunner:
         end_o.record(d2h)
         torch.cuda.synchronize()
         span = max(start.elapsed_time(e) for e in (end_p, end_d, end_o)) * 1e-3
-        return CoRunResult(pm, dm, steps, steps * decode_per_step, span, steps * self.T,
-                           steps * decode_per_step * self.B)
+        return CoRunResult(pm, dm, steps, sum(sched), span, steps * self.T, sum(sched) * self.B)
 
-    def time_sliced(self, steps: int, decode_per_step: int) -> CoRunResult:
+    def time_sliced(self, steps: int, decode_per_step) -> CoRunResult:
         """Same work, one full-GPU stream: prefill layer then its decode steps."""
         st = self.pool.full(PREFILL)
         g = self.decode_graph(st)
         start, end = _ev(), _ev()
         p_ev = [(_ev(), _ev()) for _ in range(steps)]
-        d_ev = [(_ev(), _ev()) for _ in range(steps * decode_per_step)]
+        sched = decode_schedule(steps, decode_per_step)
+        D = sum(sched)
+        d_ev = [(_ev(), _ev()) for _ in range(D)]
         with torch.cuda.stream(st.torch_stream):
             torch.cuda._sleep(400_000)
             start.record(st.torch_stream)
@@ -328,18 +365,19 @@ class CoRunner:
                 p_ev[s][0].record(st.torch_stream)
                 self.prefill_layer(st)
                 p_ev[s][1].record(st.torch_stream)
-                for _ in range(decode_per_step):
+                for _ in range(sched[s]):
                     d_ev[di][0].record(st.torch_stream)
                     g.replay()
                     d_ev[di][1].record(st.torch_stream)
                     di += 1
             end.record(st.torch_stream)
         torch.cuda.synchronize()
-        res = CoRunResult(self.n, self.n, steps, steps * decode_per_step,
-                          start.elapsed_time(end) * 1e-3, steps * self.T,
-                          steps * decode_per_step * self.B)
+        res = CoRunResult(self.n, self.n, steps, D, start.elapsed_time(end) * 1e-3, steps * self.T,
+                          D * self.B)
         res.prefill_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in p_ev]
         res.decode_layer_s = [a.elapsed_time(b) * 1e-3 for a, b in d_ev]
+        res.prefill_window_s = [(start.elapsed_time(a) * 1e-3, start.elapsed_time(b) * 1e-3) for a, b in p_ev]
+        res.decode_window_s = [(start.elapsed_time(a) * 1e-3, start.elapsed_time(b) * 1e-3) for a, b in d_ev]
         return res
 
     def chunked(self, chunk: int, reps: int = 1) -> dict:

@@ -25,7 +25,7 @@ def _port():
 def _main(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    split = bench.agree_split(dist, 8 * (rank + 1), 1 + rank, "cpu")
+    split = tuple(bench.bcast(dist, [8 * (rank + 1), 1.5 + rank], "cpu"))
     span, tokens = bench.job_totals(dist, 0.010 + 0.005 * rank, 4128 * (rank + 1), "cpu")
     q.put((rank, split, span, tokens))
     dist.destroy_process_group()
@@ -43,7 +43,7 @@ def test_bench_job_totals_and_split_agreement_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     for rank, split, span, tokens in got:
-        assert split == (8, 1)                  # rank 0's decision everywhere
+        assert split == (8.0, 1.5)              # rank 0's decision everywhere
         assert abs(span - 0.015) < 1e-12        # max over ranks
         assert tokens == 4128 * 3               # whole-job tokens
 
