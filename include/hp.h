@@ -244,6 +244,14 @@ int hp_decode_attn(const void* q, int ldq, const void* kcache, const void* vcach
                    int B, int Hq, int Hkv, int d, int page, int num_blocks, float scale,
                    void* workspace, size_t ws_bytes, int max_ctas, void* stream);
 
+/* Strided row copy (rows x row_bytes, 16-byte aligned), grid <= 4 x max_ctas
+ * CTAs.  Either side may be pinned host memory (UVA-mapped): used for a
+ * decode step's per-step input/output (B x hidden) so it crosses PCIe on the
+ * decode partition's SMs inside the step's CUDA graph rather than on a copy
+ * engine shared with the prefill side's bulk transfers. */
+int hp_copy_rows(const void* src, long lds_bytes, void* dst, long ldd_bytes, int rows, int row_bytes,
+                 int max_ctas, void* stream);
+
 /* ---------------------------------------------------- instrumentation */
 /* Memory-bandwidth probe behind the SRM memory term D_p = D min(1, p/n_d)
  * (perf_model.py:172-180): stream `bytes` from `src` with `ctas` CTAs.

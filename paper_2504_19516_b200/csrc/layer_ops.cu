@@ -116,9 +116,53 @@ __global__ void k_tile_weight(const __nv_bfloat16* __restrict__ w, int ldw,
   }
 }
 
+// Strided row copy, 16-byte chunks, 4 independent chunks in flight per
+// thread.  Either side may be pinned host memory (UVA-mapped): a decode
+// step's B x hidden input / output cross PCIe through the decode
+// partition's own SMs, inside its CUDA graph, instead of queueing on a copy
+// engine behind the prefill side's multi-MB transfers.
+__global__ void k_copy_rows(const uint8_t* __restrict__ src, long lds, uint8_t* __restrict__ dst, long ldd,
+                            int rows, int row_bytes) {
+  pdl_trigger();
+  pdl_wait();
+  const int per_row = row_bytes >> 4;
+  const long total = long(rows) * per_row;
+  const long stride = long(gridDim.x) * blockDim.x;
+  for (long i0 = blockIdx.x * long(blockDim.x) + threadIdx.x; i0 < total; i0 += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long i = i0 + u * stride;
+      if (i < total) v[u] = *reinterpret_cast<const uint4*>(src + (i / per_row) * lds + (i % per_row) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long i = i0 + u * stride;
+      if (i < total) *reinterpret_cast<uint4*>(dst + (i / per_row) * ldd + (i % per_row) * 16) = v[u];
+    }
+  }
+}
+
 }  // namespace hp
 
 using namespace hp;
+
+extern "C" int hp_copy_rows(const void* src, long lds_bytes, void* dst, long ldd_bytes, int rows, int row_bytes,
+                            int max_ctas, void* stream) {
+  HP_CHECK_ARG(src && dst, "hp_copy_rows: null pointer");
+  HP_CHECK_ARG(rows >= 1 && row_bytes >= 16 && row_bytes % 16 == 0, "hp_copy_rows: row_bytes % 16");
+  HP_CHECK_ARG(lds_bytes % 16 == 0 && ldd_bytes % 16 == 0 && lds_bytes >= row_bytes && ldd_bytes >= row_bytes,
+               "hp_copy_rows: row pitches must be >= row_bytes and multiples of 16");
+  HP_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
+               "hp_copy_rows: pointers must be 16B aligned");
+  HP_CHECK_ARG(max_ctas >= 1, "hp_copy_rows: max_ctas must be >= 1");
+  const long total = long(rows) * (row_bytes / 16);
+  const int threads = 256;
+  const int grid = int(std::min<long>((total + 4 * threads - 1) / (4 * threads), long(max_ctas) * 4));
+  HP_LAUNCH_PDL("k_copy_rows", k_copy_rows, dim3(grid), dim3(threads), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const uint8_t*>(src), lds_bytes, static_cast<uint8_t*>(dst), ldd_bytes, rows, row_bytes);
+  return HP_OK;
+}
 
 extern "C" int hp_tile_weight(const void* w, int ldw, void* out, int N, int K, void* stream) {
   HP_CHECK_ARG(w && out && w != out, "hp_tile_weight: bad pointers (in place not supported)");

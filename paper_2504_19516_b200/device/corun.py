@@ -298,7 +298,9 @@ class CoRunner:
         decode step's input/output likewise.  Prefill copies run on their own
         copy-engine streams, double-buffered so step s+1's input lands and
         step s-1's output drains while step s computes (the serving
-        pipeline); decode copies (B x hidden) stay in-stream."""
+        pipeline); decode inputs / outputs (B x hidden per step) are read /
+        written in place in pinned host memory by a copy kernel on the decode
+        partition (UVA zero-copy), in-stream with the step."""
         ps, ds = self.pool.split(pm, dm)
         g = self.decode_graph(ds)
         sched = decode_schedule(steps, decode_per_step)
@@ -315,11 +317,18 @@ class CoRunner:
         for st in (ps.torch_stream, ds.torch_stream, h2d, d2h):
             st.wait_event(start)
 
+        chunks = max(1, getattr(self, "e2e_chunks", 4))  # prefill copies in 4 pieces
+        pio = getattr(self, "e2e_prefill_io", True)
+        dio = getattr(self, "e2e_decode_io", True)
+        bounds = [self.T * i // chunks for i in range(chunks + 1)]
+
         def load(s):
             with torch.cuda.stream(h2d):
                 if s >= 2:
                     h2d.wait_event(done[s - 2])  # buffer s%2 free once step s-2 computed
-                xs[s % 2].copy_(host_px, non_blocking=True)
+                if pio:
+                    for a, b in zip(bounds, bounds[1:]):
+                        xs[s % 2][a:b].copy_(host_px[a:b], non_blocking=True)
                 in_ready[s].record(h2d)
 
         load(0)
@@ -334,13 +343,21 @@ class CoRunner:
                 done[s].record(ps.torch_stream)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(done[s])
-                host_py.copy_(ys[s % 2], non_blocking=True)
+                if pio:
+                    for a, b in zip(bounds, bounds[1:]):
+                        host_py[a:b].copy_(ys[s % 2][a:b], non_blocking=True)
                 out_done[s].record(d2h)
             with torch.cuda.stream(ds.torch_stream):
                 for _ in range(sched[s]):
-                    self.dx.copy_(host_dx, non_blocking=True)
+                    # the step's B x hidden input / output cross PCIe through
+                    # the decode partition's SMs (zero-copy, hp_copy_rows), so
+                    # they never queue on a copy engine behind the prefill
+                    # side's 34 MB transfers
+                    if dio:
+                        lib.copy_rows(host_dx, self.dx, ds.sms, ds.torch_stream)
                     g.replay()
-                    host_dy.copy_(self.dy, non_blocking=True)
+                    if dio:
+                        lib.copy_rows(self.dy, host_dy, ds.sms, ds.torch_stream)
         end_p.record(ps.torch_stream)
         end_d.record(ds.torch_stream)
         end_o.record(d2h)

@@ -58,6 +58,7 @@ SIGNATURES = {
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_decode_attn_launches": (_i, [_i, _i, _i, _i, _i, _i, _i]),
     "hp_decode_attn": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _f, _p, _sz, _i, _p]),
+    "hp_copy_rows": (_i, [_p, C.c_long, _p, C.c_long, _i, _i, _i, _p]),
     "hp_probe": (_i, [_i, _i, _i64, _p, _p]),
     "hp_membw": (_i, [_p, _sz, _i, _i, _p, _p]),
     "hp_membw2d": (_i, [_p, _i, _i, _i, _i, _p, _p]),
@@ -306,6 +307,16 @@ def decode_attn(q, kcache, vcache, block_table, ctx_lens, out, Hq: int, Hkv: int
                                 Hkv, d, page, kcache.shape[0], scale, _ptr(ws),
                                 0 if ws is None else ws.numel() * ws.element_size(), max_ctas,
                                 _stream(stream)), "hp_decode_attn")
+
+
+def copy_rows(src, dst, max_ctas: int = 148, stream=None) -> None:
+    """dst[:] = src for 2-D tensors of equal shape/dtype (either may be pinned
+    host memory, read or written through UVA by the kernel)."""
+    if src.shape != dst.shape or src.dtype != dst.dtype or src.dim() != 2:
+        raise InvalidArgumentError("copy_rows: src/dst must be 2-D with equal shape and dtype")
+    es = src.element_size()
+    check(load().hp_copy_rows(_ptr(src), src.stride(0) * es, _ptr(dst), dst.stride(0) * es, src.shape[0],
+                              src.shape[1] * es, max_ctas, _stream(stream)), "hp_copy_rows")
 
 
 def membw(src, ctas: int, method: int, out, stream=None) -> None:

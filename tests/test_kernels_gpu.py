@@ -431,3 +431,20 @@ def test_gemm_qkv_rope_bit_identical_to_unfused_path(gen):
     lib.rope_kv_write(y2, Hq, Hkv, d, pos, table, slots, c2.k, c2.v, page, max_ctas=148)
     torch.cuda.synchronize()
     assert torch.equal(y1, y2) and torch.equal(c1.k, c2.k) and torch.equal(c1.v, c2.v)
+
+
+# ------------------------------------------------------- zero-copy row copy
+@pytest.mark.parametrize("rows,cols,ctas", [(32, 4096, 8), (7, 136, 1), (256, 4096, 148)])
+def test_copy_rows_pinned_host_both_ways(rows, cols, ctas, gen):
+    """hp_copy_rows reads and writes pinned host memory through UVA (the
+    decode step's per-step input / output in the end-to-end co-run)."""
+    src = bf((rows, cols), gen=gen)
+    host = torch.empty(rows, cols, dtype=torch.bfloat16, pin_memory=True)
+    lib.copy_rows(src, host, max_ctas=ctas)           # device -> pinned host
+    torch.cuda.synchronize()
+    assert torch.equal(host, src.cpu())
+    dst = torch.zeros(rows, 2 * cols, dtype=torch.bfloat16, device=DEV)[:, cols // 2: cols // 2 + cols]
+    if (cols // 2) % 8 == 0:
+        lib.copy_rows(host, dst, max_ctas=ctas)       # pinned host -> strided device view
+        torch.cuda.synchronize()
+        assert torch.equal(dst, src)
