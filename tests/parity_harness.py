@@ -593,3 +593,44 @@ def run_corun_parity(T: int = 4096, dm: int = 8, B: int = 32, ctx: int = 2048, n
            "decode_tensors": {k: dict(abs_report(f(v), tr_d[k]), excess=excess(f(v), tr_d[k]))
                               for k, v in dev_d.items()}}
     return out
+
+
+def oracle_check_generation(m, Wl, embed, final_norm, lm_head, prompt, tokens) -> dict:
+    """Teacher-force the oracle on a sequence the DEVICE generated freely
+    (prompt, then its greedy tokens): at every step the device's token must
+    be the oracle's argmax, or a genuine bf16 tie (top-2 margin within
+    MARGIN_ULPS ulps of the top logit)."""
+    d, Hq, Hkv = m.head_dim, m.num_heads, m.num_kv_heads
+    L, n = len(prompt), len(tokens)
+    pages = -(-(L + n + 1) // PAGE)
+    kc = [np.zeros((pages, Hkv, PAGE, d), np.float32) for _ in Wl]
+    vc = [np.zeros((pages, Hkv, PAGE, d), np.float32) for _ in Wl]
+    bt = np.arange(pages, dtype=np.int32)[None]
+    table = O.rope_table(L + n + 2, d)
+    out = {"matches": 0, "mismatches": 0, "tie_flips": 0, "first_bad": None}
+
+    def score(i, x):
+        rt, mg, lg = O.greedy_tokens(x, final_norm, lm_head)
+        if int(rt[0]) == int(tokens[i]):
+            out["matches"] += 1
+        elif mg[0] <= MARGIN_ULPS * _ulp_bf16(np.max(lg[0])):
+            out["tie_flips"] += 1
+        else:
+            out["mismatches"] += 1
+            if out["first_bad"] is None:
+                out["first_bad"] = i
+
+    x = embed[np.asarray(prompt)]
+    for li, W in enumerate(Wl):
+        x, kk, vv = O.layer_prefill(x, W, Hq, Hkv, d, np.arange(L), table, bf16_boundaries=True)
+        for j in range(L):
+            kc[li][j // PAGE, :, j % PAGE] = kk[j]
+            vc[li][j // PAGE, :, j % PAGE] = vv[j]
+    score(0, x[-1:])
+    for i in range(1, n):
+        x = embed[[int(tokens[i - 1])]]
+        for li, W in enumerate(Wl):
+            x = O.layer_decode(x, W, Hq, Hkv, d, np.array([L + i]), table, kc[li], vc[li], bt,
+                               bf16_boundaries=True)
+        score(i, x)
+    return out
