@@ -49,6 +49,9 @@ from .layer import (EPS, PAGE, DecodeScratch, DeviceLayer, KVCache, LayerWeights
                     decode_slots)
 from .partition import PartitionPool
 
+__all__ = ["ServingModel", "RealtimeSim", "RealtimeChunked", "kv_pages_for", "state_to_json", "state_from_json",
+           "store_from_json"]
+
 BUCKETS = (8, 16, 32, 64, 128, 256)
 
 
@@ -143,6 +146,29 @@ class ServingModel:
                 self.p_next[:nseq].copy_(torch.argmax(self.p_logits[:nseq], dim=-1))
                 lib.copy_rows(self.p_next.view(1, -1), self.h_p_next.view(1, -1), sms, stream)
 
+    def hybrid_step(self, meta: dict, sms: int, stream) -> None:
+        """One lockstep hybrid iteration through every layer (the chunked
+        baseline, reference _ChunkedSim engine.py:741-800): prompt-chunk rows
+        (cached prefixes via paged prefill attention) then one row per
+        decoding request; the rows in meta["emit"] go through the LM head and
+        their argmax ids land in h_p_next."""
+        T, ne = meta["T"], meta["n_emit"]
+        with torch.cuda.stream(stream):
+            torch.index_select(self.embed, 0, meta["tokens"], out=self.pbuf[0][:T])
+            for li, (lyr, cache) in enumerate(zip(self.layers, self.caches)):
+                x, y = self.pbuf[li % 2][:T], self.pbuf[(li + 1) % 2][:T]
+                lyr.hybrid(x, y, self.psc, self.dsc, meta["Tc"], meta["cu"], meta["n_chunks"], meta["max_chunk"],
+                           meta["prior"], meta["cbt"], meta["dctx"], meta["dbt"], meta["pos"], meta["slots"],
+                           cache, sms, stream)
+            if ne:
+                hid = self.pbuf[self.model.num_layers % 2]
+                last = self.p_norm[:ne]
+                torch.index_select(hid, 0, meta["emit"], out=last)
+                lib.rmsnorm(last, self.final_norm, last, EPS, sms, stream)
+                self._lm_head(last, self.p_logits[:ne], 0, sms, stream)
+                self.p_next[:ne].copy_(torch.argmax(self.p_logits[:ne], dim=-1))
+                lib.copy_rows(self.p_next.view(1, -1), self.h_p_next.view(1, -1), sms, stream)
+
     def _lm_head(self, x, out, which: int, sms: int, stream) -> None:
         if x.shape[0] <= 256:
             lib.gemm_swap(x, self.lm_head, out, self.lm_ws[which], self.lm_cnt[which], lib.EPI_STORE,
@@ -181,6 +207,21 @@ class ServingModel:
             torch.cuda.synchronize(self.dev)
             self._graphs[key] = g
         return g
+
+    def warm(self, pool: PartitionPool, buckets=BUCKETS, shares=None) -> int:
+        """Capture every decode graph a run can replay -- each bucket on every
+        decode share of the 8-SM grid plus the full device -- before the
+        clock starts (a first-use capture costs tens of ms)."""
+        from .partition import DECODE
+
+        n = 0
+        for dm in (shares or list(range(pool.granularity, pool.n, pool.granularity)) + [pool.n]):
+            ps = pool.phase(DECODE, dm)
+            for b in buckets:
+                if b <= self.max_batch:
+                    self.decode_graph(b, ps)
+                    n += 1
+        return n
 
     def stage_decode(self, tokens, ctxs, rows) -> int:
         """Write one decode step's inputs (last token, context incl. it,
@@ -532,6 +573,43 @@ def state_from_json(d: dict, mod) -> object:
                              kv_blocked=frozenset(d["kv_blocked"]), decode_last_step_s=d["decode_last_step_s"])
 
 
+def delta_encode(decisions: list[dict]) -> list[dict]:
+    """Fixture compaction: each entry's store snapshot replaced by the alpha
+    / contention entries that changed since the previous entry (the first
+    entry keeps its full snapshot).  `delta_decode` inverts it."""
+    out, prev_a, prev_c = [], {}, {}
+    for d in decisions:
+        a = {(x[0], x[1], x[2]): x[3] for x in d["store"]["alpha"]}
+        c = {(x[0], x[1]): x[2] for x in d["store"]["contention"]}
+        da = [[*k, v] for k, v in a.items() if prev_a.get(k) != v]
+        dc = [[*k, v] for k, v in c.items() if prev_c.get(k) != v]
+        gone = [list(k) for k in prev_a if k not in a] + [list(k) for k in prev_c if k not in c]
+        e = dict(d)
+        e["store"] = {"alpha": da, "contention": dc, "delta": True, "removed": gone}
+        out.append(e)
+        prev_a, prev_c = a, c
+    return out
+
+
+def delta_decode(decisions: list[dict]) -> list[dict]:
+    out, a, c = [], {}, {}
+    for d in decisions:
+        st = d["store"]
+        if not st.get("delta"):
+            out.append(d)
+            a = {(x[0], x[1], x[2]): x[3] for x in st["alpha"]}
+            c = {(x[0], x[1]): x[2] for x in st["contention"]}
+            continue
+        for k in st.get("removed", []):
+            a.pop(tuple(k), None) if len(k) == 3 else c.pop(tuple(k), None)
+        a.update({(x[0], x[1], x[2]): x[3] for x in st["alpha"]})
+        c.update({(x[0], x[1]): x[2] for x in st["contention"]})
+        e = dict(d)
+        e["store"] = {"alpha": [[*k, v] for k, v in a.items()], "contention": [[*k, v] for k, v in c.items()]}
+        out.append(e)
+    return out
+
+
 def store_from_json(d: dict, perf_model):
     s = perf_model.CalibrationStore()
     for ph, sms, tok, v in d["alpha"]:
@@ -539,3 +617,189 @@ def store_from_json(d: dict, perf_model):
     for sms, sl, v in d["contention"]:
         s.contention_bw[(int(sms), int(sl))] = v
     return s
+
+
+class RealtimeChunked(E._ChunkedSim):
+    """The reference's lockstep chunked-prefill loop (`_ChunkedSim`,
+    engine.py:715-859) on a wall clock, every iteration a real hybrid batch
+    through the whole model on the full GPU (the SGLang-style baseline)."""
+
+    def __init__(self, cfg: E.SimConfig, trace, server: ServingModel, pool: PartitionPool, prompts=None,
+                 seed: int = 0):
+        super().__init__(cfg, trace, oracle=_NoOracle())
+        self.server = server
+        self.pool = pool
+        self.pages = PageAllocator(server.kv_pages)
+        rng = np.random.default_rng(seed)
+        self.prompts = prompts if prompts is not None else {
+            r.id: rng.integers(0, server.vocab, r.input_len).astype(np.int32) for r in trace}
+        self.seq_pages: dict[int, list[int]] = {}
+        self.generated: dict[int, list[int]] = {r.id: [] for r in trace}
+        self.last_tok: dict[int, int] = {}
+        self.pending: _Pending | None = None
+        self.host_busy_s = 0.0
+        self.device_calls = {"hybrid_iterations": 0}
+
+    def run(self) -> E.MetricsReport:
+        for r in self.trace:
+            self._push(r.arrival_s, "arrival", r.id)
+        dev = self.server.dev
+        torch.cuda.synchronize(dev)
+        self._t0 = _ev()
+        self._t0.record(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
+        self._h0 = time.perf_counter()
+        while self.heap or self.pending:
+            now = time.perf_counter() - self._h0
+            due = []
+            if self.heap and self.heap[0][0] <= now:
+                due.append((self.heap[0][0], 0))
+            if self.pending is not None and self.pending.end.query():
+                due.append((self._t0.elapsed_time(self.pending.end) * 1e-3, 1))
+            if not due:
+                if not self.heap and not self.pending:
+                    break
+                time.sleep(2e-5)
+                continue
+            t, k = min(due)
+            h0 = time.perf_counter()
+            self.makespan = max(self.makespan, t)
+            if k == 0:
+                t, _, kind, rid = heapq.heappop(self.heap)
+                self.queue.append(rid)
+                self._log(t)
+                if not self.busy:
+                    self._start_iteration(t)
+            else:
+                p, self.pending = self.pending, None
+                step_s = p.start.elapsed_time(p.end) * 1e-3
+                pl = p.payload
+                nxt = self.server.h_p_next[:len(pl["emit_ids"])].tolist()
+                for rid, tok in zip(pl["emit_ids"], nxt):
+                    self.generated[rid].append(int(tok))
+                    self.last_tok[rid] = int(tok)
+                tot = pl["chunk_tokens"] + len(pl["decode"])
+                if tot > 0:
+                    self.occ_prefill += self.gpu.num_sms * step_s * pl["chunk_tokens"] / tot
+                    self.occ_decode += self.gpu.num_sms * step_s * len(pl["decode"]) / tot
+                self._on_iteration(t, {"chunks": pl["chunks"], "decode": pl["decode"], "step_s": step_s})
+            self.host_busy_s += time.perf_counter() - h0
+        torch.cuda.synchronize(dev)
+        self.wall_s = time.perf_counter() - self._h0
+        mk = self.makespan
+        rep = E.compute_metrics([self.records[r.id] for r in self.trace], self.cfg.slo, mk,
+                                self.occ_prefill / mk if mk > 0 else 0.0,
+                                self.occ_decode / mk if mk > 0 else 0.0)
+        rep.queue_timeline = self.queue_timeline
+        rep.partition_timeline = self.partition_timeline
+        rep.decision_log = []
+        return rep
+
+    def _start_iteration(self, t: float) -> None:
+        """The reference's `_start_iteration` (engine.py:741-800) with the
+        oracle replaced by the device iteration."""
+        if self.busy:
+            return
+        for rid in self.decode_ready:
+            self.records[rid].decode_start_s = t
+        self.decode_running.extend(self.decode_ready)
+        self.decode_ready = []
+        ds = len(self.decode_running)
+        room = max(0, self.cs - ds)
+        chunks: list[tuple[int, int, int]] = []
+        for rid in self.prefill_fifo:
+            if room <= 0:
+                break
+            left = self.records[rid].request.input_len - self.progress[rid]
+            take = min(room, left)
+            if take > 0:
+                chunks.append((rid, take, self.progress[rid]))
+                room -= take
+        while room > 0 and self.queue:
+            nxt = next((r for r in self.queue if self.kv_used + self._kv_need(r) <= self.kv_budget), None)
+            if nxt is None:
+                break
+            self.queue.remove(nxt)
+            self.kv_used += self._kv_need(nxt)
+            self.prefill_fifo.append(nxt)
+            self.progress[nxt] = 0
+            self.records[nxt].state = "prefilling"
+            req = self.records[nxt].request
+            self.seq_pages[nxt] = self.pages.alloc(-(-(req.input_len + req.output_len + 1) // PAGE))
+            take = min(room, req.input_len)
+            chunks.append((nxt, take, 0))
+            room -= take
+        if not chunks and not self.decode_running:
+            return
+        meta = self._iteration_meta(chunks, list(self.decode_running))
+        st = self.pool.full(0)
+        a, b = _ev(), _ev()
+        a.record(st.torch_stream)
+        self.server.hybrid_step(meta, st.sms, st.torch_stream)
+        b.record(st.torch_stream)
+        self.busy = True
+        self.device_calls["hybrid_iterations"] += 1
+        self.pending = _Pending("iteration", b, a, {"chunks": chunks, "decode": list(self.decode_running),
+                                                    "emit_ids": meta["emit_ids"],
+                                                    "chunk_tokens": sum(tk for _, tk, _ in chunks)})
+
+    def _iteration_meta(self, chunks, decode) -> dict:
+        srv, dev = self.server, self.server.dev
+        MP = srv.max_pages
+        toks, pos, slots, emit, emit_ids = [], [], [], [], []
+        cu, prior, cbt = [0], [], []
+        r = 0
+        for rid, take, p in chunks:
+            pages = np.asarray(self.seq_pages[rid], np.int64)
+            q = np.arange(p, p + take)
+            toks.append(self.prompts[rid][p:p + take])
+            pos.append(q)
+            slots.append(pages[q // PAGE] * PAGE + q % PAGE)
+            cu.append(cu[-1] + take)
+            prior.append(p)
+            row = np.zeros(MP, np.int32)
+            row[:len(pages)] = pages
+            cbt.append(row)
+            r += take
+            if p + take >= self.records[rid].request.input_len:
+                emit.append(r - 1)
+                emit_ids.append(rid)
+        Tc = r
+        dctx, dbt = [], []
+        for rid in decode:
+            c = self.records[rid].ctx_len
+            pages = np.asarray(self.seq_pages[rid], np.int64)
+            toks.append(np.array([self.last_tok[rid]], np.int32))
+            pos.append(np.array([c - 1]))
+            slots.append(np.array([pages[(c - 1) // PAGE] * PAGE + (c - 1) % PAGE]))
+            dctx.append(c)
+            row = np.zeros(MP, np.int32)
+            row[:len(pages)] = pages
+            dbt.append(row)
+            emit.append(r)
+            emit_ids.append(rid)
+            r += 1
+        T = r
+
+        def d(a, dt=torch.int32):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(dev)
+
+        return {"T": T, "Tc": Tc, "n_chunks": len(chunks), "max_chunk": max([tk for _, tk, _ in chunks] or [1]),
+                "tokens": d(np.concatenate(toks)), "pos": d(np.concatenate(pos)), "slots": d(np.concatenate(slots)),
+                "cu": d(np.asarray(cu)), "prior": d(np.asarray(prior or [0])),
+                "cbt": d(np.stack(cbt) if cbt else np.zeros((1, MP), np.int32)),
+                "dctx": d(np.asarray(dctx or [1])), "dbt": d(np.stack(dbt) if dbt else np.zeros((1, MP), np.int32)),
+                "emit": d(np.asarray(emit, np.int64), torch.int64), "n_emit": len(emit), "emit_ids": emit_ids}
+
+    def _on_iteration(self, t: float, p: dict) -> None:
+        # release the pages of requests this iteration finishes BEFORE the base
+        # handler admits new ones (it frees their KV bytes, then starts the
+        # next iteration)
+        done = [rid for rid in p["decode"]
+                if self.records[rid].emitted + 1 >= self.records[rid].request.output_len]
+        done += [rid for rid, take, _ in p["chunks"]
+                 if self.progress[rid] + take >= self.records[rid].request.input_len
+                 and self.records[rid].request.output_len <= 1]
+        for rid in done:
+            self.pages.release(self.seq_pages.pop(rid))
+        super()._on_iteration(t, p)

@@ -10,7 +10,7 @@ layers to run, and the decode step's predicted latency (IEEE-equal).
 
 Fixtures: tests/golden/realtime_decisions_*.json, written by
 tests/test_realtime_gpu.py (HP_DECISIONS_OUT) and
-`python -m paper_2504_19516_b200.device.serve --realtime --decisions-out`
+`python -m paper_2504_19516_b200.device.serve --decisions-out` (real-time mode)
 on the B200.
 """
 
@@ -25,7 +25,7 @@ import pytest
 from paper_2504_19516_b200 import perf_model as PM
 from paper_2504_19516_b200 import scheduler as S
 from paper_2504_19516_b200 import workload as W
-from paper_2504_19516_b200.device.realtime import state_from_json, store_from_json
+from paper_2504_19516_b200.device.realtime import delta_decode, state_from_json, store_from_json
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 FIXTURES = sorted(GOLDEN.glob("realtime_decisions_*.json"))
@@ -67,7 +67,7 @@ def _replay(fix, sched, pm, wl):
     scfg = sched.SchedulerConfig(sm_step=cfgd["sm_step"], l_step=cfgd["l_step"])
     L = model.num_layers
     counts = {"prefill": 0, "decode": 0, "branches": set()}
-    for i, d in enumerate(fix["decisions"]):
+    for i, d in enumerate(delta_decode(fix["decisions"])):
         st = state_from_json(d["state"], (sched, pm))
         est = pm.PerfEstimator(model, gpu, store_from_json(d["store"], pm))
         if d["kind"] == "decode":

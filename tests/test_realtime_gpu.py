@@ -32,8 +32,8 @@ from paper_2504_19516_b200 import perf_model as PM  # noqa: E402
 from paper_2504_19516_b200 import scheduler as S  # noqa: E402
 from paper_2504_19516_b200.device.layer import PAGE, LayerWeights  # noqa: E402
 from paper_2504_19516_b200.device.partition import PartitionPool  # noqa: E402
-from paper_2504_19516_b200.device.realtime import (RealtimeSim, ServingModel, kv_pages_for,  # noqa: E402
-                                                   state_from_json, store_from_json)
+from paper_2504_19516_b200.device.realtime import (RealtimeChunked, RealtimeSim, ServingModel,  # noqa: E402
+                                                   kv_pages_for, state_from_json, store_from_json)
 from paper_2504_19516_b200.device.split import b200_gpu, b200_store  # noqa: E402
 from paper_2504_19516_b200.workload import TINY_MODEL, Request  # noqa: E402
 
@@ -137,3 +137,26 @@ def replay_decisions(decisions, cfg, sched=S, perf_model=PM) -> dict:
                                            want["layers"]), (d["state"], want)
         n[d["kind"]] += 1
     return n
+
+
+@pytest.mark.parametrize("chunk", [256, 64])
+def test_realtime_tiny_chunked_generates_oracle_tokens(tiny, chunk):
+    """The lockstep chunked baseline on the same model: hybrid batches with
+    cached-prefix chunks and decode rows, real tokens vs the oracle."""
+    (m, Wl, embed, final_norm, lm_head), srv, pool = tiny
+    prompts = _prompts()
+    cfg = _cfg("chunked")
+    cfg.policy = E.PolicySpec("chunked", chunk_size=chunk)
+    sim = RealtimeChunked(cfg, _trace(), srv, pool, prompts=prompts)
+    rep = sim.run()
+    assert rep.aggregates["finished"] == len(INPUTS), rep.aggregates
+    flips = 0
+    for rid, (L, o) in enumerate(zip(INPUTS, OUTPUTS)):
+        toks = sim.generated[rid]
+        assert len(toks) == o, (rid, len(toks), o)
+        r = oracle_check_generation(m, Wl, embed, final_norm, lm_head, prompts[rid], toks)
+        assert r["mismatches"] == 0, (rid, r)
+        flips += r["tie_flips"]
+    assert flips <= 2
+    assert sim.device_calls["hybrid_iterations"] > len(INPUTS)
+    assert len(sim.pages.free) == srv.kv_pages - 1  # every page returned
