@@ -59,6 +59,16 @@ def _ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+def _idle(until_arrival, device_busy: bool) -> None:
+    """Wait in the event loop: spin (event polls cost ~2 us) while a device
+    step is in flight -- a sleep's ~60 us wake-up latency would sit on the
+    GPU timeline between steps -- else sleep toward the next arrival."""
+    if device_busy:
+        return
+    if until_arrival is not None and until_arrival > 2e-4:
+        time.sleep(min(until_arrival - 1e-4, 1e-3))
+
+
 def bucket_of(b: int) -> int:
     for k in BUCKETS:
         if b <= k:
@@ -313,9 +323,14 @@ class RealtimeSim(E._ConcurrentSim):
         self.d_pending: _Pending | None = None
         self.batch_meta: dict | None = None
         self.trace_decisions = trace_decisions
+        self._in_complete = None
         self.decisions: list[dict] = []
         self.host_busy_s = 0.0
         self.device_calls = {"prefill_steps": 0, "decode_steps": 0, "decode_graph_replays": 0}
+        # device-timeline gap between a phase's step completing and its next
+        # step starting while work was waiting: the control plane's cost
+        self.gaps = {"prefill": [], "decode": []}
+        self._last_end = {"prefill": None, "decode": None}
 
     # ------------------------------------------------------------ clock
     def _clock(self) -> float:
@@ -346,7 +361,7 @@ class RealtimeSim(E._ConcurrentSim):
             if not due:
                 if not self.heap and not (self.p_pending or self.d_pending):
                     break
-                time.sleep(2e-5)
+                _idle(self.heap[0][0] - now if self.heap else None, bool(self.p_pending or self.d_pending))
                 continue
             t, k = min(due)
             h0 = time.perf_counter()
@@ -364,10 +379,13 @@ class RealtimeSim(E._ConcurrentSim):
                     handlers[kind](t, payload)
             elif k == 1:
                 p, self.p_pending = self.p_pending, None
+                self._in_complete = "prefill"
                 self._complete_prefill(t, p)
             else:
                 p, self.d_pending = self.d_pending, None
+                self._in_complete = "decode"
                 self._complete_decode(t, p)
+            self._in_complete = None
             self.host_busy_s += time.perf_counter() - h0
         torch.cuda.synchronize(dev)
         self.wall_s = time.perf_counter() - self._h0
@@ -450,9 +468,17 @@ class RealtimeSim(E._ConcurrentSim):
         b.record(ps.torch_stream)
         self.prefill_busy = True
         self.device_calls["prefill_steps"] += 1
-        self.p_pending = _Pending("prefill", b, a, {"layers": layers, "es": es, "pm": pm})
+        self.p_pending = _Pending("prefill", b, a, {"layers": layers, "es": es, "pm": pm,
+                                                    "back_to_back": self._in_complete == "prefill"})
+
+    def _gap(self, phase: str, p: _Pending, t_end: float) -> None:
+        prev = self._last_end[phase]
+        if prev is not None and p.payload.get("back_to_back"):
+            self.gaps[phase].append(self._dev_time(p.start) - prev)
+        self._last_end[phase] = t_end
 
     def _complete_prefill(self, t: float, p: _Pending) -> None:
+        self._gap("prefill", p, t)
         step_s = p.start.elapsed_time(p.end) * 1e-3
         layers = p.payload["layers"]
         self.occ_prefill += p.payload["pm"] * step_s
@@ -519,9 +545,11 @@ class RealtimeSim(E._ConcurrentSim):
         self.last_decode_event_t = t
         self.device_calls["decode_steps"] += 1
         self.device_calls["decode_graph_replays"] += 1
-        self.d_pending = _Pending("decode", e, a, {"batch": batch, "es": es, "dm": dm, "b": len(batch)})
+        self.d_pending = _Pending("decode", e, a, {"batch": batch, "es": es, "dm": dm, "b": len(batch),
+                                                   "back_to_back": self._in_complete == "decode"})
 
     def _complete_decode(self, t: float, p: _Pending) -> None:
+        self._gap("decode", p, t)
         step_s = p.start.elapsed_time(p.end) * 1e-3
         self.occ_decode += p.payload["dm"] * step_s
         batch = p.payload["batch"]
@@ -659,7 +687,7 @@ class RealtimeChunked(E._ChunkedSim):
             if not due:
                 if not self.heap and not self.pending:
                     break
-                time.sleep(2e-5)
+                _idle(self.heap[0][0] - now if self.heap else None, self.pending is not None)
                 continue
             t, k = min(due)
             h0 = time.perf_counter()

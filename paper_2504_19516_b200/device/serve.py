@@ -89,6 +89,7 @@ def run_realtime(policy: str, trace, server, pool, gpu, slo, chunk: int, decisio
     a.update(rep.extended)
     a.update(wall_s=sim.wall_s, host_busy_s=sim.host_busy_s, control_plane_frac=sim.host_busy_s / sim.wall_s,
              device_calls=dict(sim.device_calls),
+             step_gap_us={ph: (1e6 * statistics.mean(v) if v else None) for ph, v in getattr(sim, "gaps", {}).items()},
              generated_tokens=sum(len(v) for v in sim.generated.values()))
     if decisions_out is not None and policy == "bullet":
         g = gpu
@@ -121,6 +122,7 @@ def main(argv=None) -> int:
     ap.add_argument("--full-model", action="store_true", help="(--replay) all 32 layers resident")
     ap.add_argument("--slo", default="paper", choices=["paper", "r01"],
                     help="paper: ShareGPT SLOs of PAPER.md Table (3.0 ms/token, 150 ms); r01: 1.5 ms, 100 ms")
+    ap.add_argument("--slo-ms", default=None, help="norm_ttft_ms_per_token,tpot_ms (overrides --slo)")
     ap.add_argument("--decisions-out", default=None, help="(realtime bullet) log decisions for the replay test")
     a = ap.parse_args(argv)
 
@@ -138,6 +140,9 @@ def main(argv=None) -> int:
 
     gpu = b200_gpu()
     slo = PAPER_SLO if a.slo == "paper" else S.SloSpec(norm_ttft_s_per_token=1.5e-3, tpot_s=0.1)
+    if a.slo_ms:
+        p_ms, d_ms = (float(v) for v in a.slo_ms.split(","))
+        slo = S.SloSpec(norm_ttft_s_per_token=p_ms * 1e-3, tpot_s=d_ms * 1e-3)
     # config 4 prompt lengths: uniform 512-8192; outputs from the ShareGPT-like preset
     out_dist = TRACE_PRESETS["sharegpt-like"][1]
     trace = gen_poisson_trace(a.rate, a.duration, LengthDist("uniform", lo=512, hi=8192), out_dist, seed=a.seed)
@@ -194,6 +199,7 @@ def main(argv=None) -> int:
                 line.update(wall_s=max(p["wall_s"] for p in per),
                             control_plane_frac=statistics.mean(p["control_plane_frac"] for p in per),
                             device_calls=per[0]["device_calls"], decode_graphs_captured=graphs,
+                            step_gap_us=per[0]["step_gap_us"],
                             generated_tokens=sum(p["generated_tokens"] for p in per),
                             timing="wall clock; real tokens; device completions from CUDA events")
             print(json.dumps(line), flush=True)
