@@ -320,6 +320,28 @@ def lat(r) -> dict:
                 r.decode_steps / r.steps}
 
 
+# decode share of the dual-roofline co-run split (>= the measured n_d = 43;
+# tools/hbm_split_sweep.py: decode attention reaches 0.73 of HBM beside the
+# prefill from dm = 88, at both T = 4096 and 16384)
+HBM_SPLIT_DM = 88
+
+
+def hbm_targets(cr, dm: int, hbm_gbs: float, tf_burst: float) -> dict:
+    """Both north-star roofline targets at one co-executed split where the
+    decode side holds at least n_d SMs: decode
+    attention GB/s and the four prefill GEMMs' TFLOP/s, measured together."""
+    N = cr.n
+    r = cr.corun_hbm(N - dm, dm)
+    peak = tf_burst * (N - dm) / N
+    r.update(decode_attn_frac_of_hbm=(r["decode_attn_gbs"] or 0.0) / hbm_gbs,
+             prefill_gemms_frac_of_partition_peak=r["prefill_gemm_tflops"] / peak,
+             hbm_peak_gbs=hbm_gbs, partition_peak_tflops=peak,
+             note="prefill layers on pm SMs with per-GEMM CUDA events while the dm-SM side streams "
+                  "back-to-back decode-attention launches (B=32, ctx 2048); attention timed over the "
+                  "launches entirely inside the prefill window")
+    return r
+
+
 def study_T(cr, gpu, store, steps: int, dist, coll, sweep: bool = True) -> dict:
     """Config 2 at one chunk size: estimator split, co-run vs time-sliced vs
     chunked on the same kernels, and the brute-force regret check."""
@@ -498,6 +520,7 @@ def main(argv=None) -> int:
     pin_dy = torch.empty(DECODE_BATCH, h, dtype=torch.bfloat16, pin_memory=True)
     pin_px.copy_(cr.px.cpu())
     pin_dx.copy_(cr.dx.cpu())
+    cr.corun_e2e(pm, dm, args.warmup, ratio, pin_px, pin_py, pin_dx, pin_dy)  # warm-up (first-use costs)
     e2e_res = cr.corun_e2e(pm, dm, args.steps, ratio, pin_px, pin_py, pin_dx, pin_dy)
     e2e_span, e2e_tokens = job_totals(dist, e2e_res.span_s, e2e_res.tokens, coll)
     h2d = (T * h * 2 * args.steps + e2e_res.decode_steps * DECODE_BATCH * h * 2) // args.steps
@@ -515,6 +538,13 @@ def main(argv=None) -> int:
     units["attn"] = (-(-T // 256) * model.num_heads, pm)                   # k_fa2: 256-query units, one per CTA
     g_s = groups.group_s
     wave_idle = sum(g_s[k] * wave_stats(u, 1, n).idle_ratio for k, (u, n) in units.items()) / sum(g_s.values())
+
+    # ---- both north-star rooflines at one co-executed split with dm >= n_d
+    hbm_split = hbm_targets(cr, HBM_SPLIT_DM, hbm_gbs, tf_burst)
+
+    # ---- SM idle MEASURED inside the co-run: per-CTA %globaltimer stamps of
+    # the prefill layer's five kernel groups + the decode side's windows
+    midle = cr.measured_idle(pm, dm, ratio)
 
     # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
     dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}
@@ -567,7 +597,17 @@ def main(argv=None) -> int:
         "time_sliced": dict(lat(ts_eq), note="same kernels and work, one full-GPU stream, prefill layer then "
                                              "its decode steps"),
         "per_T": per_T,
-        "sm_idle_pct": {"partition": 100 * res.partition_idle(N), "wave_model_prefill_layer": 100 * wave_idle,
+        "sm_idle_pct": {"corun_measured": 100 * midle["corun_measured"],
+                        "prefill_partition_measured": 100 * midle["prefill_partition_measured"],
+                        "prefill_partition_wave_model": 100 * midle["prefill_partition_predicted"],
+                        "groups_measured_vs_model": {g: {"measured": 100 * v["measured_idle"],
+                                                         "wave_model": 100 * v["predicted_idle"],
+                                                         "span_us": v["span_us"]}
+                                                     for g, v in midle["groups"].items()},
+                        "measured_note": "per-CTA %globaltimer stamps (hp_set_trace kind 2) of one co-run prefill "
+                                         "layer's qkv/attn/o_proj/mlp kernels on pm SMs + the decode graph's "
+                                         "windows on dm SMs: 1 - busy SM-time / (N x layer window)",
+                        "partition": 100 * res.partition_idle(N), "wave_model_prefill_layer": 100 * wave_idle,
                         "prefill_group_us": {k: 1e6 * v for k, v in g_s.items()},
                         "prefill_group_note": "per-group events from a separate co-run of the same split just "
                                               "before the timed region (which records events around "
@@ -581,6 +621,7 @@ def main(argv=None) -> int:
                      "frac": achieved / peak, "traffic": traffic, "kernel": "mlp_up_gate (tcgen05 GEMM + SiLU)",
                      "peak_basis": f"bf16_tflops burst ({peak_src}) x pm/N = {tf_burst} x {pm}/{N}",
                      "frac_of_full_gpu_peak": achieved / tf_burst},
+        "roofline_targets_split": hbm_split,
         "roofline_decode_attn": {"bound": "hbm", "unit": "GB/s", "peak": hbm_gbs,
                                  "bytes_per_launch": cr.decode_attn_bytes(),
                                  **{k: {"achieved": v, "frac": v / hbm_gbs} for k, v in dattn.items()}},

@@ -207,10 +207,13 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
                     int max_seqlen, int Hq, int Hkv, int d, float scale, int max_ctas,
                     void* stream);
 
-/* Development aid: kernel timeline traces.  kind 0: k_fa2 CTA 0 softmax/MMA
- * wait stamps (clock64, int64 [12][256]); kind 1: k_gemm_swap_sk per-CTA
- * globaltimer stamps (uint64 [grid][6]: entry, prologue done, producer
- * done, MMA done, epilogue done, exit).  NULL disables. */
+/* Kernel timeline traces.  kind 0: k_fa2 CTA 0 softmax/MMA wait stamps
+ * (clock64, int64 [12][256]); kind 1: k_gemm_swap_sk per-CTA globaltimer
+ * stamps (uint64 [grid][6]: entry, prologue done, producer done, MMA done,
+ * epilogue done, exit); kind 2 (one-shot, SM-idle measurement of config 2/3):
+ * the NEXT hp_gemm / hp_gemm_qkv_rope / hp_prefill_attn(_paged) launch on
+ * this thread writes per-CTA {smid, start_ns, end_ns} (uint64 [grid][3]) and
+ * disarms it.  NULL disables. */
 int hp_set_trace(int kind, void* buf);
 
 /* Prefix-aware (chunked) prefill attention over the paged cache

@@ -61,6 +61,7 @@ struct FaParams {
   const int* prior_lens;
   int max_pages, page, Hkv;
   long long* trace;  // optional clock64 trace of CTA 0 (hp_set_fa_trace; development aid)
+  uint64_t* cta_times;  // optional [grid][3] = {smid, start_ns, end_ns} (SM-idle measurement)
 };
 
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo_bytes) {
@@ -229,6 +230,8 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   pdl_wait();  // qkv from the QKV GEMM / rope_kv_write; `out` may still be read upstream
+  uint64_t t_start = 0;
+  if (p.cta_times != nullptr && threadIdx.x == 0) t_start = globaltimer();
   const uint32_t tmem = *tmem_slot;
   const int total = p.nseq * p.n_qt * p.Hq;
   // per SM sub-partition: one warp of each warpgroup, 96 + 200 + 200 <= 3 x 168 (the pool the launch got)
@@ -491,6 +494,11 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (p.cta_times != nullptr && threadIdx.x == 0) {
+    p.cta_times[blockIdx.x * 3 + 0] = smid();
+    p.cta_times[blockIdx.x * 3 + 1] = t_start;
+    p.cta_times[blockIdx.x * 3 + 2] = globaltimer();
+  }
 }
 
 template <int D, bool PAGED>
@@ -541,6 +549,7 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
   p.ldo = ldo;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = static_cast<long long*>(trace_buf(TRACE_FA));
+  p.cta_times = take_cta_trace();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return d == 128 ? launch_fa2<128, false>(tq, tk, tv, p, max_seqlen, max_ctas, st)
                   : launch_fa2<64, false>(tq, tk, tv, p, max_seqlen, max_ctas, st);
@@ -580,6 +589,7 @@ extern "C" int hp_prefill_attn_paged(const void* q, int ldq, const void* kcache,
   p.max_pages = max_pages;
   p.page = page;
   p.Hkv = Hkv;
+  p.cta_times = take_cta_trace();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return d == 128 ? launch_fa2<128, true>(tq, tq, tq, p, max_seqlen, max_ctas, st)
                   : launch_fa2<64, true>(tq, tq, tq, p, max_seqlen, max_ctas, st);

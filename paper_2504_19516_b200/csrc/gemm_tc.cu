@@ -617,13 +617,14 @@ extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, 
   p.Hq = Hq;
   p.Hkv = Hkv;
   p.hd = d;
+  p.cta_times = take_cta_trace();
   return plan_and_launch(ta, p, T, N, K, BN, max_ctas, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                        const void* R, int ldr, int T, int N, int K, int epilogue, int max_ctas,
                        void* stream) {
-  return hp_gemm_traced(X, ldx, W, ldw, Y, ldy, R, ldr, T, N, K, epilogue, max_ctas, nullptr, stream);
+  return hp_gemm_traced(X, ldx, W, ldw, Y, ldy, R, ldr, T, N, K, epilogue, max_ctas, take_cta_trace(), stream);
 }
 
 // Tile-width choice for a partition of `ctas` SMs.  A persistent grid over

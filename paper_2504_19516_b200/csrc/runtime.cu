@@ -129,8 +129,13 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
   return HP_OK;
 }
 
-static void* g_trace[TRACE_KINDS] = {nullptr, nullptr};
+static void* g_trace[TRACE_KINDS] = {nullptr, nullptr, nullptr};
 void* trace_buf(int kind) { return g_trace[kind]; }
+uint64_t* take_cta_trace() {
+  void* b = g_trace[TRACE_CTAS];
+  g_trace[TRACE_CTAS] = nullptr;
+  return static_cast<uint64_t*>(b);
+}
 
 }  // namespace hp
 

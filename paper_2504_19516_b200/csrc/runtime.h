@@ -72,8 +72,11 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
 int device_sm_count();
 
 // Development aid: per-kernel trace buffers (hp_set_trace); nullptr = off.
-enum { TRACE_FA = 0, TRACE_SWAP = 1, TRACE_KINDS = 2 };
+enum { TRACE_FA = 0, TRACE_SWAP = 1, TRACE_CTAS = 2, TRACE_KINDS = 3 };
 void* trace_buf(int kind);
+// TRACE_CTAS is one-shot: the next prefill GEMM / attention launch takes
+// the armed buffer (per-CTA {smid, start_ns, end_ns}) and disarms it.
+uint64_t* take_cta_trace();
 
 // PDL on unless the environment sets HP_PDL=0 (A/B measurement).
 bool pdl_enabled();

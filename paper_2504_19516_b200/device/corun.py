@@ -182,11 +182,11 @@ class CoRunner:
         torch.cuda.synchronize()
 
     # ------------------------------------------------------------- launches
-    def prefill_layer(self, ps: PhaseStreams, timers=None, x=None, y=None) -> int:
+    def prefill_layer(self, ps: PhaseStreams, timers=None, x=None, y=None, cta_trace=None) -> int:
         x = self.px if x is None else x
         y = self.py if y is None else y
         return self.layer.prefill(x, y, self.psc, self.p_cu, 1, self.T, self.p_pos, self.p_slots,
-                                  self.pcache, ps.sms, ps.torch_stream, timers)
+                                  self.pcache, ps.sms, ps.torch_stream, timers, cta_trace)
 
     def decode_layer(self, ds: PhaseStreams) -> int:
         return self.layer.decode(self.dx, self.dy, self.dsc, self.ctx, self.d_pos, self.d_slots,
@@ -235,7 +235,7 @@ class CoRunner:
         return ms[len(ms) // 2] * 1e-3
 
     def corun(self, pm: int, dm: int, steps: int, decode_per_step, time_upgate: bool = False,
-              copy_in=None, copy_out=None, time_groups: bool = False) -> CoRunResult:
+              copy_in=None, copy_out=None, time_groups: bool = False, cta_trace=None) -> CoRunResult:
         """`steps` prefill layers on pm SMs co-executed with
         decode layer-steps on dm SMs (`decode_schedule`).  time_upgate:
         events around the mlp_up_gate GEMM only (the roofline kernel);
@@ -262,7 +262,7 @@ class CoRunner:
                 if copy_in is not None:
                     copy_in(PREFILL, ps.torch_stream)
                 p_ev[s][0].record(ps.torch_stream)
-                self.prefill_layer(ps, ug_ev[s] if ug_ev else None)
+                self.prefill_layer(ps, ug_ev[s] if ug_ev else None, cta_trace=cta_trace if s == steps - 1 else None)
                 p_ev[s][1].record(ps.torch_stream)
                 if copy_out is not None:
                     copy_out(PREFILL, ps.torch_stream)
@@ -364,6 +364,108 @@ class CoRunner:
         torch.cuda.synchronize()
         span = max(start.elapsed_time(e) for e in (end_p, end_d, end_o)) * 1e-3
         return CoRunResult(pm, dm, steps, sum(sched), span, steps * self.T, sum(sched) * self.B)
+
+    def corun_hbm(self, pm: int, dm: int, steps: int = 2) -> dict:
+        """North-star rooflines at ONE co-executed split: prefill layers on
+        pm SMs (per-group CUDA events around the four GEMMs) while the dm-SM
+        side streams back-to-back decode-attention launches (B sequences of
+        context C) for the whole prefill window.  Returns the GEMMs' TFLOP/s
+        and the attention's algorithmic GB/s over the launches that ran
+        entirely inside the prefill window -- both measured at the same time
+        on the device."""
+        ps, ds = self.pool.split(pm, dm)
+        m = self.model
+        qkv = self.dsc.qkv[:self.B]
+
+        def attn():
+            lib.decode_attn(qkv, self.dcache.k, self.dcache.v, self.block_table, self.ctx, self.dsc.attn[:self.B],
+                            m.num_heads, m.num_kv_heads, m.head_dim, PAGE, self.layer.scale, ws=self.dsc.attn_ws,
+                            max_ctas=ds.sms, stream=ds.torch_stream)
+
+        t_p = self.isolated(PREFILL, pm, reps=2)
+        with torch.cuda.stream(ds.torch_stream):
+            attn()  # warm
+        a0, a1 = _ev(), _ev()
+        with torch.cuda.stream(ds.torch_stream):
+            torch.cuda._sleep(200_000)
+            a0.record(ds.torch_stream)
+            for _ in range(20):
+                attn()
+            a1.record(ds.torch_stream)
+        torch.cuda.synchronize()
+        t_a = a0.elapsed_time(a1) * 1e-3 / 20
+        n_attn = int(steps * t_p / t_a * 1.3) + 4
+        ctrl = torch.cuda.current_stream(self.dev)
+        start = _ev()
+        p_ev = [(_ev(), _ev()) for _ in range(steps)]
+        g_ev = [{g: (_ev(), _ev()) for g in GROUPS} for _ in range(steps)]
+        d_ev = [(_ev(), _ev()) for _ in range(n_attn)]
+        torch.cuda._sleep(400_000)
+        start.record(ctrl)
+        ps.torch_stream.wait_event(start)
+        ds.torch_stream.wait_event(start)
+        with torch.cuda.stream(ds.torch_stream):
+            for e0, e1 in d_ev:
+                e0.record(ds.torch_stream)
+                attn()
+                e1.record(ds.torch_stream)
+        with torch.cuda.stream(ps.torch_stream):
+            for s in range(steps):
+                p_ev[s][0].record(ps.torch_stream)
+                self.prefill_layer(ps, g_ev[s])
+                p_ev[s][1].record(ps.torch_stream)
+        torch.cuda.synchronize()
+        win = [(start.elapsed_time(a) * 1e-3, start.elapsed_time(b) * 1e-3) for a, b in p_ev]
+        p0, p1 = win[0][0], win[-1][1]
+        inside = [b - a for a, b in ((start.elapsed_time(x) * 1e-3, start.elapsed_time(y) * 1e-3) for x, y in d_ev)
+                  if a >= p0 and b <= p1]
+        gemm_s = statistics.median(sum(e[g][0].elapsed_time(e[g][1]) * 1e-3 for g in GROUPS if g != "attn")
+                                   for e in g_ev)
+        h = m.hidden
+        gemm_flops = 2.0 * self.T * h * (m.qkv_out_dim + h + 3 * mlp_width(m))
+        return {"pm": pm, "dm": dm, "T": self.T, "prefill_layers": steps,
+                "decode_attn_launches_inside": len(inside),
+                "decode_attn_gbs": self.decode_attn_bytes() / statistics.median(inside) / 1e9 if inside else None,
+                "decode_attn_alone_gbs": self.decode_attn_bytes() / t_a / 1e9,
+                "prefill_gemm_tflops": gemm_flops / gemm_s / 1e12,
+                "prefill_layer_us": 1e6 * statistics.median(b - a for a, b in win)}
+
+    def measured_idle(self, pm: int, dm: int, decode_per_step) -> dict:
+        """SM idle of the co-run MEASURED on the device (config 3's method
+        inside config 2): the last of three co-run prefill layers records
+        every CTA's {smid, start, end} (%globaltimer) for its five kernel
+        groups while the decode graph replays on the dm side.  Per group:
+        measured idle = 1 - sum(CTA busy) / (pm x group span), beside the
+        wave model's wave_stats(units, 1, slots) (perf_model.py:157-169).
+        Whole co-run (prefill layer window): 1 - (prefill CTA busy + dm x
+        decode busy) / (N x window); the two RMSNorm launches and the
+        decode kernels' intra-graph gaps count as busy only where timed."""
+        from ..perf_model import wave_stats
+
+        N, T, m = self.n, self.T, self.model
+        traces = {g: torch.zeros(N, 3, dtype=torch.int64, device=self.dev) for g in GROUPS}
+        r = self.corun(pm, dm, 3, decode_per_step, time_groups=True, cta_trace=traces)
+        w = self.layer.W
+        units = {}
+        for g, wt in (("qkv", w.w_qkv), ("o_proj", w.w_o), ("mlp_up_gate", w.w_ug), ("mlp_down", w.w_down)):
+            _, tiles, cpt = lib.gemm_plan(T, wt.shape[0], pm)
+            units[g] = (tiles, pm // cpt)
+        units["attn"] = (-(-T // 256) * m.num_heads, pm)
+        groups, busy_sm_s = {}, 0.0
+        for g in GROUPS:
+            idle, span, ctas = lib.cta_idle(traces[g], pm)
+            busy_sm_s += (1.0 - idle) * pm * span
+            groups[g] = {"measured_idle": idle, "predicted_idle": wave_stats(units[g][0], 1, units[g][1]).idle_ratio,
+                         "span_us": 1e6 * span, "ctas": ctas, "units": units[g][0], "slots": units[g][1]}
+        p0, p1 = r.prefill_window_s[-1]
+        dec = sum(max(0.0, min(p1, b) - max(p0, a)) for a, b in r.decode_window_s)
+        window = p1 - p0
+        tot_span = sum(v["span_us"] for v in groups.values())
+        return {"groups": groups,
+                "prefill_partition_measured": sum(v["measured_idle"] * v["span_us"] for v in groups.values()) / tot_span,
+                "prefill_partition_predicted": sum(v["predicted_idle"] * v["span_us"] for v in groups.values()) / tot_span,
+                "corun_measured": 1.0 - (busy_sm_s + dm * dec) / (N * window),
+                "window_us": 1e6 * window, "decode_busy_in_window_us": 1e6 * dec}
 
     def time_sliced(self, steps: int, decode_per_step) -> CoRunResult:
         """Same work, one full-GPU stream: prefill layer then its decode steps."""

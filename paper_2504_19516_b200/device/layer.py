@@ -197,22 +197,27 @@ class DeviceLayer:
 
     # -------------------------------------------------------------- prefill
     def prefill(self, x, y, sc: PrefillScratch, cu_seqlens, nseq: int, max_seqlen: int,
-                positions, slots, cache: KVCache, sms: int, stream=None, timers=None) -> int:
+                positions, slots, cache: KVCache, sms: int, stream=None, timers=None, cta_trace=None) -> int:
         """y = layer(x) for the packed prefill tokens of x [T, h]; writes the
         sequences' K/V into `cache` at `slots`.  Returns the launch count.
         `timers`: optional {kernel group: (start_event, end_event)} recorded on
         `stream` around that group's main launch (qkv, attn, o_proj,
-        mlp_up_gate, mlp_down)."""
+        mlp_up_gate, mlp_down).  `cta_trace`: optional {group: int64 [grid, 3]}
+        receiving that launch's per-CTA {smid, start_ns, end_ns}."""
         T = x.shape[0]
         qkv = sc.qkv[:T]
         Hq, Hkv, d = self.Hq, self.Hkv, self.d
         timers = timers or {}
         rs = stream if stream is not None else torch.cuda.current_stream().cuda_stream
 
+        cta_trace = cta_trace or {}
+
         def mark(name, i):
             ev = timers.get(name)
             if ev is not None:
                 ev[i].record(torch.cuda.ExternalStream(rs) if isinstance(rs, int) else rs)
+            if i == 0 and name in cta_trace:
+                lib.arm_cta_trace(cta_trace[name])
 
         lib.rmsnorm(x, self.W.attn_norm, sc.xn[:T], EPS, sms, stream)
         mark("qkv", 0)

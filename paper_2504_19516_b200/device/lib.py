@@ -319,6 +319,31 @@ def copy_rows(src, dst, max_ctas: int = 148, stream=None) -> None:
                               src.shape[1] * es, max_ctas, _stream(stream)), "hp_copy_rows")
 
 
+def set_trace(kind: int, buf) -> None:
+    check(load().hp_set_trace(kind, _ptr(buf)), "hp_set_trace")
+
+
+TRACE_CTAS = 2
+
+
+def arm_cta_trace(buf) -> None:
+    """The next prefill GEMM / attention launch records per-CTA {smid,
+    start_ns, end_ns} into `buf` (uint64/int64 [grid, 3]); one-shot."""
+    set_trace(TRACE_CTAS, buf)
+
+
+def cta_idle(times, sms: int) -> tuple[float, float, int]:
+    """(idle fraction, span s, CTAs) of one traced launch on an `sms`-SM
+    partition: 1 - sum(CTA busy) / (sms x kernel span) -- config 3's
+    measured idle, against wave_stats(units, 1, slots) (perf_model.py:157-169)."""
+    t = times.cpu()
+    t = t[t[:, 2] > 0]
+    start, end = t[:, 1], t[:, 2]
+    span = float(end.max() - start.min())
+    busy = float((end - start).sum())
+    return 1.0 - busy / (sms * span), span * 1e-9, int(t.shape[0])
+
+
 def membw(src, ctas: int, method: int, out, stream=None) -> None:
     check(load().hp_membw(_ptr(src), src.numel() * src.element_size(), ctas, method, _ptr(out),
                           _stream(stream)), "hp_membw")

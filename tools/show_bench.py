@@ -21,8 +21,11 @@ for e in d["per_T"]:
           f"wins={e['corun_vs_time_sliced']['wins']} ratio={e['corun_vs_time_sliced']['tokens_per_s_ratio']:.3f} "
           f"chunked {[round(x['tokens_per_s']/1e6, 3) for x in e['chunked']]} "
           f"best {rs.get('best_measured', {}).get('dm')} regret {rs.get('estimator_regret')}")
-    for cnd in rs.get("candidates", []):
-        print("     ", cnd)
+    if "-v" in sys.argv:
+        for cnd in rs.get("candidates", []):
+            print("     ", cnd)
 if d.get("cpu_baseline"):
     cb = dict(d["cpu_baseline"])
     print("cpu", json.dumps(cb)[:1500])
+if d.get("roofline_targets_split"):
+    print("hbm split", d["roofline_targets_split"])
