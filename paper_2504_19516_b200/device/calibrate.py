@@ -12,7 +12,11 @@ Writes
   calibration.jsonl  alpha samples (prefill / decode, measured / SRM) and the
                      contention table, in the reference's JSONL format
                      (CalibrationStore.load_jsonl reads it)
-  mape.json          estimator error on held-out points (Table 3 analogue)
+  mape.json          estimator error on held-out points (Table 3 analogue):
+                     36 prefill + 120 decode grid states + the decode SM axis
+
+Also reachable as the reference's own command: `smshare calibrate --device
+b200` (cli.py cmd_calibrate).
 """
 
 from __future__ import annotations
@@ -23,9 +27,8 @@ from pathlib import Path
 
 import torch
 
-from ..engine import CalibrationBudget, canonical_decode_es, mape
-from ..perf_model import CalibrationStore, ExecutionState, PerfEstimator, b200_spec, update_online
-from ..perf_model import srm_decode_step_s, srm_prefill_layer_s
+from ..engine import CalibrationBudget
+from ..perf_model import CalibrationStore, PerfEstimator, b200_spec
 from ..workload import MODEL_PRESETS
 from . import lib
 from .executor import B200Executor
@@ -44,7 +47,7 @@ def bandwidth_curve(pool: PartitionPool, grid, nbytes: int = 1 << 30, reps: int 
         with torch.cuda.stream(st.torch_stream):
             for _ in range(reps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda._sleep(100_000)
+                lib.hold(st.torch_stream, 100_000)
                 a.record()
                 lib.membw(buf, st.sms, 1, out, stream=st.torch_stream)
                 b.record()
@@ -73,7 +76,7 @@ def reconfig_latency(pool: PartitionPool, dm_a: int = 32, dm_b: int = 48, reps: 
     def gap(first, second, cross: bool) -> float:
         ev = torch.cuda.Event()
         with torch.cuda.stream(first.torch_stream):
-            torch.cuda._sleep(400_000)  # both launches queued before the first runs
+            lib.hold(first.torch_stream, 400_000)  # both launches queued before the first runs
             lib.probe(t1, first.sms, spin_ns=5000, stream=first.torch_stream)
             ev.record(first.torch_stream)
         st = second.torch_stream if cross else first.torch_stream
@@ -106,17 +109,31 @@ def fit_n_d(curve, d_peak: float) -> int:
     return best
 
 
-def main(argv=None) -> int:
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default="calib")
-    ap.add_argument("--model", default="llama3-8b")
-    ap.add_argument("--quick", action="store_true")
-    a = ap.parse_args(argv)
-    out = Path(a.out)
+B200_BUDGET = dict(prefill_tokens=(512, 1024, 4096, 16384),
+                  decode_tokens=(1024, 4096, 16384, 65536, 262144, 1048576, 2097152),
+                  contention_prefill_lens=(1024, 4096, 16384))
+# held-out points (disjoint from the budget's SM counts and token counts):
+# 36 prefill and 120 decode states, plus the decode SM axis at the budget's
+# token counts on every 8-SM share not in the budget
+HELD_OUT = dict(prefill_seq_lens=(768, 2048, 3072, 6144, 8192, 12288), prefill_sms=(140, 124, 100, 68, 36, 20),
+                decode_ctx_lens=(1536, 3072, 6144, 12288), decode_batch_sizes=(1, 8, 24, 64, 128, 192),
+                decode_sms=(24, 40, 56, 96, 136))
+
+
+def calibrate_b200(model, out: Path, quick: bool = False, pool: PartitionPool | None = None) -> dict:
+    """The reference's calibration flow (cli.py:415-458 cmd_calibrate:
+    build_calibration_store over a budget, then the decode SM-axis / decode
+    grid / prefill grid MAPE helpers of engine.py:884-928) with the B200 as
+    the oracle: every sample and every held-out point is a CUDA-event
+    measurement of the real kernels on a green-context partition.  Also
+    measures the GpuSpec half (HBM curve -> n_d, repartition latency).
+    Writes gpu.json, bandwidth.json, calibration.jsonl, mape.json to `out`."""
+    from ..engine import (build_calibration_store, canonical_decode_es, decode_mape_grid, decode_mape_sm_axis,
+                          prefill_mape_grid)
+
     out.mkdir(parents=True, exist_ok=True)
-    model = MODEL_PRESETS[a.model]
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    pool = PartitionPool(0)
+    pool = pool or PartitionPool(0)
     N = pool.n
     grid = [8, 16, 24, 32, 40, 48, 56, 64, 80, 96, 112, 128, 144, N]
     curve = bandwidth_curve(pool, grid)
@@ -126,48 +143,76 @@ def main(argv=None) -> int:
     rc = reconfig_latency(pool)
     (out / "gpu.json").write_text(json.dumps({**{k: getattr(gpu, k) for k in
                                                 ("name", "num_sms", "c_peak", "d_peak", "w_peak", "n_d", "n_w")},
+                                             "n_w_note": "preset: collective bandwidth vs SM count needs NVLink "
+                                                         "peers (one GPU per gpurun call)",
                                              "reconfig_s": rc["reconfig_s"], "reconfig_gaps_us": rc},
                                              indent=2) + "\n")
     (out / "bandwidth.json").write_text(json.dumps({"sms_vs_bytes_per_s": curve, "n_d_fit": n_d}, indent=2) + "\n")
 
-    ex = B200Executor(model, gpu, pool=pool, max_prefill_tokens=16384)
+    ex = B200Executor(model, gpu, pool=pool, max_prefill_tokens=32768)
+    b = dict(B200_BUDGET)
+    if quick:
+        b = dict(prefill_tokens=(1024, 4096), decode_tokens=(16384, 65536), contention_prefill_lens=(4096,))
+    # SM axes: interior to every held-out point (prefill shares are N - 8k on
+    # the green-context grid); the held-out shares are not sampled
     budget = CalibrationBudget(
-        prefill_sms=(N, N - 32, N - 64, N - 96) if not a.quick else (N, N - 64),
-        prefill_tokens=(512, 1024, 4096, 16384) if not a.quick else (1024, 4096),
-        decode_sms=(8, 16, 32, 64, N) if not a.quick else (16, 64),
-        decode_tokens=(4096, 16384, 65536, 262144) if not a.quick else (16384, 65536),
-        contention_sms=(8, 16, 32, 64) if not a.quick else (16, 32),
-        contention_prefill_lens=(1024, 4096, 16384) if not a.quick else (4096,))
-    store = CalibrationStore()
-    for sms in budget.prefill_sms:
-        for tok in budget.prefill_tokens:
-            es = ExecutionState(prefill_lens=(tok,), prefill_sms=sms)
-            update_online(store, "prefill", es, ex.prefill_layer_s(es), srm_prefill_layer_s(es, model, gpu))
-    for sms in budget.decode_sms:
-        for tok in budget.decode_tokens:
-            es = canonical_decode_es(tok, sms)
-            update_online(store, "decode", es, ex.decode_step_s(es), srm_decode_step_s(es, model, gpu))
-    for sms in budget.contention_sms:
-        for sl in budget.contention_prefill_lens:
-            store.contention_bw[(sms, sl)] = ex.contention_bw(sms, sl)
+        prefill_sms=(N, N - 16, N - 32, N - 64, N - 96, N - 120, N - 136) if not quick else (N, N - 64),
+        prefill_tokens=b["prefill_tokens"],
+        decode_sms=(8, 16, 32, 48, 64, 80, 112, N) if not quick else (16, 64), decode_tokens=b["decode_tokens"],
+        contention_sms=(8, 16, 32, 64) if not quick else (16, 32),
+        contention_prefill_lens=b["contention_prefill_lens"])
+    store = build_calibration_store(ex, budget)
     store.dump_jsonl(out / "calibration.jsonl")
 
-    # held-out error of the calibrated estimator (Table 3 analogue)
     est = PerfEstimator(model, gpu, CalibrationStore.load_jsonl(out / "calibration.jsonl"))
-    pre, dec = [], []
-    for sms in ((N - 16, N - 48, N - 80) if not a.quick else (N - 32,)):
-        for tok in ((768, 2048, 8192) if not a.quick else (2048,)):
-            es = ExecutionState(prefill_lens=(tok,), prefill_sms=sms)
-            pre.append((ex.prefill_layer_s(es), est.prefill_layer_s([tok], sms)))
-    for sms in ((24, 48, 96) if not a.quick else (32,)):
-        for tok in ((8192, 32768, 131072) if not a.quick else (32768,)):
-            es = canonical_decode_es(tok, sms)
-            dec.append((ex.decode_step_s(es), est.decode_step_s(list(es.decode_ctx_lens), sms)))
-    rep = {"prefill_mape": mape(pre), "decode_mape": mape(dec), "prefill_pairs": pre, "decode_pairs": dec,
-           "n_alpha_samples": len(store.alpha_samples), "n_contention_samples": len(store.contention_bw)}
-    (out / "mape.json").write_text(json.dumps(rep, indent=2) + "\n")
-    print(json.dumps({"n_d": n_d, "d_peak": d_peak, "prefill_mape": rep["prefill_mape"],
-                      "decode_mape": rep["decode_mape"]}))
+    h = HELD_OUT if not quick else dict(prefill_seq_lens=(2048,), prefill_sms=(116,), decode_ctx_lens=(3072,),
+                                        decode_batch_sizes=(8,), decode_sms=(40,))
+    sm_axis = [s for s in range(8, N, 8) if s not in budget.decode_sms]
+    rep = {"device": "b200", "n_alpha_samples": len(store.alpha_samples),
+           "n_contention_samples": len(store.contention_bw),
+           "budget": {k: list(getattr(budget, k)) for k in ("prefill_sms", "prefill_tokens", "decode_sms",
+                                                           "decode_tokens", "contention_sms",
+                                                           "contention_prefill_lens")},
+           "held_out": {k: list(v) for k, v in h.items()},
+           "decode": {"sm_axis_mape": {str(tok): decode_mape_sm_axis(ex, est, tok, sm_axis if not quick else [40])
+                                       for tok in budget.decode_tokens},
+                      "grid_mape": decode_mape_grid(ex, est, h["decode_ctx_lens"], h["decode_batch_sizes"],
+                                                    h["decode_sms"]),
+                      "grid_points": len(h["decode_ctx_lens"]) * len(h["decode_batch_sizes"]) * len(h["decode_sms"])},
+           "prefill": {"grid_mape": prefill_mape_grid(ex, est, h["prefill_seq_lens"], h["prefill_sms"]),
+                       "grid_points": len(h["prefill_seq_lens"]) * len(h["prefill_sms"])},
+           "n_d": n_d, "d_peak": d_peak}
+    # per-point detail of the decode grid (measured, predicted), same states
+    # as decode_mape_grid
+    from ..perf_model import ExecutionState
+
+    pts = []
+    for cl in h["decode_ctx_lens"]:
+        for bs in h["decode_batch_sizes"]:
+            for dm in h["decode_sms"]:
+                es = ExecutionState(decode_ctx_lens=tuple([cl] * bs), decode_sms=dm)
+                pts.append([cl, bs, dm, ex.decode_step_s(es), est.decode_step_s([cl] * bs, dm)])
+    rep["decode"]["grid_points_detail"] = pts
+    axis = []
+    for tok in budget.decode_tokens:
+        for dm in (sm_axis if not quick else [40]):
+            es = canonical_decode_es(tok, dm)
+            axis.append([tok, dm, ex.decode_step_s(es), est.decode_step_s(list(es.decode_ctx_lens), dm)])
+    rep["decode"]["sm_axis_points_detail"] = axis
+    (out / "mape.json").write_text(json.dumps(rep, indent=2, sort_keys=True) + "\n")
+    return rep
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="calib")
+    ap.add_argument("--model", default="llama3-8b")
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args(argv)
+    rep = calibrate_b200(MODEL_PRESETS[a.model], Path(a.out), a.quick)
+    print(json.dumps({"n_d": rep["n_d"], "d_peak": rep["d_peak"], "prefill_grid_mape": rep["prefill"]["grid_mape"],
+                      "decode_grid_mape": rep["decode"]["grid_mape"],
+                      "decode_sm_axis_mape": rep["decode"]["sm_axis_mape"]}))
     return 0
 
 

@@ -221,7 +221,7 @@ class CoRunner:
         g = self.decode_graph(st) if phase == DECODE else None
         with torch.cuda.stream(st.torch_stream):
             for _ in range(reps + 1):
-                torch.cuda._sleep(200_000)
+                lib.hold(st.torch_stream, 200_000)
                 a, b = _ev(), _ev()
                 a.record(st.torch_stream)
                 if phase == PREFILL:
@@ -387,7 +387,7 @@ class CoRunner:
             attn()  # warm
         a0, a1 = _ev(), _ev()
         with torch.cuda.stream(ds.torch_stream):
-            torch.cuda._sleep(200_000)
+            lib.hold(ds.torch_stream, 200_000)
             a0.record(ds.torch_stream)
             for _ in range(20):
                 attn()
@@ -576,7 +576,7 @@ class CoRunner:
         with torch.cuda.stream(st.torch_stream):
             launch()
             for _ in range(3):
-                torch.cuda._sleep(200_000)
+                lib.hold(st.torch_stream, 200_000)
                 a, b = _ev(), _ev()
                 a.record(st.torch_stream)
                 for _ in range(reps):

@@ -317,9 +317,11 @@ class B200Executor:
             return self.prefill_layer_s(es) / srm_prefill_layer_s(es, self.model, self.gpu)
         from ..engine import canonical_decode_es
 
-        # alpha is a ratio, so a canonical batch beyond the resident scratch is
-        # measured at the largest batch of the same per-sequence context
-        es = canonical_decode_es(min(int(tokens), self.max_decode_batch * 1024), sms)
+        # the reference's canonical batch (<= 256 sequences of ~1k, longer
+        # contexts beyond 256k tokens) -- measured at its real size
+        es = canonical_decode_es(int(tokens), sms)
+        if es.decode_batch > self.max_decode_batch:
+            raise InvalidArgumentError(f"canonical decode batch {es.decode_batch} exceeds max_decode_batch")
         return self.decode_step_s(es) / srm_decode_step_s(es, self.model, self.gpu)
 
     def contention_bw(self, sms: int, co_prefill_len: int, nbytes: int = 1 << 30) -> float:

@@ -319,6 +319,27 @@ def copy_rows(src, dst, max_ctas: int = 148, stream=None) -> None:
                               src.shape[1] * es, max_ctas, _stream(stream)), "hp_copy_rows")
 
 
+_SIDE: dict = {}
+
+
+def hold(stream, cycles: int) -> None:
+    """Delay the work queued next on `stream` by ~`cycles` GPU clocks (so a
+    burst of host launches is queued before any of it runs).  The spin
+    kernel runs on a primary-context side stream that `stream` then waits on:
+    torch's spin kernel launched straight into a green-context stream is the
+    one kernel ncu fails to prepare for profiling."""
+    import torch
+
+    dev = stream.device
+    side = _SIDE.get(dev)
+    if side is None:
+        side = _SIDE[dev] = torch.cuda.Stream(device=dev)
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(cycles)
+    stream.wait_stream(side)
+
+
 def set_trace(kind: int, buf) -> None:
     check(load().hp_set_trace(kind, _ptr(buf)), "hp_set_trace")
 

@@ -36,9 +36,35 @@ class PhaseStreams:
         self.torch_stream = torch_stream
 
 
+class _GridOnlyPartition:
+    """HP_NO_GREEN=1 (profiling only): plain streams with the split's SM
+    counts as grid sizes and no confinement.  ncu cannot prepare kernels
+    launched into green-context streams on this driver, so the launch list
+    is captured in this mode; every kernel keeps the grid it has in the
+    real co-run, and ncu serialises launches anyway."""
+
+    def __init__(self, decode_sms: int, device: int, n: int):
+        import torch
+
+        self.sms = {0: n - decode_sms, 1: decode_sms}
+        self._streams = {ph: torch.cuda.Stream(device=device) for ph in (0, 1)}
+
+    def raw_stream(self, phase: int) -> int:
+        return self._streams[phase].cuda_stream
+
+    def stream(self, phase: int):
+        return self._streams[phase]
+
+    def close(self) -> None:
+        pass
+
+
 class PartitionPool:
     def __init__(self, device: int = 0, granularity: int = 8):
+        import os
+
         self.device = device
+        self.grid_only = os.environ.get("HP_NO_GREEN") == "1"
         self.n = lib.device_sms(device)
         self.granularity = granularity
         self._parts: dict[int, lib.Partition] = {}
@@ -54,7 +80,7 @@ class PartitionPool:
         dm = self.realizable_decode_sms(dm)
         part = self._parts.get(dm)
         if part is None:
-            part = lib.Partition(dm, self.device)
+            part = _GridOnlyPartition(dm, self.device, self.n) if self.grid_only else lib.Partition(dm, self.device)
             self._parts[dm] = part
         return part
 

@@ -37,7 +37,7 @@ def measure(pool: PartitionPool, x, w, y, epi, resid, n: int, reps: int = 3):
     best = None
     with torch.cuda.stream(st.torch_stream):
         for _ in range(reps):
-            torch.cuda._sleep(100_000)
+            lib.hold(st.torch_stream, 100_000)
             lib.gemm_traced(x, w, y, times, epi, resid=resid, max_ctas=st.sms, stream=st.torch_stream)
             st.torch_stream.synchronize()
             t = times.cpu()
