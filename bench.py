@@ -320,10 +320,11 @@ def lat(r) -> dict:
                 r.decode_steps / r.steps}
 
 
-# decode share of the dual-roofline co-run split (>= the measured n_d = 43;
-# tools/hbm_split_sweep.py: decode attention reaches 0.73 of HBM beside the
-# prefill from dm = 88, at both T = 4096 and 16384)
-HBM_SPLIT_DM = 88
+# the dual-roofline co-run split: decode share >= the measured n_d = 42-43
+# beside the sweep's longest prefill chunk (tools/hbm_split_sweep.py: decode
+# attention at 0.73 of HBM from dm = 88 with the T = 16384 prefill GEMMs
+# above their partition's peak; 96 leaves margin for power-capped clocks)
+HBM_SPLIT = (16384, 96)
 
 
 def hbm_targets(cr, dm: int, hbm_gbs: float, tf_burst: float) -> dict:
@@ -471,11 +472,14 @@ def main(argv=None) -> int:
     T = args.prefill_tokens
     sweep_T = [int(x) for x in args.sweep.split(",") if x] if args.sweep else []
     per_T = []
+    hbm_split = None  # both north-star rooflines at one co-executed split with dm >= n_d
     for t in [x for x in sweep_T if x != T]:
         cr_t = CoRunner(model, t, DECODE_BATCH, DECODE_CTX, device=local, seed=1234 + rank, pool=pool,
                         weights=weights)
         per_T.append(study_T(cr_t, gpu, store, min(args.steps, 10), dist, coll,
                              sweep=not args.no_regret_sweep))
+        if t == HBM_SPLIT[0]:
+            hbm_split = hbm_targets(cr_t, HBM_SPLIT[1], hbm_gbs, tf_burst)
         del cr_t
         torch.cuda.empty_cache()
 
@@ -539,8 +543,8 @@ def main(argv=None) -> int:
     g_s = groups.group_s
     wave_idle = sum(g_s[k] * wave_stats(u, 1, n).idle_ratio for k, (u, n) in units.items()) / sum(g_s.values())
 
-    # ---- both north-star rooflines at one co-executed split with dm >= n_d
-    hbm_split = hbm_targets(cr, HBM_SPLIT_DM, hbm_gbs, tf_burst)
+    if hbm_split is None and T == HBM_SPLIT[0]:
+        hbm_split = hbm_targets(cr, HBM_SPLIT[1], hbm_gbs, tf_burst)
 
     # ---- SM idle MEASURED inside the co-run: per-CTA %globaltimer stamps of
     # the prefill layer's five kernel groups + the decode side's windows

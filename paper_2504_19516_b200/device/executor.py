@@ -101,6 +101,7 @@ class B200Executor:
         self.dx = torch.randn(max_decode_batch, h, generator=gen).to(**bf)
         self.dy = torch.empty_like(self.dx)
         self.dsc = DecodeScratch(model, max_decode_batch, 1024, self.dev, max_ctas=self.pool.n)
+        self.max_ctx = 1024 * PAGE  # contexts the decode scratch's block tables address
         self.calls = {"prefill": 0, "decode": 0}
         self._warm: set = set()
         # memo=True: reuse a measurement for states with the same partition,
@@ -318,10 +319,18 @@ class B200Executor:
         from ..engine import canonical_decode_es
 
         # the reference's canonical batch (<= 256 sequences of ~1k, longer
-        # contexts beyond 256k tokens) -- measured at its real size
+        # contexts beyond 256k tokens) measured at its real token count; a
+        # batch beyond the resident scratch keeps the token count with
+        # max_decode_batch longer sequences
         es = canonical_decode_es(int(tokens), sms)
-        if es.decode_batch > self.max_decode_batch:
-            raise InvalidArgumentError(f"canonical decode batch {es.decode_batch} exceeds max_decode_batch")
+        if es.decode_batch > self.max_decode_batch or max(es.decode_ctx_lens) > self.max_ctx:
+            # alpha is a ratio: beyond the resident scratch (max_decode_batch
+            # sequences of <= max_ctx) it is measured at the largest batch
+            bs = self.max_decode_batch
+            tok = min(int(tokens), bs * self.max_ctx)
+            ctx = max(1, tok // bs)
+            es = ExecutionState(decode_ctx_lens=(ctx,) * (bs - 1) + (max(1, tok - ctx * (bs - 1)),),
+                                decode_sms=sms)
         return self.decode_step_s(es) / srm_decode_step_s(es, self.model, self.gpu)
 
     def contention_bw(self, sms: int, co_prefill_len: int, nbytes: int = 1 << 30) -> float:
