@@ -160,3 +160,31 @@ def test_realtime_tiny_chunked_generates_oracle_tokens(tiny, chunk):
     assert flips <= 2
     assert sim.device_calls["hybrid_iterations"] > len(INPUTS)
     assert len(sim.pages.free) == srv.kv_pages - 1  # every page returned
+
+
+def test_realtime_llama3_8b_whole_model_serving():
+    """Config 4's engine at full size (32 random-init Llama-3-8B layers, real
+    tokens): a short Poisson-like burst through bullet; every decode step is
+    one CUDA graph of the whole model on its partition, and requests of
+    different lengths finish with their full output."""
+    from paper_2504_19516_b200.workload import MODEL_PRESETS
+
+    m = MODEL_PRESETS["llama3-8b"]
+    cfg = E.SimConfig(gpu=b200_gpu(), model=m, slo=S.SloSpec(norm_ttft_s_per_token=3e-3, tpot_s=0.15),
+                      sched=S.SchedulerConfig(sm_step=8), policy=E.PolicySpec("bullet"),
+                      kv_pool_bytes=m.weight_bytes() + (4 << 30), reconfig_s=0.0,
+                      metadata_overhead_s=0.0, predict_overhead_s=0.0)
+    trace = [Request(i, 0.01 * i, L, o) for i, (L, o) in enumerate(((3000, 24), (700, 40), (5000, 8), (1500, 30)))]
+    srv = ServingModel(m, 128256, DEV, kv_pages=kv_pages_for(cfg, 16), max_prefill_tokens=16384,
+                       max_pages_per_seq=-(-(5000 + 40 + 1) // PAGE), max_batch=64, seed=3)
+    sim = RealtimeSim(cfg, trace, srv, PartitionPool(0), store=b200_store())
+    rep = sim.run()
+    assert rep.aggregates["finished"] == len(trace), rep.aggregates
+    for r in trace:
+        toks = sim.generated[r.id]
+        assert len(toks) == r.output_len and all(0 <= t < 128256 for t in toks)
+    assert sim.device_calls["decode_graph_replays"] == sim.device_calls["decode_steps"] > 0
+    assert sim.device_calls["prefill_steps"] >= len(trace) * m.num_layers // cfg.sched.l_step // 2
+    assert rep.extended["ttft_p50_s"] > 0 and rep.extended["tpot_p50_ms"] > 0
+    del srv
+    torch.cuda.empty_cache()
