@@ -34,6 +34,7 @@
 #include "../../include/hp.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 namespace hp {
@@ -501,6 +502,388 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_fa2p: the CTA-pair form of k_fa2 (dense operands, D = 128).  A 2-CTA
+// cluster owns a (sequence, 512-query block, q head) unit: tile A = rows
+// [q0, q0+256), tile B = [q0+256, q0+512), CTA r holding rows 128r.. of
+// each.  The leader issues tcgen05.mma.cta_group::2 (M = 256):
+//     S_X  = Q_X . K_j^T   (N = 128 keys; each CTA stages 64 keys of K_j)
+//     O_X += P_X . V_j     (N = D = 128; each CTA stages 64 dims of V_j,
+//                           A = P from each CTA's own TMEM)
+// so the pair MMAs run at the full 4096 MAC/clk/SM (the 1-CTA SS M=128 N=128
+// QK reaches 58 %, profiles/r01_umma_rates.md) and every K/V byte crosses
+// one SM's shared-memory port instead of two.  The two tiles ping-pong as in
+// k_fa2: PV_A(j) QK_A(j+1) PV_B(j) QK_B(j+1).  Each CTA's softmax warps work
+// on their own 128 rows (TMEM lanes) and arrive on the leader's p_full /
+// o_empty (count 8); s_full / o_full / the ring's empty barriers are
+// committed to both CTAs.
+constexpr int FAP_THREADS = 384;
+constexpr int FAP_KST = 3;   // K ring stages (16 KB per CTA each)
+constexpr int FAP_VST = 3;   // V ring stages
+
+struct FapCfg {
+  static constexpr uint32_t QB = 2 * BOX;           // one CTA's 128 rows x 128 dims (32 KB)
+  static constexpr uint32_t KB = 2 * (BOX / 2);     // 64 keys x 128 dims (16 KB)
+  static constexpr uint32_t VB = BOX;               // 128 keys x 64 dims (16 KB)
+  static constexpr size_t SMEM = 1024 + 2 * QB + FAP_KST * KB + FAP_VST * VB + 512;
+};
+
+struct UnitP {
+  int head, seq, s0, len;
+  int q0;          // first query row of tile A (512-row block)
+  int nA, nB;      // kv tiles of tile A / tile B (nB = 0: tile B absent)
+};
+
+__device__ __forceinline__ bool unitp_of(const FaParams& p, int u, UnitP& x) {
+  x.head = u % p.Hq;
+  const int rest = u / p.Hq;
+  x.seq = rest % p.nseq;
+  const int qb = p.n_qt - 1 - rest / p.nseq;  // n_qt counts 512-row blocks here
+  x.s0 = p.cu_seqlens[x.seq];
+  x.len = p.cu_seqlens[x.seq + 1] - x.s0;
+  x.q0 = qb * 4 * FQ;
+  if (x.q0 >= x.len) return false;
+  const int kvt = (x.len + FK - 1) / FK;
+  x.nA = min((x.q0 + 2 * FQ + FK - 1) / FK, kvt);
+  x.nB = (x.q0 + 2 * FQ < x.len) ? min((x.q0 + 4 * FQ + FK - 1) / FK, kvt) : 0;
+  return true;
+}
+
+__device__ __forceinline__ void umma_bf16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// snake order over the grid's CTA pairs
+__device__ __forceinline__ int snake_unit_pair(int r) {
+  const int np = int(gridDim.x) >> 1, pi = int(blockIdx.x) >> 1;
+  return r * np + ((r & 1) ? np - 1 - pi : pi);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FAP_THREADS, 1)
+    k_fa2p(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK64,
+           const __grid_constant__ CUtensorMap tmV, const FaParams p) {
+  constexpr int D = 128;
+  using C = FapCfg;
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                 // [2 tiles][QB]
+  uint8_t* sK = sQ + 2 * C::QB;       // [KST][KB]
+  uint8_t* sV = sK + FAP_KST * C::KB; // [VST][VB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + FAP_VST * C::VB);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;                 // [KST]
+  uint64_t* k_empty = k_full + FAP_KST;
+  uint64_t* v_full = k_empty + FAP_KST;        // [VST]
+  uint64_t* v_empty = v_full + FAP_VST;
+  uint64_t* s_full = v_empty + FAP_VST;        // [2] per tile
+  uint64_t* p_full = s_full + 2;               // [2] (leader's, count 8)
+  uint64_t* o_full = p_full + 2;               // [2]
+  uint64_t* o_empty = o_full + 2;              // [2] (leader's, count 8)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK64);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < FAP_KST; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < FAP_VST; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 8);
+      mbar_init(&o_full[t], 1);
+      mbar_init(&o_empty[t], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  pdl_wait();
+  uint64_t t_start = 0;
+  if (p.cta_times != nullptr && threadIdx.x == 0) t_start = globaltimer();
+  const uint32_t tmem = *tmem_slot;
+  const int total = p.nseq * p.n_qt * p.Hq;
+  const int npairs = int(gridDim.x) >> 1;
+  if (warp < FA2_SOFTMAX_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+    if (warp == 0) {
+      // ---------------------------------------------------------- producer
+      // this CTA's halves, completing on the LEADER's barriers (pair TMA)
+      if (lane == 0) {
+        const uint32_t lq = mapa_shared(q_full, 0), lk = mapa_shared(k_full, 0), lv = mapa_shared(v_full, 0);
+        uint32_t un = 0, kt = 0, vt = 0;
+        for (int r = 0; r * npairs < total; ++r) {
+          const int u = snake_unit_pair(r);
+          if (u >= total) continue;
+          UnitP x;
+          if (!unitp_of(p, u, x)) continue;
+          const int kvh = x.head / p.G;
+          const int ntile = x.nB > 0 ? 2 : 1;
+          const int J = max(x.nA, x.nB);
+          mbar_wait(q_empty, (un & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(q_full, 2 * C::QB * ntile);
+          for (int t = 0; t < ntile; ++t)
+            for (int b = 0; b < 2; ++b)
+              tma_load_2d_pair(sQ + t * C::QB + b * BOX, &tmQ, lq, x.head * D + b * 64,
+                               x.s0 + x.q0 + t * 2 * FQ + int(rank) * FQ);
+          for (int j = 0; j < J; ++j, ++kt, ++vt) {
+            const int ks = kt % FAP_KST, vs = vt % FAP_VST;
+            mbar_wait(&k_empty[ks], ((kt / FAP_KST) & 1) ^ 1);
+            if (leader) mbar_arrive_expect_tx(&k_full[ks], 2 * C::KB);
+            for (int b = 0; b < 2; ++b)  // keys [64 rank, +64) of K_j, both 64-dim halves
+              tma_load_2d_pair(sK + ks * C::KB + b * (BOX / 2), &tmK64, lk + 8u * ks, kvh * D + b * 64,
+                               x.s0 + j * FK + int(rank) * 64);
+            mbar_wait(&v_empty[vs], ((vt / FAP_VST) & 1) ^ 1);
+            if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * C::VB);
+            // dims [64 rank, +64) of V_j, all 128 keys
+            tma_load_2d_pair(sV + vs * C::VB, &tmV, lv + 8u * vs, kvh * D + int(rank) * 64, x.s0 + j * FK);
+          }
+          ++un;
+        }
+      }
+    } else if (warp == 1 && leader) {
+      // ------------------------------------------------------ MMA issuer
+      if (lane == 0) {
+        constexpr uint32_t idesc_qk = umma_idesc_bf16(2 * FQ, FK);
+        constexpr uint32_t idesc_pv = umma_idesc_bf16(2 * FQ, D) | (1u << 16);  // B (V) MN-major
+        uint32_t un = 0, kt = 0, vt = 0;
+        uint32_t pc[2] = {0, 0};
+        uint32_t oc[2] = {0, 0};
+        auto qk = [&](int t, uint32_t kslot) {
+          const uint32_t qa = smem_u32(sQ + t * C::QB), kb = smem_u32(sK + kslot * C::KB);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            umma_bf16_pair(tmem + t * 128, umma_desc_sw128(qa + (kk >> 2) * BOX + (kk & 3) * 32),
+                           umma_desc_sw128(kb + (kk >> 2) * (BOX / 2) + (kk & 3) * 32), idesc_qk,
+                           kk > 0 ? 1u : 0u);
+          umma_commit_pair(&s_full[t]);
+        };
+        auto pv = [&](int t, uint32_t vslot, bool first) {
+          const uint32_t vb = smem_u32(sV + vslot * C::VB);
+#pragma unroll
+          for (int kk = 0; kk < FK / 16; ++kk)
+            umma_bf16_ts_pair(tmem + 256 + t * D, tmem + t * 128 + kk * 8, desc_mn_sw128(vb + kk * 2048, BOX),
+                              idesc_pv, (first && kk == 0) ? 0u : 1u);
+        };
+        for (int r = 0; r * npairs < total; ++r) {
+          const int u = snake_unit_pair(r);
+          if (u >= total) continue;
+          UnitP x;
+          if (!unitp_of(p, u, x)) continue;
+          const int n[2] = {x.nA, x.nB};
+          const int J = max(x.nA, x.nB);
+          mbar_wait(q_full, un & 1);
+          {
+            const int ks = kt % FAP_KST;
+            mbar_wait(&k_full[ks], (kt / FAP_KST) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+              if (n[t] > 0) qk(t, ks);
+          }
+          for (int j = 0; j < J; ++j) {
+            const uint32_t vs = (vt + j) % FAP_VST;
+            const uint32_t ks_cur = (kt + j) % FAP_KST, ks_nxt = (kt + j + 1) % FAP_KST;
+            bool k_next_ready = false;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              if (j >= n[t]) continue;
+              mbar_wait_cluster(&p_full[t], pc[t] & 1);
+              ++pc[t];
+              if (j == 0) mbar_wait_cluster(&o_empty[t], (oc[t] & 1) ^ 1);
+              mbar_wait(&v_full[vs], ((vt + j) / FAP_VST) & 1);
+              tc_fence_after();
+              pv(t, vs, j == 0);
+              if (j + 1 < n[t]) {
+                if (!k_next_ready) {
+                  mbar_wait(&k_full[ks_nxt], ((kt + j + 1) / FAP_KST) & 1);
+                  tc_fence_after();
+                  k_next_ready = true;
+                }
+                qk(t, ks_nxt);
+              } else {
+                umma_commit_pair(&o_full[t]);
+                ++oc[t];
+              }
+            }
+            umma_commit_pair(&v_empty[vs]);
+            umma_commit_pair(&k_empty[ks_cur]);
+            if (j == J - 1) umma_commit_pair(q_empty);
+          }
+          kt += J;
+          vt += J;
+          ++un;
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    // ------------------------------------------------------------- softmax
+    const int t = (warp - FA2_SOFTMAX_WARP0) >> 2;  // tile 0 (A) or 1 (B)
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_base = uint32_t(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_base + t * 128;
+    const uint32_t tO = tmem + lane_base + 256 + t * D;
+    const uint32_t lp_full = mapa_shared(&p_full[t], 0), lo_empty = mapa_shared(&o_empty[t], 0);
+    uint32_t sc = 0, un = 0;
+    for (int r = 0; r * npairs < total; ++r) {
+      const int u = snake_unit_pair(r);
+      if (u >= total) continue;
+      UnitP x;
+      if (!unitp_of(p, u, x)) continue;
+      const int nt = t == 0 ? x.nA : x.nB;
+      if (nt == 0) continue;
+      const int q0 = x.q0 + t * 2 * FQ + int(rank) * FQ;  // this CTA's first row of tile t
+      const int qi = q0 + row;
+      float m_run = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j, ++sc) {
+        mbar_wait(&s_full[t], sc & 1);
+        tc_fence_after();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+        tmem_ld_wait();
+        const int kbase = j * FK;
+        const bool need_mask = (kbase + FK - 1 > q0) || (kbase + FK > x.len);
+        if (need_mask) {
+          const int lim = min(qi + 1, x.len) - kbase;  // keys [0, lim) visible
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c >= lim) s[c] = -INFINITY;
+        }
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+        for (int c = 8; c < 128; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m8[k] = fmaxf(m8[k], m8[k + 4]);
+        const float mx = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])) * p.scale_log2;
+        const float m_new = fmaxf(m_run, mx);
+        const bool grow = m_new > m_run + RESCALE_THRESHOLD;
+        if (__any_sync(0xffffffffu, grow) && j > 0) {
+          const float alpha = grow ? exp2f(m_run - m_new) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            float o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] *= alpha;
+            tmem_st32(tO + c * 32, o);
+          }
+          if (grow) l *= alpha;
+        }
+        if (grow) m_run = m_new;
+        const float mb = (m_run == -INFINITY) ? 0.f : m_run;
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nm2 = make_float2(-mb, -mb);
+        float2 l4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float w[32];
+          uint32_t* wu = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            float2 v2 = __ffma2_rn(make_float2(s[h * 64 + 2 * k], s[h * 64 + 2 * k + 1]), sc2, nm2);
+            v2.x = ex2(v2.x);
+            v2.y = ex2(v2.y);
+            l4[k & 3] = __fadd2_rn(l4[k & 3], v2);
+            wu[k] = pack_bf16(v2.x, v2.y);
+          }
+          tmem_st32(tS + h * 32, w);
+        }
+        const float2 ls = __fadd2_rn(__fadd2_rn(l4[0], l4[1]), __fadd2_rn(l4[2], l4[3]));
+        l += ls.x + ls.y;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(lp_full);
+      }
+      mbar_wait(&o_full[t], un & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const bool ok = qi < x.len;
+      __nv_bfloat16* orow = p.out + size_t(x.s0 + qi) * p.ldo + size_t(x.head) * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_ld_wait();
+        if (ok) {
+          uint4 w[4];
+          uint32_t* ww = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) ww[k] = pack_bf16(o[2 * k] * inv, o[2 * k + 1] * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dst[k] = w[k];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(lo_empty);
+      ++un;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+  if (p.cta_times != nullptr && threadIdx.x == 0) {
+    p.cta_times[blockIdx.x * 3 + 0] = smid();
+    p.cta_times[blockIdx.x * 3 + 1] = t_start;
+    p.cta_times[blockIdx.x * 3 + 2] = globaltimer();
+  }
+}
+
+// Pair form for long prompts (max_seqlen >= 8192) on >= 2 SMs: measured
+// (tools/fa_ab.py) 1272 vs 1231 TFLOP/s at T = 16384 on 148 SMs, but 923 vs
+// 968 at T = 4096 on 140 (512-row units: fewer of them, more causal waste on
+// the diagonal).  Either way the pair lifts the MMA rate and halves the K/V
+// shared-memory traffic yet gains little: the softmax chain, not the tensor
+// core, bounds k_fa2.  HP_FA_PAIR=0|1 forces it off/on.
+static bool fa_pair_enabled(int max_ctas, int max_seqlen) {
+  static const int forced = [] {
+    const char* e = std::getenv("HP_FA_PAIR");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  if (max_ctas < 2 || forced == 0) return false;
+  return forced == 1 || max_seqlen >= 8192;
+}
+
+static int launch_fa2p(const CUtensorMap& tq, const CUtensorMap& tk64, const CUtensorMap& tv, FaParams p,
+                       int max_seqlen, int max_ctas, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_fa2p, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FapCfg::SMEM)));
+    attr = true;
+  }
+  p.n_qt = (max_seqlen + 4 * FQ - 1) / (4 * FQ);
+  const int pairs = std::min(p.nseq * p.n_qt * p.Hq, max_ctas / 2);
+  HP_LAUNCH_PDL("k_fa2p", k_fa2p, dim3(2 * pairs), dim3(FAP_THREADS), FapCfg::SMEM, st, tq, tk64, tv, p);
+  return HP_OK;
+}
+
 template <int D, bool PAGED>
 static int launch_fa2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, FaParams p,
                       int max_seqlen, int max_ctas, cudaStream_t st) {
@@ -551,6 +934,12 @@ extern "C" int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, c
   p.trace = static_cast<long long*>(trace_buf(TRACE_FA));
   p.cta_times = take_cta_trace();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (d == 128 && p.trace == nullptr && fa_pair_enabled(max_ctas, max_seqlen)) {
+    CUtensorMap tk64;  // the pair stages 64 keys of each K tile per CTA
+    rc = cached_tmap_bf16(&tk64, k, rows, uint64_t(Hkv) * d, ldk, 64, 64, true);
+    if (rc) return rc;
+    return launch_fa2p(tq, tk64, tv, p, max_seqlen, max_ctas, st);
+  }
   return d == 128 ? launch_fa2<128, false>(tq, tk, tv, p, max_seqlen, max_ctas, st)
                   : launch_fa2<64, false>(tq, tk, tv, p, max_seqlen, max_ctas, st);
 }

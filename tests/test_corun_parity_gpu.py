@@ -115,3 +115,28 @@ def test_prefill_attn_T16384(sms):
     assert err.max().item() < 2e-2, (err.max().item(), err.argmax().item())
     # every query row (incl. the last, which sees all 16384 keys) is covered
     assert torch.isfinite(o.float()).all()
+
+
+@pytest.mark.parametrize("lens", [[9000, 300, 5000], [8192, 8193]])
+def test_prefill_attn_long_varlen_pair_kernel(lens):
+    """max_seqlen >= 8192 selects the CTA-pair kernel (k_fa2p, 512-row units
+    split over a 2-CTA cluster): ragged sequences, tails inside a unit, a
+    sequence shorter than one unit."""
+    Hq, Hkv, d = 32, 8, 128
+    T = sum(lens)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(T)
+    qkv = torch.randn(T, (Hq + 2 * Hkv) * d, generator=g, device=DEV).to(torch.bfloat16)
+    q, k, v = qkv[:, : Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
+    o = torch.zeros(T, Hq * d, device=DEV, dtype=torch.bfloat16)
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), device=DEV, dtype=torch.int32)
+    scale = 1.0 / math.sqrt(d)
+    lib.prefill_attn(q, k, v, o, cu, len(lens), max(lens), Hq, Hkv, d, scale, max_ctas=148)
+    torch.cuda.synchronize()
+    s0 = 0
+    for L in lens:
+        sl = slice(s0, s0 + L)
+        ref = _causal_ref_chunked(q[sl].view(L, Hq, d), k[sl].view(L, Hkv, d), v[sl].view(L, Hkv, d), scale)
+        err = (o[sl].float().view(L, Hq, d) - ref).abs().max().item()
+        assert err < 2e-2, (L, err)
+        s0 += L

@@ -1,18 +1,43 @@
-"""Prefill attention TFLOP/s (k_fa2) at the bench shapes; HP_LIB=<path>
-loads an alternative libb200hot.so for A/B comparisons.
-    python tools/fa_ab.py"""
+"""Prefill attention TFLOP/s (causal, one sequence, Llama-3-8B heads) at
+several T and grid sizes; run twice with HP_FA_PAIR=0/1 for A/B.
+
+    HP_FA_PAIR=1 python tools/fa_ab.py
+"""
+import json
+import math
 import os
 import sys
+
+import torch
 
 sys.path.insert(0, ".")
 from paper_2504_19516_b200.device import lib  # noqa: E402
 
-if os.environ.get("HP_LIB"):
-    lib.load(os.environ["HP_LIB"])
-from paper_2504_19516_b200.device import kbench  # noqa: E402
+dev = torch.device("cuda", 0)
+Hq, Hkv, d = 32, 8, 128
+out = {}
+for T, sms in ((1024, 124), (2048, 132), (4096, 140), (4096, 148), (16384, 140), (16384, 148)):
+    qkv = torch.randn(T, (Hq + 2 * Hkv) * d, device=dev).to(torch.bfloat16)
+    q, k, v = qkv[:, :Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
+    o = torch.empty(T, Hq * d, device=dev, dtype=torch.bfloat16)
+    cu = torch.tensor([0, T], device=dev, dtype=torch.int32)
 
-res = []
-for T, sms in ((4096, 148), (4096, 140), (16384, 148), (1024, 148)):
-    kbench.bench_prefill_attn(T, 32, 8, sms, res)
-for r in res:
-    print(r, flush=True)
+    def go():
+        lib.prefill_attn(q, k, v, o, cu, 1, T, Hq, Hkv, d, 1 / math.sqrt(d), max_ctas=sms)
+
+    go()
+    torch.cuda.synchronize()
+    reps = max(3, int(2e10 / (2 * T * T * Hq * d)))
+    ts = []
+    for _ in range(3):
+        torch.cuda._sleep(100_000)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            go()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3 / reps)
+    t = sorted(ts)[1]
+    out[f"T{T}_sms{sms}"] = round(2.0 * T * T * Hq * d / t / 1e12, 1)
+print(json.dumps({"HP_FA_PAIR": os.environ.get("HP_FA_PAIR", "1"), "tflops": out}))
