@@ -774,6 +774,10 @@ class RealtimeChunked(E._ChunkedSim):
     def _iteration_meta(self, chunks, decode) -> dict:
         srv, dev = self.server, self.server.dev
         MP = srv.max_pages
+        n_emit = len(decode) + sum(1 for rid, take, p in chunks if p + take >= self.records[rid].request.input_len)
+        if n_emit > srv.max_batch or len(decode) > srv.dsc.max_batch:
+            raise InvalidArgumentError(f"hybrid iteration emits {n_emit} rows ({len(decode)} decoding); "
+                                       f"the serving model holds {srv.max_batch}")
         toks, pos, slots, emit, emit_ids = [], [], [], [], []
         cu, prior, cbt = [0], [], []
         r = 0
