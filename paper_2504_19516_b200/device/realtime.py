@@ -225,8 +225,10 @@ class ServingModel:
         from .partition import DECODE
 
         n = 0
-        for dm in (shares or list(range(pool.granularity, pool.n, pool.granularity)) + [pool.n]):
-            ps = pool.phase(DECODE, dm)
+        streams = [pool.phase(DECODE, dm) for dm in
+                   (shares or list(range(pool.granularity, pool.n, pool.granularity)) + [pool.n])]
+        streams.append(pool.full(0))  # the time-sliced baseline's single stream
+        for ps in streams:
             for b in buckets:
                 if b <= self.max_batch:
                     self.decode_graph(b, ps)
@@ -303,12 +305,20 @@ class RealtimeSim(E._ConcurrentSim):
     (module docstring).  Policies: bullet, nopartition, static."""
 
     def __init__(self, cfg: E.SimConfig, trace, server: ServingModel, pool: PartitionPool, store=None,
-                 trace_decisions: bool = False, clock_scale: float = 1.0, prompts=None, seed: int = 0):
+                 trace_decisions: bool = False, clock_scale: float = 1.0, prompts=None, seed: int = 0,
+                 serialize: bool = False):
+        """serialize=True (with policy nopartition): both phases on ONE
+        full-device stream -- the time-sliced serving baseline (prefill
+        layer steps and decode steps alternate on the device in launch
+        order, never concurrently)."""
         if cfg.policy.name == "chunked":
             raise InvalidArgumentError("RealtimeSim runs the concurrent policies; chunked has its own loop")
         if store is None:
             raise InvalidArgumentError("RealtimeSim needs a measured CalibrationStore (no synthetic oracle)")
         super().__init__(cfg, trace, oracle=_NoOracle(), store=store)
+        if serialize and cfg.policy.name != "nopartition":
+            raise InvalidArgumentError("serialize=True is the time-sliced form of policy nopartition")
+        self.serialize = serialize
         self.server = server
         self.pool = pool
         self.pages = PageAllocator(server.kv_pages)
@@ -460,7 +470,8 @@ class RealtimeSim(E._ConcurrentSim):
         if self.layers_done == 0 or self.batch_meta is None or self.batch_meta["ids"] != list(self.inflight):
             self.batch_meta = self._build_batch()
         dm = self._decode_sms_now() if self.decode_running else 0
-        ps, _ = self.pool.split(pm, dm if 0 < dm and pm + dm <= self.n else 0)
+        ps = (self.pool.full(0) if self.serialize else
+              self.pool.split(pm, dm if 0 < dm and pm + dm <= self.n else 0)[0])
         a, b = _ev(), _ev()
         a.record(ps.torch_stream)
         self.server.prefill_layers(self.layers_done, self.layers_done + layers, self.batch_meta, ps.sms,
@@ -536,7 +547,8 @@ class RealtimeSim(E._ConcurrentSim):
         srv = self.server
         b = srv.stage_decode([self.last_tok[r] for r in batch], [self.records[r].ctx_len for r in batch],
                              [self.seq_pages[r] for r in batch])
-        _, ds = self.pool.split(pm if 0 < pm and pm + dm <= self.n else 0, dm)
+        ds = (self.pool.full(0) if self.serialize else
+              self.pool.split(pm if 0 < pm and pm + dm <= self.n else 0, dm)[1])
         a, e = _ev(), _ev()
         a.record(ds.torch_stream)
         srv.launch_decode(b, ds)

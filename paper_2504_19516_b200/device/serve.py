@@ -79,11 +79,13 @@ def run_replay(policy: str, trace, ex, gpu, slo, chunk: int):
 def run_realtime(policy: str, trace, server, pool, gpu, slo, chunk: int, decisions_out=None, max_decisions=400):
     from .realtime import RealtimeChunked, RealtimeSim, delta_encode
 
-    cfg = sim_config(policy, gpu, slo, chunk)
+    serialize = policy == "timesliced"  # nopartition with both phases on one stream
+    cfg = sim_config("nopartition" if serialize else policy, gpu, slo, chunk)
     if policy == "chunked":
         sim = RealtimeChunked(cfg, trace, server, pool)
     else:
-        sim = RealtimeSim(cfg, trace, server, pool, store=calib_store(), trace_decisions=decisions_out is not None)
+        sim = RealtimeSim(cfg, trace, server, pool, store=calib_store(), trace_decisions=decisions_out is not None,
+                          serialize=serialize)
     rep = sim.run()
     a = dict(rep.aggregates)
     a.update(rep.extended)
@@ -115,7 +117,8 @@ def main(argv=None) -> int:
     ap.add_argument("--rate", type=float, default=4.0, help="requests/s (whole job)")
     ap.add_argument("--duration", type=float, default=10.0)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--policies", default="bullet,chunked,nopartition")
+    ap.add_argument("--policies", default="bullet,chunked,nopartition,timesliced",
+                    help="timesliced = nopartition with both phases serialised on one stream (real time only)")
     ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--out", default=None)
     ap.add_argument("--replay", action="store_true", help="round-1 mode: simulated clock, measured step times")
