@@ -90,6 +90,36 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): round x to the
+// nearest integer n with the 1.5 * 2^23 magic add, 2^(x - n) by a degree-3
+// minimax polynomial on [-0.5, 0.5] (relative error 7.7e-5, below bf16's
+// 3.9e-3), then n added to the exponent field with one IMAD.  x is clamped
+// to -126 (masked scores: -inf -> 2^-126 ~ 1e-38 instead of 0).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(f, make_float2(0.055088683807510905f, 0.055088683807510905f),
+                        make_float2(0.24260405145947916f, 0.24260405145947916f));
+  q = __ffma2_rn(q, f, make_float2(0.6932762416819607f, 0.6932762416819607f));
+  q = __ffma2_rn(q, f, make_float2(0.9999289403695112f, 0.9999289403695112f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(q.x)),
+                     __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(q.y)));
+}
+
+#ifndef HP_FA_POLY
+#define HP_FA_POLY 0  // score pairs per 32-pair half computed on the FMA pipe
+#endif
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -407,14 +437,16 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
             if (c >= lim) s[c] = -INFINITY;
         }
         // raw-score row max with 8 independent chains (ILP), then scale once
+        // 3-input FMNMX3: 8 chains take two scores per instruction
         float m8[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) m8[k] = s[k];
 #pragma unroll
-        for (int c = 8; c < 128; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+        for (int c = 8; c < 128; c += 16)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m8[k] = fmaxf(m8[k], m8[k + 4]);
-        const float mx = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])) * p.scale_log2;
+          for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], s[c + k], s[c + 8 + k]);
+        const float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) *
+                         p.scale_log2;
         const float m_new = fmaxf(m_run, mx);
         const bool grow = m_new > m_run + RESCALE_THRESHOLD;
         // O_t holds PV(0..j-1), complete (issued before QK(j)); rescale lazily
@@ -447,8 +479,12 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             float2 x = __ffma2_rn(make_float2(s[h * 64 + 2 * k], s[h * 64 + 2 * k + 1]), sc2, nm2);
-            x.x = ex2(x.x);
-            x.y = ex2(x.y);
+            if (k < HP_FA_POLY) {
+              x = ex2_poly2(x);
+            } else {
+              x.x = ex2(x.x);
+              x.y = ex2(x.y);
+            }
             l4[k & 3] = __fadd2_rn(l4[k & 3], x);
             wu[k] = pack_bf16(x.x, x.y);
           }
@@ -767,14 +803,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FAP_THREADS, 1)
           for (int c = 0; c < 128; ++c)
             if (c >= lim) s[c] = -INFINITY;
         }
+        // 3-input FMNMX3: 8 chains take two scores per instruction
         float m8[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) m8[k] = s[k];
 #pragma unroll
-        for (int c = 8; c < 128; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+        for (int c = 8; c < 128; c += 16)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m8[k] = fmaxf(m8[k], m8[k + 4]);
-        const float mx = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])) * p.scale_log2;
+          for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], s[c + k], s[c + 8 + k]);
+        const float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) *
+                         p.scale_log2;
         const float m_new = fmaxf(m_run, mx);
         const bool grow = m_new > m_run + RESCALE_THRESHOLD;
         if (__any_sync(0xffffffffu, grow) && j > 0) {
@@ -803,8 +841,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FAP_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             float2 v2 = __ffma2_rn(make_float2(s[h * 64 + 2 * k], s[h * 64 + 2 * k + 1]), sc2, nm2);
-            v2.x = ex2(v2.x);
-            v2.y = ex2(v2.y);
+            if (k < HP_FA_POLY) {
+              v2 = ex2_poly2(v2);
+            } else {
+              v2.x = ex2(v2.x);
+              v2.y = ex2(v2.y);
+            }
             l4[k & 3] = __fadd2_rn(l4[k & 3], v2);
             wu[k] = pack_bf16(v2.x, v2.y);
           }
