@@ -53,7 +53,8 @@ def shard(trace, rank: int, world: int):
     return [Request(i, r.arrival_s, r.input_len, r.output_len) for i, r in enumerate(mine)]
 
 
-def sim_config(policy: str, gpu, slo: S.SloSpec, chunk: int = 1024, realtime: bool = True) -> E.SimConfig:
+def sim_config(policy: str, gpu, slo: S.SloSpec, chunk: int = 1024, realtime: bool = True,
+               static_pm: int = 116) -> E.SimConfig:
     model = MODEL_PRESETS["llama3-8b"]
     g = CALIB / "gpu.json"
     reconfig = json.loads(g.read_text()).get("reconfig_s") if g.exists() else None
@@ -61,7 +62,7 @@ def sim_config(policy: str, gpu, slo: S.SloSpec, chunk: int = 1024, realtime: bo
     if realtime:  # the control plane's cost is real, not modelled
         kw.update(metadata_overhead_s=0.0, predict_overhead_s=0.0)
     return E.SimConfig(gpu=gpu, model=model, slo=slo, sched=S.SchedulerConfig(sm_step=8),
-                       policy=E.PolicySpec(policy, chunk_size=chunk), seed=0, **kw)
+                       policy=E.PolicySpec(policy, chunk_size=chunk, static_pm=static_pm), seed=0, **kw)
 
 
 def calib_store():
@@ -76,11 +77,12 @@ def run_replay(policy: str, trace, ex, gpu, slo, chunk: int):
     return a
 
 
-def run_realtime(policy: str, trace, server, pool, gpu, slo, chunk: int, decisions_out=None, max_decisions=400):
+def run_realtime(policy: str, trace, server, pool, gpu, slo, chunk: int, decisions_out=None, max_decisions=400,
+                 static_pm: int = 116):
     from .realtime import RealtimeChunked, RealtimeSim, delta_encode
 
     serialize = policy == "timesliced"  # nopartition with both phases on one stream
-    cfg = sim_config("nopartition" if serialize else policy, gpu, slo, chunk)
+    cfg = sim_config("nopartition" if serialize else policy, gpu, slo, chunk, static_pm=static_pm)
     if policy == "chunked":
         sim = RealtimeChunked(cfg, trace, server, pool)
     else:
@@ -125,6 +127,8 @@ def main(argv=None) -> int:
     ap.add_argument("--full-model", action="store_true", help="(--replay) all 32 layers resident")
     ap.add_argument("--slo", default="paper", choices=["paper", "r01"],
                     help="paper: ShareGPT SLOs of PAPER.md Table (3.0 ms/token, 150 ms); r01: 1.5 ms, 100 ms")
+    ap.add_argument("--static-pm", type=int, default=116,
+                    help="policy static: fixed prefill share (decode gets the rest while prefill runs)")
     ap.add_argument("--slo-ms", default=None, help="norm_ttft_ms_per_token,tpot_ms (overrides --slo)")
     ap.add_argument("--decisions-out", default=None, help="(realtime bullet) log decisions for the replay test")
     a = ap.parse_args(argv)
@@ -166,7 +170,9 @@ def main(argv=None) -> int:
         pool.warm()
         cfg0 = sim_config("bullet", gpu, slo)
         server = ServingModel(model, VOCAB, torch.device("cuda", local), kv_pages=kv_pages_for(cfg0),
-                              max_prefill_tokens=65536, max_pages_per_seq=-(-(8192 + out_dist.hi + 1) // PAGE),
+                              # the reference's _form_batch has no token cap (static /
+                              # nopartition batch a long queue at once): 192k packed tokens
+                              max_prefill_tokens=196608, max_pages_per_seq=-(-(8192 + out_dist.hi + 1) // PAGE),
                               seed=a.seed + rank)
         graphs = server.warm(pool)
     lines = []
@@ -175,7 +181,7 @@ def main(argv=None) -> int:
             agg = run_replay(pol, mine, dev_obj, gpu, slo, a.chunk)
         else:
             agg = run_realtime(pol, mine, server, pool, gpu, slo, a.chunk,
-                               a.decisions_out if rank == 0 else None)
+                               a.decisions_out if rank == 0 else None, static_pm=a.static_pm)
         per = [agg]
         if dist is not None:
             per = [None] * world
