@@ -489,9 +489,11 @@ def main(argv=None) -> int:
     per_T.append(head)
     per_T.sort(key=lambda e: e["T"])
     pm, dm = head["split"]["pm"], head["split"]["dm"]
-    if args.split:
-        pm, dm = (int(v) for v in args.split.split(","))
     ratio = head["decode_steps_per_prefill_layer"]
+    if args.split:  # profiling override: re-derive the decode cadence at that split
+        pm, dm = (int(v) for v in args.split.split(","))
+        r0 = cr.corun(pm, dm, 3, 1.0)
+        ratio = max(1.0, r0.p50(r0.prefill_layer_s) / r0.p50(r0.decode_layer_s))
     for _ in range(args.warmup):
         cr.corun(pm, dm, 2, ratio)
     # per-group breakdown from a separate, fully instrumented co-run of the
