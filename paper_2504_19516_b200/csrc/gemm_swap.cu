@@ -660,6 +660,31 @@ static int launch_swap(const CUtensorMap& tx, const SwapParams& p, int grid,
 
 static inline int swap_bn(int T) { return T <= 32 ? 32 : (T <= 64 ? 64 : (T <= 128 ? 128 : 256)); }
 
+// Stream-K grid on a large partition: among [ceil(3 units / 4), units] CTAs,
+// prefer a count whose per-CTA k range aligns with tile boundaries -- whole
+// tiles per CTA (no fixup at all), or an even split of every tile (one
+// segment per CTA) -- over a misaligned range whose CTAs straddle tiles and
+// serialise on split-tile fixups (tools/swap_ctas.py, full GPU, T = 32:
+// o_proj 14.4 -> 12.4 us at 128 CTAs, mlp_up_gate 38.9 -> 35.3 at 112,
+// mlp_down 27.4 -> 23.6 at 128).  Below 64 units every SM's own streaming
+// bandwidth counts (HBM is not the limit) and the walk uses all of them.
+static int swap_grid(int total, int num_kb, int units) {
+  const int g0 = std::max(1, std::min(units, total));
+  if (units < 64) return g0;
+  int best = g0;
+  double best_score = 1e30;
+  for (int c = g0; c >= (3 * units + 3) / 4; --c) {
+    const int ipc = (total + c - 1) / c;
+    const double pen = ipc % num_kb == 0 ? 0.0 : (num_kb % ipc == 0 ? 0.05 : 0.35);
+    const double score = ipc * (1.0 + pen);
+    if (score < best_score - 1e-9) {
+      best_score = score;
+      best = c;
+    }
+  }
+  return best;
+}
+
 }  // namespace hp
 
 using namespace hp;
@@ -955,7 +980,7 @@ static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* 
   p.m_walk = pair ? p.m_tiles / 2 : p.m_tiles;
   p.total_iters = p.m_walk * p.n_tiles * p.num_kb;
   const int units = pair ? max_ctas / 2 : max_ctas;
-  const int grid = std::min(units, p.total_iters);
+  const int grid = swap_grid(p.total_iters, p.num_kb, units);
   p.ipc = (p.total_iters + grid - 1) / grid;
   p.max_contrib = (p.num_kb + p.ipc - 1) / p.ipc + 1;
   p.out = static_cast<__nv_bfloat16*>(Y);
