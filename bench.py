@@ -538,7 +538,7 @@ def main(argv=None) -> int:
     # ---- SM idle: partition-level (SM-time with no work in either partition)
     # and the wave model's intra-kernel idle of the prefill layer on pm SMs
     wl = cr.layer.W
-    plans = {gname: hplib.gemm_plan(T, w.shape[0], pm) for gname, w in
+    plans = {gname: hplib.gemm_plan(T, w.shape[0], w.shape[1], pm) for gname, w in
              (("qkv", wl.w_qkv), ("o_proj", wl.w_o), ("mlp_up_gate", wl.w_ug), ("mlp_down", wl.w_down))}
     units = {gname: (pl[1], pm // pl[2]) for gname, pl in plans.items()}  # (tiles, concurrent tile slots)
     units["attn"] = (-(-T // 256) * model.num_heads, pm)                   # k_fa2: 256-query units, one per CTA

@@ -117,8 +117,11 @@ int hp_gemm_tiles(int T, int N);
  * or 256: fewer wave-quantised column-rounds, wave_stats perf_model.py:
  * 157-169), tile count, and CTAs per tile (2 = CTA-pair 256 x 256 tiles on
  * tcgen05.mma.cta_group::2; the persistent grid then has max_ctas / 2 units
- * of work-in-flight, i.e. waves = wave_stats(tiles, 1, max_ctas / 2)). */
-int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles, int* ctas_per_tile);
+ * of work-in-flight, i.e. waves = wave_stats(tiles, 1, max_ctas / 2)).
+ * tail_tiles: tiles the stream-K tail (hp_set_gemm_tail) splits over every
+ * pair instead of running them as the last rounds (0: plain rounds). */
+int hp_gemm_plan(int T, int N, int K, int max_ctas, int* bn, int* tiles, int* ctas_per_tile,
+                 int* tail_tiles);
 
 /* Swap-AB stream-K tcgen05 GEMM for decode (T <= 256 tokens): same math as
  * hp_gemm; W streams through UMMA-M and the (tile, k-block) space is split
@@ -216,6 +219,16 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
  * disarms it.  NULL disables. */
 int hp_set_trace(int kind, void* buf);
 
+/* Stream-K tail of the prefill CTA-pair GEMM (hp_gemm, hp_gemm_qkv_rope):
+ * mode 1 splits the last full round plus the partial one (or every tile,
+ * when there are fewer tiles than pairs) into equal k-block ranges, one per
+ * pair, with a deterministic fp32 fix-up in the finishing pair; 0 runs plain
+ * persistent rounds (the grid wave_stats describes, perf_model.py:157-169);
+ * -1 restores the default (on unless HP_GEMM_TAIL=0).  Per process.  The
+ * fix-up workspace is allocated per stream on first use (~21 MB), which
+ * must not happen inside a stream capture (the tail is then skipped). */
+int hp_set_gemm_tail(int mode);
+
 /* Prefix-aware (chunked) prefill attention over the paged cache
  * (workload.py:176-183 with prior_lens > 0; the attention of a hybrid batch,
  * hybrid_kernels workload.py:213-257, as issued by _ChunkedSim engine.py:
@@ -274,6 +287,18 @@ int hp_umma_rate(int n, int bn, int chains, int ctas, long long* out, void* stre
 /* Pair MMA rate: `pairs` 2-CTA clusters issue n tcgen05.mma.cta_group::2
  * (M=256, N=bn, K=16); out[cta] = issue cycles, out[grid + cta] = done cycles. */
 int hp_umma2_rate(int n, int bn, int pairs, long long* out, void* stream);
+
+/* Register-direct streaming: `threads` per CTA, `unroll` (2/4/8/16) 128-bit
+ * loads per lane in flight twice over, noalloc = L1::no_allocate. */
+int hp_membw_ldg(const void* src, size_t bytes, int ctas, int threads, int unroll, int noalloc,
+                 float* out, void* stream);
+/* Both streaming paths at once: one warp's bulk-copy ring takes bulk_frac/256
+ * of each CTA's range, `ldg_warps` warps stream the rest with 128-bit loads. */
+int hp_membw_mix(const void* src, size_t bytes, int ctas, int ldg_warps, int bulk_frac, float* out,
+                 void* stream);
+/* mma.sync.m16n8k16 (bf16) rate: `chains` independent accumulators per warp,
+ * n rounds; out[cta] = cycles. */
+int hp_hmma_rate(int n, int chains, int ctas, int threads, long long* out, void* stream);
 
 /* Per-CTA probe: out[i] = {smid, start_ns, end_ns} for `ctas` CTAs spinning
  * `spin_ns` each -- partition confinement (%smid) and measured idle. */

@@ -49,6 +49,12 @@ struct GemmParams {
   __nv_bfloat16* kc;
   __nv_bfloat16* vc;
   int page, Hq, Hkv, hd;
+  // Stream-K tail (CTA-pair kernel): tiles [0, sk_dp) run in persistent
+  // rounds; the last sk_tail tiles' sk_tail * num_kb k-blocks are split into
+  // one contiguous range per pair.  sk_tail = 0: plain rounds.
+  int sk_dp, sk_tail;
+  float* sk_ws;  // [pairs][2 ranks][8 col chunks][128 rows][32] fp32 partial tiles
+  int* sk_cnt;   // [tail tile][rank] arrivals (the finishing CTA resets it)
 };
 
 constexpr int BM = 128;
@@ -107,10 +113,122 @@ __device__ __forceinline__ void add_row32(float* v, const __nv_bfloat16* src) {
   }
 }
 
+// ---- stream-K tail -------------------------------------------------------
+// Pair i owns k-block range [start(i), start(i+1)) of the tail's flattened
+// (tile, k-block) space.  A range is cut at tile boundaries into <= 3
+// segments; the one ending mid-tile (at most one per pair) is a PARTIAL: its
+// fp32 accumulator goes to workspace slot i and the tile's arrival counter is
+// raised.  The pair whose range holds a tile's last k-block FINISHES it: it
+// waits for the tile's other contributors (pairs j0..f-1), adds their slots in
+// pair order to its own accumulator (a fixed order: deterministic sums) and
+// runs the normal fused epilogue.  Pairs process their partial first, so no
+// finisher waits on a pair that is itself waiting.
+struct Seg {
+  int tile, kb0, kb1, kind;  // kind: 0 whole tile, 1 finishing, 2 partial
+};
+
+__device__ __forceinline__ int sk_start(const GemmParams& p, int i, int P) {
+  return int((long long)i * (long long)(p.sk_tail * p.num_kb) / P);
+}
+
+// Work item `it` of pair `pair`: its round-robin data-parallel tiles, then its
+// tail segments (partial first).  Returns false past the last item.
+__device__ __forceinline__ bool work_item(const GemmParams& p, int pair, int P, int it, Seg& w) {
+  const int dp_end = p.sk_tail ? p.sk_dp : p.m_tiles * p.n_tiles;
+  const int ndp = pair < dp_end ? (dp_end - pair + P - 1) / P : 0;
+  if (it < ndp) {
+    w.tile = pair + it * P;
+    w.kb0 = 0;
+    w.kb1 = p.num_kb;
+    w.kind = 0;
+    return true;
+  }
+  if (!p.sk_tail) return false;
+  int k = it - ndp;
+  const int a = sk_start(p, pair, P), b = sk_start(p, pair + 1, P);
+  if (a >= b) return false;
+  const int last_t = (b - 1) / p.num_kb;
+  const bool has_partial = b != (last_t + 1) * p.num_kb;
+  if (has_partial) {
+    if (k == 0) {
+      w.tile = p.sk_dp + last_t;
+      w.kb0 = max(a, last_t * p.num_kb) - last_t * p.num_kb;
+      w.kb1 = b - last_t * p.num_kb;
+      w.kind = 2;
+      return true;
+    }
+    --k;
+  }
+  // finishing segments in k order: tiles first_t .. (has_partial ? last_t-1 : last_t)
+  const int first_t = a / p.num_kb;
+  const int t = first_t + k;
+  if (t > (has_partial ? last_t - 1 : last_t)) return false;
+  w.tile = p.sk_dp + t;
+  w.kb0 = max(a, t * p.num_kb) - t * p.num_kb;
+  w.kb1 = p.num_kb;
+  w.kind = w.kb0 == 0 ? 0 : 1;  // a whole tile inside the range needs no fix-up
+  return true;
+}
+
+// The contributors of tail tile `tr` finished by pair f: pairs [j0, f).
+__device__ __forceinline__ int sk_first_contributor(const GemmParams& p, int tr, int f, int P) {
+  const int A = tr * p.num_kb;
+  int j = f - 1;
+  while (j >= 0 && sk_start(p, j + 1, P) > A) --j;
+  return j + 1;
+}
+
+struct TailFix {
+  const float* ws;  // nullptr: nothing to add
+  int j0, j1, rank, row;
+};
+
+__device__ __forceinline__ const float* sk_slot(const float* ws, int j, int rank) {
+  return ws + size_t(j) * SK_SLOT_FLOATS + size_t(rank) * (SK_SLOT_FLOATS / 2);
+}
+
+// v[0..31] (accumulator columns col..col+31 of this thread's row) += the
+// contributors' partials, in pair order
+__device__ __forceinline__ void fix_add(const TailFix& f, int col, float* v) {
+  if (f.ws == nullptr) return;
+  for (int j = f.j0; j < f.j1; ++j) {
+    const float4* src = reinterpret_cast<const float4*>(sk_slot(f.ws, j, f.rank) +
+                                                        (size_t(col >> 5) * 128 + f.row) * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 a = __ldcg(src + k);
+      v[4 * k] += a.x;
+      v[4 * k + 1] += a.y;
+      v[4 * k + 2] += a.z;
+      v[4 * k + 3] += a.w;
+    }
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void write_partial(uint32_t taddr, float* slot, int row) {
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    tmem_ld_wait();
+    float4* dst = reinterpret_cast<float4*>(slot + (size_t(c) * 128 + row) * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) __stcg(dst + k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+  }
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Epilogue of one output tile for the thread owning accumulator row `gm`
 // (TMEM address `taddr` = its lane, column 0 of the tile's accumulator).
 template <int BN>
-__device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr, int gm, int nt) {
+__device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr, int gm, int nt,
+                                             const TailFix& fx) {
   const bool ok = gm < p.Ma;
   if (p.epi == EPI_ROPE) {
     // the tile's BN columns are BN/hd whole heads of the q | k | v blocks
@@ -134,6 +252,8 @@ __device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr
         tmem_ld32(taddr + hh * p.hd + half + c * 32, y);
         tmem_ld_wait();
         if (!ok) continue;
+        fix_add(fx, hh * p.hd + c * 32, x);
+        fix_add(fx, hh * p.hd + half + c * 32, y);
         if (rot) {  // y[i] = x cos - x' sin, y' = x' cos + x sin (rotate_half)
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -187,6 +307,8 @@ __device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr
         tmem_ld32(taddr + h * 128 + c * 32, g);
         tmem_ld32(taddr + h * 128 + 64 + c * 32, v);
         tmem_ld_wait();
+        fix_add(fx, h * 128 + c * 32, g);
+        fix_add(fx, h * 128 + 64 + c * 32, v);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = silu(g[j]) * v[j];
         if (ok) store_row32(p.out + size_t(gm) * p.ldo + nt * (BN / 2) + h * 64 + c * 32, v);
@@ -198,6 +320,7 @@ __device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr
       float v[32];
       tmem_ld32(taddr + c * 32, v);
       tmem_ld_wait();
+      fix_add(fx, c * 32, v);
       const int col = nt * BN + c * 32;
       if (ok) {
         if (p.epi == EPI_RESID) add_row32(v, p.resid + size_t(gm) * p.ldr + col);
@@ -329,7 +452,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       {
-        epilogue_row<BN>(p, taddr, mt * BM + row, nt);
+        epilogue_row<BN>(p, taddr, mt * BM + row, nt, TailFix{nullptr, 0, 0, 0, 0});
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -424,10 +547,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     // leader's producer posts the expected bytes of both halves
     uint32_t g = 0;
     const uint32_t lfull = mapa_shared(full, 0);
-    for (int tile = pair; tile < total; tile += npairs) {
+    Seg w;
+    for (int it = 0; work_item(p, pair, npairs, it, w); ++it) {
       int mt, nt;
-      tile_coords(p, tile, mt, nt);
-      for (int kb = 0; kb < p.num_kb; ++kb, ++g) {
+      tile_coords(p, w.tile, mt, nt);
+      for (int kb = w.kb0; kb < w.kb1; ++kb, ++g) {
         const int stage = g % STAGES;
         const uint32_t phase = (g / STAGES) & 1;
         mbar_wait(&empty[stage], phase ^ 1);
@@ -454,11 +578,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < total; tile += npairs) {
+    Seg w;
+    for (int it = 0; work_item(p, pair, npairs, it, w); ++it) {
       mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < p.num_kb; ++kb) {
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint64_t ad = adesc0 + uint64_t((stage * C::A_BYTES) >> 4);
@@ -466,7 +591,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
           umma_commit_pair(&empty[stage]);
         }
         __syncwarp();
@@ -483,13 +608,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     const uint32_t ltempty = mapa_shared(tempty, 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < total; tile += npairs) {
+    Seg w;
+    for (int it = 0; work_item(p, pair, npairs, it, w); ++it) {
       int mt, nt;
-      tile_coords(p, tile, mt, nt);
+      tile_coords(p, w.tile, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      epilogue_row<BN>(p, taddr, mt * 2 * BM + int(rank) * BM + row, nt);
+      if (w.kind == 2) {
+        // partial: raw fp32 accumulator to this pair's slot, then one arrival
+        // per CTA on the tile's counter (every thread's stores fenced first)
+        write_partial<BN>(taddr, p.sk_ws + size_t(pair) * SK_SLOT_FLOATS + size_t(rank) * (SK_SLOT_FLOATS / 2),
+                          row);
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) atomicAdd(p.sk_cnt + (w.tile - p.sk_dp) * 2 + int(rank), 1);
+      } else {
+        TailFix fx{nullptr, 0, 0, int(rank), row};
+        if (w.kind == 1) {
+          const int tr = w.tile - p.sk_dp;
+          const int j0 = sk_first_contributor(p, tr, pair, npairs);
+          if (threadIdx.x == 64) {
+            int* c = p.sk_cnt + tr * 2 + int(rank);
+            while (ld_acquire_gpu(c) < pair - j0) __nanosleep(32);
+            *c = 0;  // every contributor has arrived: ready for the next launch
+          }
+          named_bar_sync(1, 128);
+          __threadfence();
+          fx = TailFix{p.sk_ws, j0, pair, int(rank), row};
+        }
+        epilogue_row<BN>(p, taddr, mt * 2 * BM + int(rank) * BM + row, nt, fx);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(ltempty + 8u * acc);
@@ -559,6 +708,32 @@ static bool use_pair(int BN, int max_ctas) {
   return on && BN == PAIR_BN && max_ctas >= 2;
 }
 
+// Stream-K tail policy.  Measured (tools/tail_layer_ab.py,
+// profiles/r02_gemm_tail_ab.jsonl): a last round with fewer busy pairs runs
+// its tiles faster than the wave model's equal-tile assumption (less HBM /
+// power contention), and the fix-up costs a few microseconds per finishing
+// tile (latency-bound partial reads in the epilogue), so splitting pays only
+// for long-K GEMMs (>= 128 k-blocks: the down projection) whose last round
+// would leave at least half of the pairs idle.  Then the last full round +
+// the partial one are split (units > P), or every tile (units < P).
+static bool tail_plan(int units, int P, int num_kb, int* dp, int* tail) {
+  *dp = units;
+  *tail = 0;
+  if (!gemm_tail_mode() || P < 2 || P > SK_MAX_PAIRS || num_kb < 128) return false;
+  if (units > P) {
+    const int R = units % P;
+    if (R == 0 || 2 * R > P) return false;
+    *dp = (units / P - 1) * P;
+  } else {
+    if (2 * units > P) return false;
+    *dp = 0;
+  }
+  *tail = units - *dp;
+  return long(*tail) * num_kb >= 8l * P;
+}
+
+static bool use_pair(int BN, int max_ctas);
+
 // Fill the tile geometry of `p` (T x N output, K reduction) and launch the
 // 1-CTA kernel or the CTA-pair kernel on at most `max_ctas` SMs.
 static int plan_and_launch(const CUtensorMap& ta, GemmParams& p, int T, int N, int K, int BN, int max_ctas,
@@ -580,12 +755,26 @@ static int plan_and_launch(const CUtensorMap& ta, GemmParams& p, int T, int N, i
   p.group_m = a_tile_bytes * p.m_tiles <= 2 * budget ? p.m_tiles
                                                      : int(std::max<long>(pair ? 4 : 8, budget / a_tile_bytes));
   const int units = p.m_tiles * p.n_tiles;
-  if (pair) return launch_pair(ta, p, 2 * std::min(units, max_ctas / 2), st);
+  p.sk_dp = units;
+  p.sk_tail = 0;
+  if (pair) {
+    int P = std::min(units, max_ctas / 2);
+    int dp = 0, tail = 0;
+    SkWorkspace ws{};
+    if (tail_plan(units, max_ctas / 2, p.num_kb, &dp, &tail) && sk_workspace(st, &ws) == HP_OK) {
+      P = max_ctas / 2;
+      p.sk_dp = dp;
+      p.sk_tail = tail;
+      p.sk_ws = ws.ws;
+      p.sk_cnt = ws.cnt;
+    }
+    return launch_pair(ta, p, 2 * P, st);
+  }
   const int grid = std::min(units, max_ctas);
   return BN == 128 ? launch<128>(ta, p, grid, st) : launch<256>(ta, p, grid, st);
 }
 
-static int gemm_bn(int T, int N, int ctas);
+static int gemm_bn(int T, int N, int K, int ctas);
 
 extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, int T,
                                 int Hq, int Hkv, int d, int K, const int* positions, const float* cos_sin,
@@ -599,7 +788,7 @@ extern "C" int hp_gemm_qkv_rope(const void* X, int ldx, const void* W, int ldw, 
   HP_CHECK_ARG(page >= 64 && page % 64 == 0 && max_ctas >= 1, "hp_gemm_qkv_rope: page must be a multiple of 64");
   const int N = (Hq + 2 * Hkv) * d;
   HP_CHECK_ARG(N % 128 == 0 && ldy >= N && ldy % 8 == 0, "hp_gemm_qkv_rope: (Hq+2Hkv)*d must be a multiple of 128");
-  const int BN = gemm_bn(T, N, max_ctas);
+  const int BN = gemm_bn(T, N, K, max_ctas);
   CUtensorMap ta;
   int rc = cached_tmap_bf16(&ta, X, T, K, ldx, BM, BK, true);
   if (rc) return rc;
@@ -636,7 +825,7 @@ extern "C" int hp_gemm(const void* X, int ldx, const void* W, int ldw, void* Y, 
 // the activation tile is re-streamed per 128 columns and the MMA is half
 // as wide), folded in as 1.25.
 // HP_GEMM_BN=128|256 forces a width (measurement).
-static int gemm_bn(int T, int N, int ctas) {
+static int gemm_bn(int T, int N, int K, int ctas) {
   static const int forced = [] {
     const char* e = std::getenv("HP_GEMM_BN");
     return e ? std::atoi(e) : 0;
@@ -645,21 +834,34 @@ static int gemm_bn(int T, int N, int ctas) {
   if (N % 256 != 0) return 128;
   const int m = (T + BM - 1) / BM;
   const long t256 = long(m) * (N / 256), t128 = long(m) * (N / 128);
-  const double c256 = double((t256 + ctas - 1) / ctas) * 256.0;
+  double c256 = double((t256 + ctas - 1) / ctas) * 256.0;
+  if (ctas >= 4 && use_pair(256, ctas)) {  // pair tiles: 256-row units over ctas / 2 pairs
+    const int units = ((T + 2 * BM - 1) / (2 * BM)) * (N / 256);
+    int dp = 0, tail = 0;
+    if (tail_plan(units, ctas / 2, K / BK, &dp, &tail))
+      c256 = (double(units) / (ctas / 2) + 0.1) * 256.0;  // rounds spread evenly, + fix-up
+    else
+      c256 = double((units + ctas / 2 - 1) / (ctas / 2)) * 256.0;
+  }
   const double c128 = double((t128 + ctas - 1) / ctas) * 128.0 * 1.25;
   return c128 < c256 ? 128 : 256;
 }
 
 extern "C" int hp_gemm_tiles(int T, int N) { return ((T + BM - 1) / BM) * (N / 256); }
 
-extern "C" int hp_gemm_plan(int T, int N, int max_ctas, int* bn, int* tiles, int* ctas_per_tile) {
-  HP_CHECK_ARG(T >= 1 && N % 128 == 0 && max_ctas >= 1, "hp_gemm_plan: bad shape");
-  const int b = gemm_bn(T, N, max_ctas);
+extern "C" int hp_gemm_plan(int T, int N, int K, int max_ctas, int* bn, int* tiles, int* ctas_per_tile,
+                            int* tail_tiles) {
+  HP_CHECK_ARG(T >= 1 && N % 128 == 0 && K % 128 == 0 && max_ctas >= 1, "hp_gemm_plan: bad shape");
+  const int b = gemm_bn(T, N, K, max_ctas);
   const bool pair = use_pair(b, max_ctas);
   const int rows = pair ? 2 * BM : BM;
+  const int t = ((T + rows - 1) / rows) * (N / b);
+  int dp = 0, tail = 0;
+  if (!pair || !tail_plan(t, max_ctas / 2, K / BK, &dp, &tail)) tail = 0;
   if (bn) *bn = b;
-  if (tiles) *tiles = ((T + rows - 1) / rows) * (N / b);
+  if (tiles) *tiles = t;
   if (ctas_per_tile) *ctas_per_tile = pair ? 2 : 1;
+  if (tail_tiles) *tail_tiles = tail;
   return HP_OK;
 }
 
@@ -674,7 +876,7 @@ extern "C" int hp_gemm_traced(const void* X, int ldx, const void* W, int ldw, vo
   HP_CHECK_ARG(max_ctas >= 1, "hp_gemm: max_ctas must be >= 1");
   HP_CHECK_ARG(N % 128 == 0, "hp_gemm: N must be a multiple of 128 (tiled weight layout)");
   HP_CHECK_ARG(ldw == K, "hp_gemm: W must be in the tiled layout (ldw == K)");
-  const int BN = gemm_bn(T, N, max_ctas);
+  const int BN = gemm_bn(T, N, K, max_ctas);
   CUtensorMap ta;
   int rc = cached_tmap_bf16(&ta, X, T, K, ldx, BM, BK, true);
   if (rc) return rc;

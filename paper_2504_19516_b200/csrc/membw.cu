@@ -35,6 +35,154 @@ __global__ void __launch_bounds__(512) k_membw_ldg(const uint4* __restrict__ src
   if (acc == 0x12345678u) out[0] = 1.f;  // keep the loads alive
 }
 
+
+// Register-direct streaming probe: every warp streams contiguous 512*U-byte
+// chunks with U independent 128-bit loads per lane, software-pipelined so
+// the next chunk's loads are in flight while the current one is consumed
+// (2U loads per lane outstanding).  noalloc: ld.global.nc.L1::no_allocate
+// (bypasses the L1 data array), else ld.global.cs.  Question it answers:
+// does a reader that never stages through shared memory stream more bytes
+// per SM than the bulk-copy + ldmatrix path (smem crossbar, 128 B/clk shared
+// by the copy's writes and the reads)?
+HP_DEVICE uint4 ldg_na(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+template <int U, bool NA>
+__global__ void k_membw_ldg2(const uint4* __restrict__ src, size_t n16, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const size_t warps = size_t(gridDim.x) * (blockDim.x >> 5);
+  const size_t w = size_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const size_t chunk = size_t(U) * 32;  // uint4 per chunk
+  const size_t nch = n16 / chunk;
+  uint32_t acc = 0;
+  uint4 v[U], nv[U];
+  size_t c = w;
+  auto ld = [&](size_t cc, uint4 (&d)[U]) {
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint4* a = src + cc * chunk + j * 32 + lane;
+      d[j] = NA ? ldg_na(a) : __ldcs(a);
+    }
+  };
+  if (c < nch) ld(c, v);
+  for (; c < nch; c += warps) {
+    const bool more = c + warps < nch;
+    if (more) ld(c + warps, nv);
+#pragma unroll
+    for (int j = 0; j < U; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = nv[j];
+  }
+  if (acc == 0x12345678u) out[0] = 1.f;
+}
+
+// Legacy warp-level MMA rate (mma.sync.m16n8k16 bf16 -> fp32, HMMA.16816):
+// every warp issues n x C independent MMAs; out[cta] = cycles.  Tells whether
+// a register-fed decode GEMM could keep up with ~200 GB/s per SM of weights
+// (N = 32 tokens: 16 MAC per weight byte).
+template <int C>
+__global__ void k_hmma_rate(int n, long long* out) {
+  uint32_t a[4] = {threadIdx.x, threadIdx.x * 3u, threadIdx.x ^ 5u, 7u};
+  uint32_t b[2] = {threadIdx.x * 7u, 11u};
+  float d[C][4];
+#pragma unroll
+  for (int c = 0; c < C; ++c) d[c][0] = d[c][1] = d[c][2] = d[c][3] = 0.f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) mma_bf16_16816(d[c], a, b);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c) s += d[c][0] + d[c][1] + d[c][2] + d[c][3];
+  if (s == 1.2345f) out[gridDim.x] = 1;
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+}
+
+
+// Both paths at once on every SM: warp 0 streams the first `bulk_frac`/256
+// of the buffer's 32 KB chunks (per CTA blocked range) through a 6 x 32 KB
+// bulk-copy ring, the other warps stream the rest with U=8 pipelined LDGs.
+// If the two paths' per-SM limits (smem port / registers in flight) are
+// independent, the sum exceeds either alone.
+__global__ void __launch_bounds__(544, 1) k_membw_mix(const uint8_t* __restrict__ src, size_t bytes,
+                                                      int bulk_frac, float* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  constexpr uint32_t CH = 32 * 1024;
+  constexpr int NST = 6;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * CH);
+  const size_t nch = bytes / CH;
+  const size_t per = (nch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = blockIdx.x * per;
+  const size_t my = c0 >= nch ? 0 : std::min(per, nch - c0);
+  uint32_t acc = 0;
+  const bool read_all = bulk_frac >= 1024;  // + 1024: warp 0 reads every staged byte (ld.shared.v4)
+  if (read_all) bulk_frac -= 1024;
+  const size_t nb = my * size_t(bulk_frac) / 256;  // chunks for the bulk path
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    auto issue = [&](size_t k) {
+      const int s = int(k % NST);
+      mbar_arrive_expect_tx(&full[s], CH);
+      bulk_load(base + size_t(s) * CH, src + (c0 + k) * CH, CH, &full[s]);
+    };
+    if (lane == 0)
+      for (size_t k = 0; k < std::min<size_t>(nb, NST); ++k) issue(k);
+    for (size_t k = 0; k < nb; ++k) {
+      const int s = int(k % NST);
+      mbar_wait(&full[s], uint32_t((k / NST) & 1));
+      if (read_all) {
+        const uint4* b4 = reinterpret_cast<const uint4*>(base + size_t(s) * CH);
+#pragma unroll 8
+        for (int i = lane; i < int(CH / 16); i += 32) {
+          const uint4 v = b4[i];
+          acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+      } else if (lane == 0) {
+        acc ^= *reinterpret_cast<const uint32_t*>(base + size_t(s) * CH);
+      }
+      __syncwarp();
+      if (lane == 0 && k + NST < nb) issue(k + NST);
+    }
+  } else {
+    constexpr int U = 8;
+    const int lane = threadIdx.x & 31;
+    const int w = (threadIdx.x >> 5) - 1, nw = (blockDim.x >> 5) - 1;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + (c0 + nb) * CH);
+    const size_t n16 = (my - nb) * (CH / 16);
+    const size_t chunk = U * 32;
+    const size_t nc = n16 / chunk;
+    uint4 v[U], nv[U];
+    size_t c = w;
+    auto ld = [&](size_t cc, uint4 (&d)[U]) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) d[j] = ldg_na(s4 + cc * chunk + j * 32 + lane);
+    };
+    if (c < nc) ld(c, v);
+    for (; c < nc; c += nw) {
+      if (c + nw < nc) ld(c + nw, nv);
+#pragma unroll
+      for (int j = 0; j < U; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = nv[j];
+    }
+  }
+  if (acc == 0x12345678u) out[0] = 1.f;
+}
+
 constexpr int MB_STAGES = 6;
 constexpr uint32_t MB_CHUNK = 32 * 1024;
 
@@ -467,5 +615,53 @@ extern "C" int hp_membw(const void* src, size_t bytes, int ctas, int method, flo
     k_membw_tma<<<ctas, 128, smem, st>>>(static_cast<const uint8_t*>(src), bytes, out);
   }
   HP_LAUNCH_CHECK("k_membw");
+  return HP_OK;
+}
+
+extern "C" int hp_membw_ldg(const void* src, size_t bytes, int ctas, int threads, int unroll, int noalloc,
+                            float* out, void* stream) {
+  HP_CHECK_ARG(src && out && ctas >= 1 && threads >= 32 && threads <= 1024 && threads % 32 == 0 &&
+                   (unroll == 2 || unroll == 4 || unroll == 8 || unroll == 16),
+               "hp_membw_ldg: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint4* s = static_cast<const uint4*>(src);
+  const size_t n = bytes / 16;
+#define HP_LDG_CASE(U)                                                        \
+  if (unroll == U) {                                                          \
+    if (noalloc) k_membw_ldg2<U, true><<<ctas, threads, 0, st>>>(s, n, out);  \
+    else k_membw_ldg2<U, false><<<ctas, threads, 0, st>>>(s, n, out);         \
+  }
+  HP_LDG_CASE(2) HP_LDG_CASE(4) HP_LDG_CASE(8) HP_LDG_CASE(16)
+#undef HP_LDG_CASE
+  HP_LAUNCH_CHECK("k_membw_ldg2");
+  return HP_OK;
+}
+
+extern "C" int hp_membw_mix(const void* src, size_t bytes, int ctas, int ldg_warps, int bulk_frac, float* out,
+                            void* stream) {
+  HP_CHECK_ARG(src && out && ctas >= 1 && ldg_warps >= 1 && ldg_warps <= 16 && bulk_frac >= 0 &&
+                   bulk_frac % 1024 <= 256 && bytes % (32 * 1024) == 0, "hp_membw_mix: bad arguments");
+  const size_t smem = 6 * 32 * 1024 + 128 + 64;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_membw_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  k_membw_mix<<<ctas, 32 * (1 + ldg_warps), smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), bytes, bulk_frac, out);
+  HP_LAUNCH_CHECK("k_membw_mix");
+  return HP_OK;
+}
+
+extern "C" int hp_hmma_rate(int n, int chains, int ctas, int threads, long long* out, void* stream) {
+  HP_CHECK_ARG(out && n >= 1 && ctas >= 1 && threads >= 32 && threads <= 1024 && threads % 32 == 0 &&
+                   (chains == 1 || chains == 2 || chains == 4 || chains == 8),
+               "hp_hmma_rate: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (chains == 1) k_hmma_rate<1><<<ctas, threads, 0, st>>>(n, out);
+  if (chains == 2) k_hmma_rate<2><<<ctas, threads, 0, st>>>(n, out);
+  if (chains == 4) k_hmma_rate<4><<<ctas, threads, 0, st>>>(n, out);
+  if (chains == 8) k_hmma_rate<8><<<ctas, threads, 0, st>>>(n, out);
+  HP_LAUNCH_CHECK("k_hmma_rate");
   return HP_OK;
 }

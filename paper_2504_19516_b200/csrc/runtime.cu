@@ -3,6 +3,7 @@
 #include <cstdlib>
 
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -130,6 +131,7 @@ int cached_tmap_bf16(CUtensorMap* out, const void* base, uint64_t rows, uint64_t
 }
 
 static void* g_trace[TRACE_KINDS] = {nullptr, nullptr, nullptr};
+static int g_gemm_tail = -1;  // -1: HP_GEMM_TAIL environment default
 void* trace_buf(int kind) { return g_trace[kind]; }
 uint64_t* take_cta_trace() {
   void* b = g_trace[TRACE_CTAS];
@@ -162,4 +164,44 @@ int device_sm_count() {
   return n;
 }
 
+int gemm_tail_mode() {
+  static const int env = [] {
+    const char* e = std::getenv("HP_GEMM_TAIL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return g_gemm_tail < 0 ? env : g_gemm_tail;
+}
+
+// One stream-K workspace per stream: launches on one stream are ordered, so
+// they may share it; two streams running prefill GEMMs at once must not.
+// Never freed (a captured graph may hold the pointers).
+static std::mutex g_sk_mu;
+static std::map<cudaStream_t, SkWorkspace> g_sk;
+
+int sk_workspace(cudaStream_t st, SkWorkspace* out) {
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  auto it = g_sk.find(st);
+  if (it != g_sk.end()) {
+    *out = it->second;
+    return HP_OK;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return set_error(HP_ERR_CUDA, "stream-K workspace: first use may not be inside a capture");
+  SkWorkspace w{};
+  HP_CUDA_TRY(cudaMalloc(&w.ws, size_t(SK_MAX_PAIRS) * SK_SLOT_FLOATS * sizeof(float)));
+  HP_CUDA_TRY(cudaMalloc(&w.cnt, size_t(SK_MAX_PAIRS) * 4 * sizeof(int)));
+  HP_CUDA_TRY(cudaMemset(w.cnt, 0, size_t(SK_MAX_PAIRS) * 4 * sizeof(int)));
+  HP_CUDA_TRY(cudaDeviceSynchronize());
+  g_sk.emplace(st, w);
+  *out = w;
+  return HP_OK;
+}
+
 }  // namespace hp
+
+extern "C" int hp_set_gemm_tail(int mode) {
+  HP_CHECK_ARG(mode >= -1 && mode <= 1, "hp_set_gemm_tail: mode must be -1, 0 or 1");
+  hp::g_gemm_tail = mode;
+  return HP_OK;
+}

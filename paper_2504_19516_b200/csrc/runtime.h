@@ -78,6 +78,22 @@ void* trace_buf(int kind);
 // the armed buffer (per-CTA {smid, start_ns, end_ns}) and disarms it.
 uint64_t* take_cta_trace();
 
+// Stream-K tail of the prefill CTA-pair GEMM (hp_set_gemm_tail; default
+// on unless HP_GEMM_TAIL=0): 1 = split the last partial wave of tiles along
+// K over all pairs, 0 = plain persistent rounds (wave_stats rounds).
+int gemm_tail_mode();
+// Per-stream workspace: SK_MAX_PAIRS partial-tile slots of SK_SLOT_FLOATS
+// fp32 (a 256 x 256 accumulator, both CTAs' halves) + [pairs][2] arrival
+// counters for up to 2 * SK_MAX_PAIRS tail tiles (zero between launches:
+// the finishing CTA resets its counter).
+constexpr int SK_MAX_PAIRS = 80;
+constexpr int SK_SLOT_FLOATS = 256 * 256;
+struct SkWorkspace {
+  float* ws;
+  int* cnt;
+};
+int sk_workspace(cudaStream_t st, SkWorkspace* out);
+
 // PDL on unless the environment sets HP_PDL=0 (A/B measurement).
 bool pdl_enabled();
 

@@ -448,7 +448,7 @@ class CoRunner:
         w = self.layer.W
         units = {}
         for g, wt in (("qkv", w.w_qkv), ("o_proj", w.w_o), ("mlp_up_gate", w.w_ug), ("mlp_down", w.w_down)):
-            _, tiles, cpt = lib.gemm_plan(T, wt.shape[0], pm)
+            _, tiles, cpt = lib.gemm_plan(T, wt.shape[0], wt.shape[1], pm)
             units[g] = (tiles, pm // cpt)
         units["attn"] = (-(-T // 256) * m.num_heads, pm)
         groups, busy_sm_s = {}, 0.0

@@ -38,7 +38,7 @@ SIGNATURES = {
     "hp_gemm_traced": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "hp_gemm_tiles": (_i, [_i, _i]),
     "hp_gemm_qkv_rope": (_i, [_p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
-    "hp_gemm_plan": (_i, [_i, _i, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "hp_gemm_plan": (_i, [_i, _i, _i, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_peer_tiles": (_i, [_i, _i]),
@@ -53,6 +53,7 @@ SIGNATURES = {
     "hp_rope_kv_write": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
     "hp_set_trace": (_i, [_i, _p]),
+    "hp_set_gemm_tail": (_i, [_i]),
     "hp_prefill_attn_paged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _i, _i, _i, _f,
                                    _i, _p]),
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
@@ -63,6 +64,9 @@ SIGNATURES = {
     "hp_membw": (_i, [_p, _sz, _i, _i, _p, _p]),
     "hp_membw2d": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "hp_membw_pipe": (_i, [_p, _sz, _i, _i, _i, _p, _p]),
+    "hp_membw_ldg": (_i, [_p, _sz, _i, _i, _i, _i, _p, _p]),
+    "hp_hmma_rate": (_i, [_i, _i, _i, _i, _p, _p]),
+    "hp_membw_mix": (_i, [_p, _sz, _i, _i, _i, _p, _p]),
     "hp_umma2_rate": (_i, [_i, _i, _i, _p, _p]),
     "hp_umma_rate": (_i, [_i, _i, _i, _i, _p, _p]),
 }
@@ -271,13 +275,23 @@ def gemm_qkv_rope(x, w, y, Hq: int, Hkv: int, d: int, positions, cos_sin, slots,
                                   _ptr(vcache), page, max_ctas, _stream(stream)), "hp_gemm_qkv_rope")
 
 
-def gemm_plan(T: int, N: int, max_ctas: int) -> tuple[int, int, int]:
+def gemm_plan(T: int, N: int, K: int, max_ctas: int) -> tuple[int, int, int]:
     """(tile width, tile count, CTAs per tile) hp_gemm uses on a
-    `max_ctas`-SM partition; its persistent grid runs
-    wave_stats(tiles, 1, max_ctas // ctas_per_tile) rounds."""
-    bn, tiles, cpt = C.c_int(), C.c_int(), C.c_int()
-    check(load().hp_gemm_plan(T, N, max_ctas, C.byref(bn), C.byref(tiles), C.byref(cpt)), "hp_gemm_plan")
+    `max_ctas`-SM partition; without a stream-K tail (gemm_tail_tiles == 0)
+    its persistent grid runs wave_stats(tiles, 1, max_ctas // ctas_per_tile)
+    rounds."""
+    bn, tiles, cpt, tail = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(load().hp_gemm_plan(T, N, K, max_ctas, C.byref(bn), C.byref(tiles), C.byref(cpt), C.byref(tail)),
+          "hp_gemm_plan")
     return bn.value, tiles.value, cpt.value
+
+
+def gemm_tail_tiles(T: int, N: int, K: int, max_ctas: int) -> int:
+    """Tiles hp_gemm's stream-K tail splits over every pair (0: plain rounds)."""
+    bn, tiles, cpt, tail = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(load().hp_gemm_plan(T, N, K, max_ctas, C.byref(bn), C.byref(tiles), C.byref(cpt), C.byref(tail)),
+          "hp_gemm_plan")
+    return tail.value
 
 
 def prefill_attn_paged(q, kcache, vcache, block_table, cu_seqlens, prior_lens, nseq: int, max_seqlen: int,
@@ -342,6 +356,13 @@ def hold(stream, cycles: int) -> None:
 
 def set_trace(kind: int, buf) -> None:
     check(load().hp_set_trace(kind, _ptr(buf)), "hp_set_trace")
+
+
+def set_gemm_tail(mode: int) -> None:
+    """Stream-K tail of the prefill CTA-pair GEMM: 1 on, 0 off (plain
+    persistent rounds, the grid wave_stats describes), -1 the HP_GEMM_TAIL
+    environment default (on)."""
+    check(load().hp_set_gemm_tail(mode), "hp_set_gemm_tail")
 
 
 TRACE_CTAS = 2

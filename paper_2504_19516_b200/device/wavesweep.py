@@ -29,25 +29,35 @@ from .layer import LayerWeights
 from .partition import DECODE, PREFILL, PartitionPool
 
 
-def measure(pool: PartitionPool, x, w, y, epi, resid, n: int, reps: int = 3):
+def measure(pool: PartitionPool, x, w, y, epi, resid, n: int, reps: int = 3, tail: int = 0):
+    """Measured idle of one GEMM launch on an n-SM partition, with the
+    launch's plan (tiles, CTAs per tile) under the same tail mode.  tail = 0 (the
+    default) times the plain persistent rounds that wave_stats describes;
+    tail = 1 the stream-K tail (lib.set_gemm_tail), which spreads the last
+    rounds' work over every pair."""
     st = pool.phase(DECODE, n) if n < pool.n else pool.full(PREFILL)
-    _, tiles, cpt = lib.gemm_plan(x.shape[0], w.shape[0], st.sms)
-    grid = min(tiles * cpt, (st.sms // cpt) * cpt)
-    times = torch.zeros(grid, 3, dtype=torch.int64, device=x.device)
+    times = torch.zeros(st.sms, 3, dtype=torch.int64, device=x.device)
     best = None
-    with torch.cuda.stream(st.torch_stream):
-        for _ in range(reps):
-            lib.hold(st.torch_stream, 100_000)
-            lib.gemm_traced(x, w, y, times, epi, resid=resid, max_ctas=st.sms, stream=st.torch_stream)
-            st.torch_stream.synchronize()
-            t = times.cpu()
-            start, end = t[:, 1], t[:, 2]
-            span = float(end.max() - start.min())
-            busy = float((end - start).sum())
-            idle = 1.0 - busy / (st.sms * span)
-            if best is None or span < best[1]:
-                best = (idle, span, len(set(t[:, 0].tolist())))
-    return best[0], best[1] * 1e-9, best[2], st.sms
+    lib.set_gemm_tail(tail)
+    try:
+        _, tiles, cpt = lib.gemm_plan(x.shape[0], w.shape[0], w.shape[1], st.sms)
+        with torch.cuda.stream(st.torch_stream):
+            for _ in range(reps):
+                times.zero_()
+                lib.hold(st.torch_stream, 100_000)
+                lib.gemm_traced(x, w, y, times, epi, resid=resid, max_ctas=st.sms, stream=st.torch_stream)
+                st.torch_stream.synchronize()
+                t = times.cpu()
+                t = t[t[:, 2] > 0]  # CTAs of this launch
+                start, end = t[:, 1], t[:, 2]
+                span = float(end.max() - start.min())
+                busy = float((end - start).sum())
+                idle = 1.0 - busy / (st.sms * span)
+                if best is None or span < best[1]:
+                    best = (idle, span, len(set(t[:, 0].tolist())))
+    finally:
+        lib.set_gemm_tail(-1)
+    return best[0], best[1] * 1e-9, best[2], st.sms, tiles, cpt
 
 
 def main(argv=None) -> int:
@@ -74,8 +84,7 @@ def main(argv=None) -> int:
                  ("mlp_down", xi, W.w_down, torch.empty(T, h, **bf), lib.EPI_RESID, xh)]
         for name, x, w, y, epi, r in gemms:
             for n in grid:
-                idle, span, sms_seen, n_real = measure(pool, x, w, y, epi, r, n)
-                _, tiles, cpt = lib.gemm_plan(T, w.shape[0], n_real)
+                idle, span, sms_seen, n_real, tiles, cpt = measure(pool, x, w, y, epi, r, n)
                 pred = wave_stats(tiles, 1, n_real // cpt)
                 row = {"kernel": name, "T": T, "tiles": tiles, "n": n_real,
                        "predicted_idle": pred.idle_ratio, "waves": pred.waves, "tail_sms": pred.tail_sms,

@@ -64,17 +64,31 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
 
 
 def test_gemm_tile_planner_is_host_side():
-    # hp_gemm_plan: CTA-pair 256x256 tiles by default; 128-wide single-CTA
-    # tiles where they save a wave-quantised round (T=1024 qkv on 148 SMs)
-    assert lib.gemm_plan(4096, 28672, 140) == (256, 16 * 112, 2)
-    assert lib.gemm_plan(4096, 4096, 140) == (256, 16 * 16, 2)
-    bn, tiles, cpt = lib.gemm_plan(1024, 6144, 148)
+    # hp_gemm_plan: CTA-pair 256x256 tiles by default (the stream-K tail
+    # absorbs the last round); without the tail, 128-wide single-CTA tiles
+    # where they save a wave-quantised round (T=1024 qkv on 148 SMs)
+    assert lib.gemm_plan(4096, 28672, 4096, 140) == (256, 16 * 112, 2)
+    assert lib.gemm_plan(4096, 4096, 4096, 140) == (256, 16 * 16, 2)
+    bn, tiles, cpt = lib.gemm_plan(1024, 6144, 4096, 148)
     assert (bn, cpt) == (128, 1) and tiles == 8 * 48
-    assert lib.gemm_plan(300, 512, 1)[2] == 1  # one SM: no pair
+    # the stream-K tail only for long-K GEMMs whose last round would leave
+    # >= half the pairs idle: T = 1024 mlp_down on 124 SMs (64 tiles, 62
+    # pairs) runs as pair tiles with the last two rounds split evenly
+    assert lib.gemm_plan(1024, 4096, 14336, 124) == (256, 4 * 16, 2)
+    assert lib.gemm_tail_tiles(1024, 4096, 14336, 124) == 64
+    assert lib.gemm_tail_tiles(4096, 4096, 14336, 140) == 0  # 256 = 3 x 70 + 46: plain
+    assert lib.gemm_tail_tiles(4096, 4096, 4096, 148) == 0   # short K: plain
+    lib.set_gemm_tail(0)
+    try:
+        assert lib.gemm_tail_tiles(1024, 4096, 14336, 124) == 0
+        assert lib.gemm_plan(1024, 4096, 14336, 124)[2] == 1  # plain: 128-wide single-CTA tiles
+    finally:
+        lib.set_gemm_tail(-1)
+    assert lib.gemm_plan(300, 512, 640, 1)[2] == 1  # one SM: no pair
     from paper_2504_19516_b200.perf_model import wave_stats
 
     # the rounds the persistent grid runs are the paper's wave count
-    _, t, c = lib.gemm_plan(4096, 6144, 140)
+    _, t, c = lib.gemm_plan(4096, 6144, 4096, 140)
     assert wave_stats(t, 1, 140 // c).waves == 6
 
 

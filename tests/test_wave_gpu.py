@@ -51,13 +51,33 @@ def test_gemm_wave_idle_measured_vs_model(env):
                                "mlp_up_gate": (W.w_ug, xh, I, lib.EPI_SILU, None),
                                "mlp_down": (W.w_down, xi, h, lib.EPI_RESID, xh)}[name]
         y = torch.empty(T, N_out, **bf)
-        idle, span, sms_seen, n_real = measure(pool, x, w, y, epi, r, n)
-        _, tiles, cpt = lib.gemm_plan(T, w.shape[0], n_real)
+        idle, span, sms_seen, n_real, tiles, cpt = measure(pool, x, w, y, epi, r, n)
         pred = wave_stats(tiles, 1, n_real // cpt).idle_ratio
         assert sms_seen <= n_real  # confined to the partition
         errs.append(abs(idle - pred))
         assert abs(idle - pred) <= 0.06, (name, T, n, idle, pred)
     assert sum(errs) / len(errs) <= 0.025, errs
+
+
+def test_gemm_stream_k_tail_reclaims_wave_idle(env):
+    """The stream-K tail (on by default for long-K GEMMs whose last round
+    would leave >= half the pairs idle) spreads the last full round plus the
+    partial one over every pair: the measured idle must be below half of what
+    the wave model predicts for the same pair tiles in plain rounds (+3 pp
+    for the fix-up)."""
+    pool, W = env
+    h, I = M.hidden, M.intermediate
+    bf = dict(dtype=torch.bfloat16, device=DEV)
+    for T, n in ((1024, 120), (2048, 104), (4096, 96)):  # SM counts on the 8-grid
+        xh, xi = torch.randn(T, h, **bf), torch.randn(T, I, **bf)
+        y = torch.empty(T, h, **bf)
+        assert lib.gemm_tail_tiles(T, h, I, n) > 0
+        idle, span, sms_seen, n_real, tiles, cpt = measure(pool, xi, W.w_down, y, lib.EPI_RESID, xh, n, tail=1)
+        assert cpt == 2
+        pred = wave_stats(tiles, 1, n_real // cpt).idle_ratio
+        assert pred >= 0.10, (T, n, pred)
+        assert idle <= pred / 2 + 0.03, (T, n, pred, idle)
+        assert sms_seen <= n_real  # still confined to the partition
 
 
 def test_prefill_attention_cta_trace_and_wave_model(env):
