@@ -554,6 +554,7 @@ def main(argv=None) -> int:
 
     # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
     dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}
+    ingest = {f"sms_{k}": cr.sm_ingest_gbs(k) for k in sorted({dm, N})}
 
     # ---- all four prefill GEMMs together (north-star target: >= 85 % of the partition's tensor peak)
     gemm_flops = 2.0 * T * model.hidden * (model.qkv_out_dim + model.hidden + 3 * mlp_width(model))
@@ -630,7 +631,12 @@ def main(argv=None) -> int:
         "roofline_targets_split": hbm_split,
         "roofline_decode_attn": {"bound": "hbm", "unit": "GB/s", "peak": hbm_gbs,
                                  "bytes_per_launch": cr.decode_attn_bytes(),
-                                 **{k: {"achieved": v, "frac": v / hbm_gbs} for k, v in dattn.items()}},
+                                 **{k: {"achieved": v, "frac": v / hbm_gbs, "sm_ingest_gbs": ingest[k],
+                                        "frac_of_sm_ingest": v / ingest[k]} for k, v in dattn.items()},
+                                 "sm_ingest_note": "sm_ingest_gbs = the same partition's raw HBM->SM stream "
+                                                   "(bulk copies into shared memory, nothing read back; "
+                                                   "hp_membw method 1): the per-SM ceiling below n_d SMs, "
+                                                   "which a staged reader pays twice (copy-in + ldmatrix)"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_tokens / e2e_span, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

@@ -134,6 +134,17 @@ int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ld
                  int ldr, int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes,
                  int* counters, int n_counters, int max_ctas, void* stream);
 
+/* Decode QKV projection with RoPE and the paged K/V write fused into the
+ * swap-AB GEMM's epilogue: hp_gemm_swap (epilogue STORE) followed by
+ * hp_rope_kv_write, as one launch with the same bits (workload.py:164-170;
+ * replaces the GEMM + rope pair of the decode step, engine.py:676).
+ * N = (Hq + 2 Hkv) * d; positions / slot_mapping / caches as hp_rope_kv_write,
+ * workspace / counters as hp_gemm_swap. */
+int hp_gemm_swap_qkv_rope(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, int T, int Hq,
+                          int Hkv, int d, int K, const int* positions, const float* cos_sin,
+                          const int* slot_mapping, void* kcache, void* vcache, int page, void* workspace,
+                          size_t ws_bytes, int* counters, int n_counters, int max_ctas, void* stream);
+
 /* Fused row-parallel GEMM + all-reduce for tensor-parallel decode (config 5,
  * SURVEY.md §8(f)#4; replaces the NCCL all-reduce after o_proj / mlp_down of
  * a Megatron row-parallel layer).  Symmetric buffers: every

@@ -422,6 +422,23 @@ HP_DEVICE float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 HP_DEVICE float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
 // byte offset of 16-byte chunk `c` (0..7) of row `r` in a 128B-swizzled tile
+// Rotary embedding of one (x, y) = (dim i, dim i + d/2) pair ("rotate_half"),
+// with explicit rounding (no FMA contraction) so every kernel that applies it
+// -- hp_rope_kv_write, the prefill QKV GEMM epilogue, the decode swap GEMM
+// epilogue -- produces the same bits, and the numpy oracle's fp32 x*c - y*s.
+HP_DEVICE void rope_rotate(float x, float y, float c, float s, float& nx, float& ny) {
+  nx = __fsub_rn(__fmul_rn(x, c), __fmul_rn(y, s));
+  ny = __fadd_rn(__fmul_rn(y, c), __fmul_rn(x, s));
+}
+
+// Element index of (kv head kvh, head dim j) of cache slot (blk, off) in the
+// paged layout [num_blocks][Hkv][page/64][d/64][64][64] with the 16-byte
+// chunks of token row (off & 63) permuted by (off & 7) (SWIZZLE_128B).
+HP_DEVICE size_t kv_cache_index(int blk, int Hkv, int kvh, int page, int off, int d, int j) {
+  return (((size_t(blk) * Hkv + kvh) * (page / 64) + off / 64) * (d / 64) + j / 64) * 4096 +
+         size_t(off & 63) * 64 + ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7);
+}
+
 HP_DEVICE uint32_t sw128(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
 
 }  // namespace hp

@@ -83,7 +83,17 @@ struct SwapParams {
   const int* epoch_dev;
   int world, rank, epoch;
   int two_shot;     // 1: a tile goes only to its owner rank (feature tile mt % world)
+  // SW_EPI_ROPE (decode QKV, hp_gemm_swap_qkv_rope): rotary embedding of the
+  // q / k heads and the paged K / V write of the new tokens, fused
+  const int* pos;
+  const float* cos_sin;  // fp32 [max_pos, hd] = [cos(hd/2) | sin(hd/2)]
+  const int* slots;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  int page, Hq, Hkv, hd;
 };
+
+constexpr int SW_EPI_ROPE = 4;  // internal epilogue id (after HP_EPI_PEER)
 
 struct Seg {
   int tile, kb0, kb1;
@@ -137,6 +147,42 @@ __device__ __forceinline__ void emit_chunk(const SwapParams& p, const float* V, 
       const float u0 = V[(r + 64) * VLD + j], u1 = V[(r + 65) * VLD + j];
       *reinterpret_cast<uint32_t*>(p.out + size_t(t) * p.ldo + mt * 64 + r) =
           pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+    }
+  } else if (p.epi == SW_EPI_ROPE) {
+    // the tile's 128 features are 128 / hd whole heads of the q | k | v
+    // blocks; lane -> rotary pair (i, i + hd/2) at i = 2 lane mod hd/2, so the
+    // warp covers all 64 pairs of the tile for token j.  Same arithmetic as
+    // hp_rope_kv_write on the bf16 projection the unfused GEMM stores.
+    const int half = p.hd / 2;
+    const int pi = 2 * lane;
+    const int hl = pi / half, i = pi % half;
+    const int rlo = hl * p.hd + i, rhi = rlo + half;
+    const int head = (mt * SBM) / p.hd + hl;
+    const bool rot = head < p.Hq + p.Hkv;
+    for (int j = w; j < 32; j += 4) {
+      const int t = nt * BN + c0 + j;
+      if (t >= p.T) break;
+      uint32_t lo = pack_bf16(V[rlo * VLD + j], V[(rlo + 1) * VLD + j]);
+      uint32_t hi = pack_bf16(V[rhi * VLD + j], V[(rhi + 1) * VLD + j]);
+      if (rot) {
+        const float* cs = p.cos_sin + size_t(p.pos[t]) * p.hd;
+        float a0, b0, a1, b1;
+        rope_rotate(bf16lo(lo), bf16lo(hi), cs[i], cs[half + i], a0, b0);
+        rope_rotate(bf16hi(lo), bf16hi(hi), cs[i + 1], cs[half + i + 1], a1, b1);
+        lo = pack_bf16(a0, a1);
+        hi = pack_bf16(b0, b1);
+      }
+      __nv_bfloat16* row = p.out + size_t(t) * p.ldo + size_t(head) * p.hd;
+      *reinterpret_cast<uint32_t*>(row + i) = lo;
+      *reinterpret_cast<uint32_t*>(row + half + i) = hi;
+      if (head >= p.Hq) {
+        const int slot = p.slots[t];
+        const int blk = slot / p.page, off = slot % p.page;
+        const int kvh = rot ? head - p.Hq : head - p.Hq - p.Hkv;
+        __nv_bfloat16* cache = rot ? p.kc : p.vc;
+        *reinterpret_cast<uint32_t*>(cache + kv_cache_index(blk, p.Hkv, kvh, p.page, off, p.hd, i)) = lo;
+        *reinterpret_cast<uint32_t*>(cache + kv_cache_index(blk, p.Hkv, kvh, p.page, off, p.hd, half + i)) = hi;
+      }
     }
   } else if (p.epi == HP_EPI_PEER) {
     // 16-byte stores: thread -> (token j, 8 consecutive features g*8..g*8+7)
@@ -857,9 +903,34 @@ struct PeerArgs {
   int two_shot;
 };
 
+struct RopeArgs {
+  const int* pos;
+  const float* cos_sin;
+  const int* slots;
+  void* kc;
+  void* vc;
+  int page, Hq, Hkv, hd;
+};
+
 static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
                           int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes, int* counters,
-                          int n_counters, int max_ctas, void* stream, const PeerArgs* peer);
+                          int n_counters, int max_ctas, void* stream, const PeerArgs* peer,
+                          const RopeArgs* rope = nullptr);
+
+extern "C" int hp_gemm_swap_qkv_rope(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, int T,
+                                     int Hq, int Hkv, int d, int K, const int* positions, const float* cos_sin,
+                                     const int* slot_mapping, void* kcache, void* vcache, int page, void* workspace,
+                                     size_t ws_bytes, int* counters, int n_counters, int max_ctas, void* stream) {
+  HP_CHECK_ARG(Y && positions && cos_sin && slot_mapping && kcache && vcache, "hp_gemm_swap_qkv_rope: null pointer");
+  HP_CHECK_ARG(d == 64 || d == 128, "hp_gemm_swap_qkv_rope: head_dim must be 64 or 128");
+  HP_CHECK_ARG(Hq >= 1 && Hkv >= 1 && Hq % Hkv == 0, "hp_gemm_swap_qkv_rope: bad head counts");
+  HP_CHECK_ARG(page >= 64 && page % 64 == 0, "hp_gemm_swap_qkv_rope: page must be a multiple of 64");
+  const int N = (Hq + 2 * Hkv) * d;
+  HP_CHECK_ARG(N % 128 == 0 && ldy >= N, "hp_gemm_swap_qkv_rope: (Hq+2Hkv)*d must be a multiple of 128");
+  const RopeArgs ra{positions, cos_sin, slot_mapping, kcache, vcache, page, Hq, Hkv, d};
+  return gemm_swap_impl(X, ldx, W, ldw, Y, ldy, nullptr, 0, T, N, K, SW_EPI_ROPE, workspace, ws_bytes, counters,
+                        n_counters, max_ctas, stream, nullptr, &ra);
+}
 
 extern "C" int hp_gemm_swap(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy,
                             const void* R, int ldr, int T, int N, int K, int epilogue,
@@ -950,7 +1021,7 @@ extern "C" int hp_peer_tiles(int T, int N) {
 
 static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* Y, int ldy, const void* R, int ldr,
                           int T, int N, int K, int epilogue, void* workspace, size_t ws_bytes, int* counters,
-                          int n_counters, int max_ctas, void* stream, const PeerArgs* peer) {
+                          int n_counters, int max_ctas, void* stream, const PeerArgs* peer, const RopeArgs* rope) {
   HP_CHECK_ARG(X && W, "hp_gemm_swap: null pointer");
   HP_CHECK_ARG(T >= 1 && T <= 256, "hp_gemm_swap: token count must be in [1, 256]");
   HP_CHECK_ARG(N % 128 == 0, "hp_gemm_swap: N must be a multiple of 128 (tiled weight layout)");
@@ -992,6 +1063,17 @@ static int gemm_swap_impl(const void* X, int ldx, const void* W, int ldw, void* 
   p.counters = counters;
   p.epi = epilogue;
   p.trace = static_cast<unsigned long long*>(trace_buf(TRACE_SWAP));
+  if (rope) {
+    p.pos = rope->pos;
+    p.cos_sin = rope->cos_sin;
+    p.slots = rope->slots;
+    p.kc = static_cast<__nv_bfloat16*>(rope->kc);
+    p.vc = static_cast<__nv_bfloat16*>(rope->vc);
+    p.page = rope->page;
+    p.Hq = rope->Hq;
+    p.Hkv = rope->Hkv;
+    p.hd = rope->hd;
+  }
   if (peer) {
     for (int q = 0; q < peer->world; ++q) {
       p.peer_out[q] = static_cast<__nv_bfloat16*>(peer->recv[q]);

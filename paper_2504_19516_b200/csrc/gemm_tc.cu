@@ -266,8 +266,7 @@ __device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr
               // unfused GEMM store + hp_rope_kv_write pair does
               const float a = __bfloat162float(__float2bfloat16(x[j + k]));
               const float b = __bfloat162float(__float2bfloat16(y[j + k]));
-              x[j + k] = a * cc[k] - b * ss[k];
-              y[j + k] = b * cc[k] + a * ss[k];
+              rope_rotate(a, b, cc[k], ss[k], x[j + k], y[j + k]);
             }
           }
         }

@@ -73,18 +73,18 @@ __global__ void k_rope_kv_write(__nv_bfloat16* __restrict__ qkv, int ld, int T, 
     const int blk = slot / page, off = slot % page;
     // cache page layout [page/64][d/64][64][64]: each 64-token tile of one
     // kv head is a contiguous 64*d run, 16B chunks swizzled by (token & 7)
-    auto cidx = [&](int kvh, int j) -> size_t {
-      return (((size_t(blk) * Hkv + kvh) * (page / 64) + off / 64) * (d / 64) + j / 64) * 4096 +
-             size_t(off & 63) * 64 + ((((j & 63) >> 3) ^ (off & 7)) << 3) + (j & 7);
-    };
+    auto cidx = [&](int kvh, int j) -> size_t { return kv_cache_index(blk, Hkv, kvh, page, off, d, j); };
     if (head < Hq + Hkv) {
       const float* c = cs + size_t(pos[t]) * d;
       const float c0 = c[i], c1 = c[i + 1], s0 = c[half + i], s1 = c[half + i + 1];
       const uint32_t lo = *reinterpret_cast<const uint32_t*>(row + i);
       const uint32_t hi = *reinterpret_cast<const uint32_t*>(row + half + i);
       const float x0 = bf16lo(lo), x1 = bf16hi(lo), y0 = bf16lo(hi), y1 = bf16hi(hi);
-      const uint32_t nlo = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
-      const uint32_t nhi = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
+      float a0, b0, a1, b1;
+      rope_rotate(x0, y0, c0, s0, a0, b0);
+      rope_rotate(x1, y1, c1, s1, a1, b1);
+      const uint32_t nlo = pack_bf16(a0, a1);
+      const uint32_t nhi = pack_bf16(b0, b1);
       *reinterpret_cast<uint32_t*>(row + i) = nlo;
       *reinterpret_cast<uint32_t*>(row + half + i) = nhi;
       if (head >= Hq) {

@@ -210,7 +210,7 @@ class CoRunner:
     def launches_per_decode_step(self, sms: int) -> int:
         """Kernels in one decode layer-step on `sms` SMs (the CUDA graph's nodes)."""
         m = self.model
-        return 8 + lib.decode_attn_launches(self.B, m.num_heads, m.num_kv_heads, m.head_dim,
+        return 7 + lib.decode_attn_launches(self.B, m.num_heads, m.num_kv_heads, m.head_dim,
                                             self.block_table.shape[1], PAGE, sms)
 
     # --------------------------------------------------------------- timing
@@ -558,6 +558,31 @@ class CoRunner:
         m = self.model
         kv_dim = m.num_kv_heads * m.head_dim
         return self.B * (self.C * 2 * kv_dim * 2 + 2 * kv_dim * 2 + 2 * m.hidden * 2)
+
+    def sm_ingest_gbs(self, sms: int, reps: int = 3) -> float:
+        """Raw HBM -> SM ingest of an `sms`-SM partition: the bulk-copy probe
+        (hp_membw method 1, TMA 1-D copies into a 6 x 32 KB shared-memory
+        ring, nothing read back) over a 1 GiB buffer, GB/s, median of `reps`.
+        The per-SM ceiling any reader that stages through shared memory works
+        under; a staged reader also reads every byte back over the same port
+        (profiles/r02_sm_ingest_probe.txt)."""
+        st = self.pool.phase(DECODE, sms)
+        buf = torch.empty(1 << 30, dtype=torch.uint8, device=self.dev)
+        out = torch.zeros(4, device=self.dev)
+        evs = []
+        with torch.cuda.stream(st.torch_stream):
+            lib.membw(buf, st.sms, 1, out, stream=st.torch_stream)
+            for _ in range(reps):
+                lib.hold(st.torch_stream, 100_000)
+                a, b = _ev(), _ev()
+                a.record(st.torch_stream)
+                lib.membw(buf, st.sms, 1, out, stream=st.torch_stream)
+                b.record(st.torch_stream)
+                evs.append((a, b))
+        torch.cuda.synchronize()
+        t = statistics.median(a.elapsed_time(b) for a, b in evs) * 1e-3
+        del buf
+        return (1 << 30) / t / 1e9
 
     def decode_attn_gbs(self, sms: int, reps: int = 10) -> float:
         """Decode attention alone on `sms` SMs, GB/s algorithmic: `reps`

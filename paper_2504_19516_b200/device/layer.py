@@ -5,7 +5,7 @@ The five device launches per pass are the five kernel groups of the
 reference's layer API (`layer_kernels`, workload.py:162-210), in order:
 
   qkv          rmsnorm + tcgen05 GEMM (prefill: RoPE + paged-KV write fused
-               into the GEMM epilogue; decode: separate rope_kv_write)
+               into the GEMM epilogue, token-major prefill and swap-AB decode alike)
   attn         causal GQA flash attention (prefill) | paged decode attention
   o_proj       tcgen05 GEMM with fused residual add
   mlp_up_gate  rmsnorm + tcgen05 GEMM with fused SiLU(gate) * up
@@ -255,9 +255,8 @@ class DeviceLayer:
         ws, cnt = sc.gemm_ws, sc.gemm_cnt
         qkv = sc.qkv[:B]
         lib.rmsnorm(x, self.W.attn_norm, sc.xn[:B], EPS, sms, stream)
-        lib.gemm_swap(sc.xn[:B], self.W.w_qkv, qkv, ws, cnt, lib.EPI_STORE, max_ctas=sms, stream=stream)
-        lib.rope_kv_write(qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k, cache.v, cache.page,
-                          max_ctas=sms, stream=stream)
+        lib.gemm_swap_qkv_rope(sc.xn[:B], self.W.w_qkv, qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k,
+                               cache.v, cache.page, ws, cnt, max_ctas=sms, stream=stream)
         lib.decode_attn(qkv, cache.k, cache.v, block_table, ctx_lens, sc.attn[:B], Hq, Hkv, d,
                         cache.page, self.scale, ws=sc.attn_ws, max_ctas=sms, stream=stream)
         lib.gemm_swap(sc.attn[:B], self.W.w_o, sc.h[:B], ws, cnt, lib.EPI_RESID, resid=x,
@@ -267,7 +266,7 @@ class DeviceLayer:
                       stream=stream)
         lib.gemm_swap(sc.act[:B], self.W.w_down, y, ws, cnt, lib.EPI_RESID, resid=sc.h[:B],
                       max_ctas=sms, stream=stream)
-        return 8 + lib.decode_attn_launches(B, Hq, Hkv, d, block_table.shape[1], cache.page, sms)
+        return 7 + lib.decode_attn_launches(B, Hq, Hkv, d, block_table.shape[1], cache.page, sms)
 
 
     # --------------------------------------------------------------- hybrid
@@ -303,11 +302,11 @@ class DeviceLayer:
 
         n = 0
         lib.rmsnorm(x, self.W.attn_norm, sc.xn[:T], EPS, sms, stream)
-        if swap:
-            linear(sc.xn[:T], self.W.w_qkv, qkv, lib.EPI_STORE)
-            lib.rope_kv_write(qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k, cache.v, cache.page,
-                              max_ctas=sms, stream=stream)
-            n += 3
+        if swap:  # RoPE + paged K/V write fused into the swap GEMM's epilogue
+            lib.gemm_swap_qkv_rope(sc.xn[:T], self.W.w_qkv, qkv, Hq, Hkv, d, positions, self.rope, slots,
+                                   cache.k, cache.v, cache.page, dsc.gemm_ws, dsc.gemm_cnt, max_ctas=sms,
+                                   stream=stream)
+            n += 2
         else:  # token-major GEMM with RoPE + paged K/V write fused into the epilogue
             lib.gemm_qkv_rope(sc.xn[:T], self.W.w_qkv, qkv, Hq, Hkv, d, positions, self.rope, slots, cache.k,
                               cache.v, cache.page, max_ctas=sms, stream=stream)

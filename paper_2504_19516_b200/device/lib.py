@@ -40,6 +40,8 @@ SIGNATURES = {
     "hp_gemm_qkv_rope": (_i, [_p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i, _p]),
     "hp_gemm_plan": (_i, [_i, _i, _i, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "hp_gemm_swap": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p, _i, _i, _p]),
+    "hp_gemm_swap_qkv_rope": (_i, [_p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i, _p, _sz, _p,
+                                   _i, _i, _p]),
     "hp_gemm_swap_ws_bytes": (_sz, [_i, _i, _i, _i]),
     "hp_peer_tiles": (_i, [_i, _i]),
     "hp_gemm_swap_peer": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, _p, _sz, _i, _i, _i, _p, _i, _p, _sz, _p, _i,
@@ -187,6 +189,19 @@ def gemm_swap(x, w, y, ws, counters, epilogue: int = EPI_STORE, resid=None,
                               epilogue, _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                               _ptr(counters), 0 if counters is None else counters.numel(), max_ctas,
                               _stream(stream)), "hp_gemm_swap")
+
+
+def gemm_swap_qkv_rope(x, w, y, Hq: int, Hkv: int, d: int, positions, cos_sin, slots, kcache, vcache,
+                       page: int, ws, counters, max_ctas: int = 148, stream=None) -> None:
+    """Decode QKV GEMM (T <= 256) with RoPE and the paged K/V write in the
+    epilogue: gemm_swap(..., EPI_STORE) + rope_kv_write in one launch."""
+    T, K = x.shape
+    check(load().hp_gemm_swap_qkv_rope(_ptr(x), x.stride(0), _ptr(w), w.stride(0), _ptr(y), y.stride(0), T, Hq,
+                                       Hkv, d, K, _ptr(positions), _ptr(cos_sin), _ptr(slots), _ptr(kcache),
+                                       _ptr(vcache), page, _ptr(ws),
+                                       0 if ws is None else ws.numel() * ws.element_size(), _ptr(counters),
+                                       0 if counters is None else counters.numel(), max_ctas, _stream(stream)),
+          "hp_gemm_swap_qkv_rope")
 
 
 def peer_tiles(T: int, N: int) -> int:
