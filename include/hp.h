@@ -239,6 +239,9 @@ int hp_set_trace(int kind, void* buf);
  * fix-up workspace is allocated per stream on first use (~21 MB), which
  * must not happen inside a stream capture (the tail is then skipped). */
 int hp_set_gemm_tail(int mode);
+/* Allocate `stream`'s stream-K fix-up workspace now (setup time, outside
+ * any capture) instead of on its first tail GEMM. */
+int hp_gemm_tail_reserve(void* stream);
 
 /* Prefix-aware (chunked) prefill attention over the paged cache
  * (workload.py:176-183 with prior_lens > 0; the attention of a hybrid batch,

@@ -191,14 +191,18 @@ int sk_workspace(cudaStream_t st, SkWorkspace* out) {
   SkWorkspace w{};
   HP_CUDA_TRY(cudaMalloc(&w.ws, size_t(SK_MAX_PAIRS) * SK_SLOT_FLOATS * sizeof(float)));
   HP_CUDA_TRY(cudaMalloc(&w.cnt, size_t(SK_MAX_PAIRS) * 4 * sizeof(int)));
-  HP_CUDA_TRY(cudaMemset(w.cnt, 0, size_t(SK_MAX_PAIRS) * 4 * sizeof(int)));
-  HP_CUDA_TRY(cudaDeviceSynchronize());
+  HP_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, size_t(SK_MAX_PAIRS) * 4 * sizeof(int), st));  // ordered before use
   g_sk.emplace(st, w);
   *out = w;
   return HP_OK;
 }
 
 }  // namespace hp
+
+extern "C" int hp_gemm_tail_reserve(void* stream) {
+  hp::SkWorkspace w{};
+  return hp::sk_workspace(static_cast<cudaStream_t>(stream), &w);
+}
 
 extern "C" int hp_set_gemm_tail(int mode) {
   HP_CHECK_ARG(mode >= -1 && mode <= 1, "hp_set_gemm_tail: mode must be -1, 0 or 1");

@@ -56,6 +56,7 @@ SIGNATURES = {
     "hp_prefill_attn": (_i, [_p, _i, _p, _i, _p, _i, _p, _i, _p, _i, _i, _i, _i, _i, _i, _f, _i, _p]),
     "hp_set_trace": (_i, [_i, _p]),
     "hp_set_gemm_tail": (_i, [_i]),
+    "hp_gemm_tail_reserve": (_i, [_p]),
     "hp_prefill_attn_paged": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _i, _p, _i, _i, _i, _i, _i, _i, _f,
                                    _i, _p]),
     "hp_decode_attn_ws_bytes": (_sz, [_i, _i, _i, _i]),
@@ -371,6 +372,12 @@ def hold(stream, cycles: int) -> None:
 
 def set_trace(kind: int, buf) -> None:
     check(load().hp_set_trace(kind, _ptr(buf)), "hp_set_trace")
+
+
+def gemm_tail_reserve(stream) -> None:
+    """Allocate the stream-K fix-up workspace of `stream` (a torch stream or
+    raw handle) now rather than on its first tail GEMM."""
+    check(load().hp_gemm_tail_reserve(_stream(stream)), "hp_gemm_tail_reserve")
 
 
 def set_gemm_tail(mode: int) -> None:

@@ -69,6 +69,9 @@ class PartitionPool:
         self.granularity = granularity
         self._parts: dict[int, lib.Partition] = {}
         self._full = {PREFILL: torch.cuda.Stream(device=device), DECODE: torch.cuda.Stream(device=device)}
+        # prefill streams get their GEMM stream-K workspace at creation, not
+        # on a first tail GEMM in the middle of a timed / served run
+        lib.gemm_tail_reserve(self._full[PREFILL])
 
     def realizable_decode_sms(self, dm: int) -> int:
         """Round a requested decode share up to the green-context grid."""
@@ -81,6 +84,7 @@ class PartitionPool:
         part = self._parts.get(dm)
         if part is None:
             part = _GridOnlyPartition(dm, self.device, self.n) if self.grid_only else lib.Partition(dm, self.device)
+            lib.gemm_tail_reserve(part.raw_stream(PREFILL))
             self._parts[dm] = part
         return part
 
