@@ -210,6 +210,15 @@ HP_DEVICE void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar, i
       : "memory");
 }
 
+HP_DEVICE void tma_load_2d_pair_hint(void* dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
+                                     uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
 HP_DEVICE void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
                                 uint64_t policy) {
   asm volatile(

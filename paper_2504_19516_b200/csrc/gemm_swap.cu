@@ -32,6 +32,10 @@ namespace hp {
 
 namespace {
 
+#ifndef HP_SWAP_W_EVICT_FIRST
+#define HP_SWAP_W_EVICT_FIRST 1
+#endif
+
 constexpr int SBM = 128;
 constexpr int SBK = 128;  // k per pipeline stage: one contiguous 32 KB weight tile
 constexpr int VLD = 33;  // padded fp32 row of the epilogue transpose buffer
@@ -608,7 +612,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SW_THREADS, 1)
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
               // this CTA's 128 x 128 weight block: one 32 KB run of the tiled layout
               const int wrow = int(wtile_offset((2 * mw + int(rank)) * SBM, 2 * kb, p.K) / 128);
+#if HP_SWAP_W_EVICT_FIRST
+              // weights are read once per step: keep them from displacing a
+              // co-running prefill's L2 working set (as the 1-CTA kernel does)
+              tma_load_2d_pair_hint(sA + stage * C::A_BYTES, &tmW, bar, 0, wrow, l2_policy_evict_first());
+#else
               tma_load_2d_pair(sA + stage * C::A_BYTES, &tmW, bar, 0, wrow);
+#endif
             }
           }
           if (pass == 1 && elect_one()) {
