@@ -57,6 +57,10 @@ struct GemmParams {
   int* sk_cnt;   // [tail tile][rank] arrivals (the finishing CTA resets it)
 };
 
+#ifndef HP_GEMM_A_EVICT_LAST
+#define HP_GEMM_A_EVICT_LAST 0
+#endif
+
 constexpr int BM = 128;
 constexpr int BK = 64;
 
@@ -557,7 +561,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           const uint32_t bar = lfull + 8u * stage;
+#if HP_GEMM_A_EVICT_LAST
+          // activations are re-read by every n-tile of their m-group: ask L2
+          // to keep them over a co-running decode's streams
+          tma_load_2d_pair_hint(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, mt * 2 * BM + int(rank) * BM,
+                                l2_policy_evict_last());
+#else
           tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, mt * 2 * BM + int(rank) * BM);
+#endif
           // weight rows of this CTA's half: one pre-swizzled [128][64] sub-tile
           // of the tiled layout, addressed as rows of a [*, 64] tensor
           const int wrow = int(wtile_offset(nt * BN + int(rank) * (BN / 2), kb, p.K) / 128);
