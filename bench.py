@@ -332,6 +332,11 @@ def hbm_targets(cr, dm: int, hbm_gbs: float, tf_burst: float) -> dict:
     decode side holds at least n_d SMs: decode
     attention GB/s and the four prefill GEMMs' TFLOP/s, measured together."""
     N = cr.n
+    # start from the power state the timed region starts from: right after
+    # seconds of full-GPU co-runs the SM clock sits at the power cap (~1.4
+    # GHz) for ~1 s, and both measurements here scale with it
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     r = cr.corun_hbm(N - dm, dm)
     peak = tf_burst * (N - dm) / N
     r.update(decode_attn_frac_of_hbm=(r["decode_attn_gbs"] or 0.0) / hbm_gbs,
@@ -552,7 +557,12 @@ def main(argv=None) -> int:
     # the prefill layer's five kernel groups + the decode side's windows
     midle = cr.measured_idle(pm, dm, ratio)
 
-    # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N
+    # ---- decode attention roofline (HBM), timed alone on dm SMs and on all N,
+    # after a pause: right after the co-runs above the SM clock is held at the
+    # power cap (~1.4 GHz) for about a second, and a small partition's
+    # decode attention is SM-bound (its GB/s scales with the SM clock)
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     dattn = {f"sms_{k}": cr.decode_attn_gbs(k) for k in sorted({dm, N})}
     ingest = {f"sms_{k}": cr.sm_ingest_gbs(k) for k in sorted({dm, N})}
 
@@ -635,8 +645,10 @@ def main(argv=None) -> int:
                                         "frac_of_sm_ingest": v / ingest[k]} for k, v in dattn.items()},
                                  "sm_ingest_note": "sm_ingest_gbs = the same partition's raw HBM->SM stream "
                                                    "(bulk copies into shared memory, nothing read back; "
-                                                   "hp_membw method 1): the per-SM ceiling below n_d SMs, "
-                                                   "which a staged reader pays twice (copy-in + ldmatrix)"},
+                                                   "hp_membw method 1); a staged reader that reads every "
+                                                   "byte back reaches ~80 % of it (hp_membw_stage), "
+                                                   "decode attention's consumer loop (QK, softmax, PV per "
+                                                   "64-token tile) is what holds it below that"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_tokens / e2e_span, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

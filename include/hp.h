@@ -310,6 +310,16 @@ int hp_membw_ldg(const void* src, size_t bytes, int ctas, int threads, int unrol
  * of each CTA's range, `ldg_warps` warps stream the rest with 128-bit loads. */
 int hp_membw_mix(const void* src, size_t bytes, int ctas, int ldg_warps, int bulk_frac, float* out,
                  void* stream);
+/* Register-direct streaming behind an L2 prefetch: per-CTA contiguous
+ * superchunks of (threads/32) x unroll x 512 bytes; the superchunk `dist`
+ * ahead is prefetched into L2 (cp.async.bulk.prefetch.L2), dist 0 = none. */
+int hp_membw_pfldg(const void* src, size_t bytes, int ctas, int threads, int unroll, int dist,
+                   float* out, void* stream);
+/* Staged reader vs register-direct on one SM: bulk_frac/256 of each CTA's
+ * 16 KB chunks go through a bulk-copy ring read back by `readers` warps
+ * (read_mode 0: released unread), the rest through `ldg_warps` LDG warps. */
+int hp_membw_stage(const void* src, size_t bytes, int ctas, int readers, int ldg_warps, int bulk_frac,
+                   int read_mode, float* out, void* stream);
 /* mma.sync.m16n8k16 (bf16) rate: `chains` independent accumulators per warp,
  * n rounds; out[cta] = cycles. */
 int hp_hmma_rate(int n, int chains, int ctas, int threads, long long* out, void* stream);

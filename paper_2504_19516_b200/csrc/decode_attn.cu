@@ -109,6 +109,13 @@ __device__ __forceinline__ int da_ctx(const DecodeParams& p, int b) {
   return max(0, min(p.ctx_lens[b], p.max_pages * p.page));
 }
 
+#ifdef HP_DA_TRACE
+// development aid: clock64 stamps of CTA 0 (consumers: 6 per tile for their
+// first 16 tiles; producers: empty-wait start/end per half-tile, first 64)
+__device__ long long g_da_trace[12][64][6];
+__device__ long long g_da_utrace[64][4];  // consumer warp 0: unit start, tiles done, merged, end
+#endif
+
 struct UnitId {
   int b, kvh, s, hb;
 };
@@ -132,10 +139,14 @@ __device__ __forceinline__ UnitId unit_of(const DecodeParams& p, int u) {
 // Producers: DA_PRODUCERS warps; warp w owns every slot s with s % P == w
 // and issues the half-tiles h with h % P == w (rs % P == 0), so each slot is
 // refilled by one thread in order and its empty-barrier waits are
-// unambiguous.  One bulk copy per half-tile; several issuing warps because a
-// single thread sustains only ~4 M copies/s.  Each producer keeps the unit's
+// unambiguous.  One bulk copy per half-tile.  Each producer keeps the unit's
 // block-table pages in registers (DA_WREG per lane, fetched one unit ahead)
-// and picks a page with a warp shuffle.
+// and resolves 32 of its positions at a time, one per lane (tile, K/V, page
+// by warp shuffle); the serial part per copy is then one empty-barrier wait
+// and one issue.  Resolving each position just before its copy (~420 of the
+// ~800 cycles per copy, clock64 trace tools/da_trace.py) capped the ring at
+// 124 GB/s per SM even without the math; batched, 142 (HP_DA_NOCOMPUTE) and
+// 109.5 with it at 8 SMs (was 98).
 //
 // Consumers: DA_CONSUMERS warps take the unit's tiles round-robin.  The K
 // slot is released as soon as the scores are in registers, the V slot after
@@ -180,7 +191,11 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     // ------------------------------------------------------------ producers
     const int pw = warp - DA_CONSUMERS;
     // KV is read once per step -- unless sibling head blocks re-read it from L2
+#ifdef HP_DA_NOHINT
+    const uint64_t pol = l2_policy_evict_last();
+#else
     const uint64_t pol = p.HB > 1 ? l2_policy_evict_last() : l2_policy_evict_first();
+#endif
     int win[DA_WREG], winn[DA_WREG];
     auto fetch = [&](int u, int (&w)[DA_WREG]) -> int {  // returns ctx of unit u
       const UnitId id = unit_of(p, u);
@@ -205,29 +220,49 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
       const int t1 = min(ntiles, t0 + p.tps);
       const int nh = 2 * max(0, t1 - t0);
       const int first = t0 / page_tiles;
-      for (int hh = (pw - int(hbase % DA_PRODUCERS) + DA_PRODUCERS) % DA_PRODUCERS; hh < nh;
-           hh += DA_PRODUCERS) {
-        const int t = t0 + (hh >> 1);
-        const int pr = t / page_tiles - first;
-        // register select in opaque selp's (a plain select chain becomes an
-        // indexed local-memory load of the whole window)
-        int sel = win[0];
-        const int wi = pr >> 5;
-#pragma unroll
-        for (int r = 1; r < DA_WREG; ++r)
-          asm("{\n .reg .pred p;\n setp.eq.s32 p, %2, %3;\n selp.b32 %0, %1, %0, p;\n}"
-              : "+r"(sel) : "r"(win[r]), "r"(wi), "r"(r));
-        const int blk = __shfl_sync(0xffffffffu, sel, pr & 31);
-        const uint32_t h = hbase + hh;
-        const int st = int(h % RS);
-        mbar_wait(&empty[st], ((h / RS) & 1) ^ 1);
-        if (lane == 0) {
-          const size_t tile = ((size_t(blk) * p.Hkv + id.kvh) * page_tiles + (t % page_tiles)) * HS;
-          mbar_arrive_expect_tx(&full[st], HS);
-          bulk_load_hint(ring + size_t(st) * HS, ((hh & 1) ? p.vc : p.kc) + tile, HS, &full[st], pol);
-          st_volatile_shared(tag + 4u * st, h);
+      // Positions hh = pw', pw' + P, ... of this unit (pw' = this warp's
+      // residue), 32 at a time: lane j resolves position hb + P*j (tile,
+      // K/V, page via the lane-distributed window) up front, then the warp
+      // walks the batch -- wait for the slot, lane j issues its copy -- so
+      // the serial part per copy is one barrier wait and one issue.
+      for (int hb = (pw - int(hbase % DA_PRODUCERS) + DA_PRODUCERS) % DA_PRODUCERS; hb < nh;
+           hb += 32 * DA_PRODUCERS) {
+        const int hh_l = hb + DA_PRODUCERS * lane;
+        int kv_l = 0, t_l = t0, pr_l = 0;
+        if (hh_l < nh) {
+          t_l = t0 + (hh_l >> 1);  // half-tile 2t: K of tile t, 2t + 1: its V
+          kv_l = hh_l & 1;
+          pr_l = t_l / page_tiles - first;
         }
-        __syncwarp();
+        int blk_l = 0;
+#pragma unroll
+        for (int r = 0; r < DA_WREG; ++r) {
+          const int v = __shfl_sync(0xffffffffu, win[r], pr_l & 31);
+          if ((pr_l >> 5) == r) blk_l = v;
+        }
+        const uint8_t* src_l = (kv_l ? p.vc : p.kc) +
+                               ((size_t(blk_l) * p.Hkv + id.kvh) * page_tiles + (t_l % page_tiles)) * HS;
+        const int cnt = min(32, (nh - hb + DA_PRODUCERS - 1) / DA_PRODUCERS);
+        for (int j = 0; j < cnt; ++j) {
+          const uint32_t h = hbase + hb + DA_PRODUCERS * j;
+          const int st = int(h % RS);
+#ifdef HP_DA_TRACE
+          const long long tw0 = clock64();
+#endif
+          mbar_wait(&empty[st], ((h / RS) & 1) ^ 1);
+#ifdef HP_DA_TRACE
+          if (blockIdx.x == 0 && lane == 0 && j < 64 && hb < DA_PRODUCERS && u == int(blockIdx.x + 2 * gridDim.x)) {
+            g_da_trace[8 + pw][j][0] = tw0;
+            g_da_trace[8 + pw][j][1] = clock64();
+          }
+#endif
+          if (lane == j) {
+            mbar_arrive_expect_tx(&full[st], HS);
+            bulk_load_hint(ring + size_t(st) * HS, src_l, HS, &full[st], pol);
+            st_volatile_shared(tag + 4u * st, h);
+          }
+          __syncwarp();
+        }
       }
       hbase += nh;
       ctx_cur = ctx_nxt;
@@ -265,7 +300,12 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   };
   auto acquire = [&](uint32_t h) -> uint32_t {
     const int st = int(h % RS);
-    while (ld_volatile_shared(tag + 4u * st) != h) __nanosleep(20);
+#ifndef HP_DA_SPIN_NS
+#define HP_DA_SPIN_NS 20
+#endif
+    while (ld_volatile_shared(tag + 4u * st) != h) {
+      if (HP_DA_SPIN_NS > 0) __nanosleep(HP_DA_SPIN_NS);
+    }
     mbar_wait(&full[st], (h / RS) & 1);
     return uint32_t(st);
   };
@@ -283,6 +323,11 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     const int ntiles = (ctx + DA_TILE - 1) / DA_TILE;
     const int t0 = id.s * p.tps;
     const int t1 = min(ntiles, t0 + p.tps);
+#ifdef HP_DA_TRACE
+    const int uix = (u - int(blockIdx.x)) / int(gridDim.x);
+    const bool utr = blockIdx.x == 0 && threadIdx.x == 0 && uix < 64;
+    if (utr) g_da_utrace[uix][0] = clock64();
+#endif
     if (t0 < t1) {
       const int nt = t1 - t0;
       float o[NB][KK][4];
@@ -297,19 +342,28 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
 
       for (int i = warp; i < nt; i += DA_CONSUMERS) {
         const uint32_t hk = hbase + 2 * i;
+        const uint32_t hv = hk + 1;
 #ifdef HP_DA_NOCOMPUTE  // experiment: stream the ring without the math
         {
           const uint32_t a = acquire(hk);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[a]);
-          const uint32_t b = acquire(hk + 1);
+          const uint32_t b = acquire(hv);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[b]);
           continue;
         }
 #endif
         // ---- S^T = K . Q^T : four independent 16-token m tiles per column block
+#ifdef HP_DA_TRACE
+        const bool trc = blockIdx.x == 0 && lane == 0 && i / DA_CONSUMERS < 64 && u == int(blockIdx.x + 2 * gridDim.x);
+        long long* tr = g_da_trace[warp][min(63, i / DA_CONSUMERS)];
+        if (trc) tr[0] = clock64();
+#endif
         const uint32_t sk = acquire(hk);
+#ifdef HP_DA_TRACE
+        if (trc) tr[1] = clock64();
+#endif
         const uint32_t kb = smem_u32(ring + size_t(sk) * HS);
         float sc[NB][4][4];
 #pragma unroll
@@ -330,6 +384,9 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sk]);  // K tile consumed
+#ifdef HP_DA_TRACE
+        if (trc) tr[2] = clock64();
+#endif
         // ---- mask, scale, online softmax
         const int tokbase = (t0 + i) * DA_TILE;
 #pragma unroll
@@ -390,7 +447,13 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
             pf[nb][kt][0] = *reinterpret_cast<const uint32_t*>(pr);
             pf[nb][kt][1] = *reinterpret_cast<const uint32_t*>(pr + 8);
           }
-        const uint32_t sv = acquire(hk + 1);
+#ifdef HP_DA_TRACE
+        if (trc) tr[3] = clock64();
+#endif
+        const uint32_t sv = acquire(hv);
+#ifdef HP_DA_TRACE
+        if (trc) tr[4] = clock64();
+#endif
         const uint32_t vb = smem_u32(ring + size_t(sv) * HS);
 #pragma unroll
         for (int kt = 0; kt < 4; ++kt) {
@@ -406,6 +469,9 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[sv]);  // V tile consumed
+#ifdef HP_DA_TRACE
+        if (trc) tr[5] = clock64();
+#endif
       }
       // ---- merge the consumer warps' (m, l, O) for the Gb live heads
       const int G = p.Gb;
@@ -440,6 +506,9 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           }
         }
       }
+#ifdef HP_DA_TRACE
+      if (utr) g_da_utrace[uix][1] = clock64();
+#endif
       named_bar_sync(1, DA_CONSUMERS * 32);
       const int nsplit = (ntiles + p.tps - 1) / p.tps;
       const int nw = min(DA_CONSUMERS, nt);  // warps that saw at least one tile
@@ -476,7 +545,13 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           }
         }
       }
+#ifdef HP_DA_TRACE
+      if (utr) g_da_utrace[uix][2] = clock64();
+#endif
       named_bar_sync(1, DA_CONSUMERS * 32);
+#ifdef HP_DA_TRACE
+      if (utr) g_da_utrace[uix][3] = clock64();
+#endif
       hbase += 2 * nt;
     }
 #pragma unroll
@@ -547,6 +622,13 @@ static int launch_decode(DecodeParams& p, int max_ctas, cudaStream_t st) {
 }  // namespace hp
 
 using namespace hp;
+
+#ifdef HP_DA_TRACE
+extern "C" int hp_da_trace_read(long long* host) {
+  if (cudaMemcpyFromSymbol(host + sizeof(g_da_trace) / 8, g_da_utrace, sizeof(g_da_utrace)) != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(host, g_da_trace, sizeof(g_da_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" size_t hp_decode_attn_ws_bytes(int B, int Hq, int d, int max_splits) {
   return size_t(B) * Hq * max_splits * (d + 2) * sizeof(float);

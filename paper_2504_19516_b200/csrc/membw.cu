@@ -80,6 +80,139 @@ __global__ void k_membw_ldg2(const uint4* __restrict__ src, size_t n16, float* _
   if (acc == 0x12345678u) out[0] = 1.f;
 }
 
+// Register-direct streaming with the HBM latency taken off the SM: each CTA
+// walks a contiguous range in superchunks of nw x U x 512 bytes (warp w
+// takes its U x 512-byte slice of every superchunk); lane 0 of warp 0 issues
+// cp.async.bulk.prefetch.L2 for the superchunk `dist` ahead, so the LDGs hit
+// L2 and the registers in flight only cover the L2 latency.  Question: can a
+// reader that never stages through shared memory (one crossing of the L1TEX
+// data path per byte instead of two) ingest more than the staged reader's
+// ~105-115 GB/s per SM on a small partition?
+template <int U>
+__global__ void k_membw_pfldg(const uint8_t* __restrict__ src, size_t bytes, int dist,
+                              float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const size_t sc = size_t(nw) * U * 512;  // superchunk bytes
+  const size_t nsc = bytes / sc;
+  const size_t per = (nsc + gridDim.x - 1) / gridDim.x;
+  const size_t k0 = blockIdx.x * per;
+  const size_t k1 = std::min(nsc, k0 + per);
+  uint32_t acc = 0;
+  auto pf = [&](size_t k) {
+    if (dist > 0 && w == 0 && lane == 0 && k < k1)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + k * sc), "r"(uint32_t(sc))
+                   : "memory");
+  };
+  for (int d = 0; d < dist; ++d) pf(k0 + d);
+  uint4 v[U], nv[U];
+  auto ld = [&](size_t k, uint4 (&d)[U]) {
+    const uint4* b = reinterpret_cast<const uint4*>(src + k * sc + size_t(w) * U * 512);
+#pragma unroll
+    for (int j = 0; j < U; ++j) d[j] = ldg_na(b + j * 32 + lane);
+  };
+  if (k0 < k1) ld(k0, v);
+  for (size_t k = k0; k < k1; ++k) {
+    pf(k + dist);
+    if (k + 1 < k1) ld(k + 1, nv);
+#pragma unroll
+    for (int j = 0; j < U; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = nv[j];
+  }
+  if (acc == 0x12345678u) out[0] = 1.f;
+}
+
+// Staged reader with consumers vs register-direct, on one SM: warp 0 bulk-
+// copies the CTA's first `bulk_frac`/256 of its 16 KB chunks into an 8-slot
+// ring; `readers` warps read every staged byte back (ld.shared.v4, a chunk
+// split across them; read_mode 0 = no read-back) and release the slot; the
+// remaining `ldg_warps` warps stream the rest with U = 8 pipelined LDGs.
+// Question: do shared-memory reads, bulk-copy writes and LDG returns share
+// one per-SM data port (then a staged byte costs two of its slots, a
+// register-direct byte one)?
+__global__ void __launch_bounds__(640, 1) k_membw_stage(const uint8_t* __restrict__ src, size_t bytes,
+                                                         int bulk_frac, int readers, int read_mode,
+                                                         float* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  constexpr uint32_t CH = 16 * 1024;
+  constexpr int NST = 12;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * CH);
+  uint64_t* empty = full + NST;
+  // a reader can reach a slot more than one phase ahead of the producer: it
+  // first waits until the slot's tag names its chunk (as k_decode_attn does)
+  const uint32_t tag = smem_u32(empty + NST);
+  const size_t nch = bytes / CH;
+  const size_t per = (nch + gridDim.x - 1) / gridDim.x;
+  const size_t c0 = blockIdx.x * per;
+  const size_t my = c0 >= nch ? 0 : std::min(per, nch - c0);
+  const size_t nb = my * size_t(bulk_frac) / 256;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t acc = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      st_volatile_shared(tag + 4u * s, 0xffffffffu);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0)
+      for (size_t k = 0; k < nb; ++k) {
+        const int s = int(k % NST);
+        if (readers > 0) mbar_wait(&empty[s], uint32_t(((k / NST) & 1) ^ 1));
+        else if (k >= NST) mbar_wait(&full[s], uint32_t(((k / NST) - 1) & 1));
+        mbar_arrive_expect_tx(&full[s], CH);
+        bulk_load(base + size_t(s) * CH, src + (c0 + k) * CH, CH, &full[s]);
+        st_volatile_shared(tag + 4u * s, uint32_t(k));
+      }
+  } else if (warp <= readers) {
+    // reader r takes chunks r, r + readers, ... (a whole 16 KB chunk each)
+    const int r = warp - 1;
+    for (size_t k = r; k < nb; k += readers) {
+      const int s = int(k % NST);
+      while (ld_volatile_shared(tag + 4u * s) != uint32_t(k)) {
+      }
+      mbar_wait(&full[s], uint32_t((k / NST) & 1));
+      if (read_mode) {
+        const uint4* b4 = reinterpret_cast<const uint4*>(base + size_t(s) * CH);
+#pragma unroll 8
+        for (int i = lane; i < int(CH / 16); i += 32) {
+          const uint4 v = b4[i];
+          acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  } else {
+    constexpr int U = 8;
+    const int w = warp - 1 - readers, nw = (blockDim.x >> 5) - 1 - readers;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + (c0 + nb) * CH);
+    const size_t n16 = (my - nb) * (CH / 16);
+    const size_t chunk = U * 32;
+    const size_t nc = n16 / chunk;
+    uint4 v[U], nv[U];
+    size_t c = w;
+    auto ld = [&](size_t cc, uint4 (&d)[U]) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) d[j] = ldg_na(s4 + cc * chunk + j * 32 + lane);
+    };
+    if (c < nc) ld(c, v);
+    for (; c < nc; c += nw) {
+      if (c + nw < nc) ld(c + nw, nv);
+#pragma unroll
+      for (int j = 0; j < U; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = nv[j];
+    }
+  }
+  if (acc == 0x12345678u) out[0] = 1.f;
+}
+
 // Legacy warp-level MMA rate (mma.sync.m16n8k16 bf16 -> fp32, HMMA.16816):
 // every warp issues n x C independent MMAs; out[cta] = cycles.  Tells whether
 // a register-fed decode GEMM could keep up with ~200 GB/s per SM of weights
@@ -663,5 +796,37 @@ extern "C" int hp_hmma_rate(int n, int chains, int ctas, int threads, long long*
   if (chains == 4) k_hmma_rate<4><<<ctas, threads, 0, st>>>(n, out);
   if (chains == 8) k_hmma_rate<8><<<ctas, threads, 0, st>>>(n, out);
   HP_LAUNCH_CHECK("k_hmma_rate");
+  return HP_OK;
+}
+
+extern "C" int hp_membw_pfldg(const void* src, size_t bytes, int ctas, int threads, int unroll, int dist,
+                              float* out, void* stream) {
+  HP_CHECK_ARG(src && out && ctas >= 1 && threads >= 32 && threads <= 1024 && threads % 32 == 0 && dist >= 0 &&
+                   (unroll == 2 || unroll == 4 || unroll == 8),
+               "hp_membw_pfldg: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  if (unroll == 2) k_membw_pfldg<2><<<ctas, threads, 0, st>>>(s, bytes, dist, out);
+  if (unroll == 4) k_membw_pfldg<4><<<ctas, threads, 0, st>>>(s, bytes, dist, out);
+  if (unroll == 8) k_membw_pfldg<8><<<ctas, threads, 0, st>>>(s, bytes, dist, out);
+  HP_LAUNCH_CHECK("k_membw_pfldg");
+  return HP_OK;
+}
+
+extern "C" int hp_membw_stage(const void* src, size_t bytes, int ctas, int readers, int ldg_warps, int bulk_frac,
+                              int read_mode, float* out, void* stream) {
+  HP_CHECK_ARG(src && out && ctas >= 1 && readers >= 0 && ldg_warps >= 0 && 1 + readers + ldg_warps <= 20 &&
+                   bulk_frac >= 0 && bulk_frac <= 256 && (bulk_frac == 0 || readers >= 1) &&
+                   (bulk_frac == 256 || ldg_warps >= 1) && bytes % (16 * 1024) == 0,
+               "hp_membw_stage: bad arguments");
+  const size_t smem = 12 * 16 * 1024 + 128 + 2 * 12 * 8 + 12 * 4;
+  static bool attr = false;
+  if (!attr) {
+    HP_CUDA_TRY(cudaFuncSetAttribute(k_membw_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  k_membw_stage<<<ctas, 32 * (1 + readers + ldg_warps), smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), bytes, bulk_frac, readers, read_mode, out);
+  HP_LAUNCH_CHECK("k_membw_stage");
   return HP_OK;
 }

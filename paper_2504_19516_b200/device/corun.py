@@ -564,8 +564,8 @@ class CoRunner:
         (hp_membw method 1, TMA 1-D copies into a 6 x 32 KB shared-memory
         ring, nothing read back) over a 1 GiB buffer, GB/s, median of `reps`.
         The per-SM ceiling any reader that stages through shared memory works
-        under; a staged reader also reads every byte back over the same port
-        (profiles/r02_sm_ingest_probe.txt)."""
+        under; one that also reads every byte back (ld.shared, 8 reader
+        warps) keeps ~80 % of it (hp_membw_stage, profiles/r02_decode_ingest.md)."""
         st = self.pool.phase(DECODE, sms)
         buf = torch.empty(1 << 30, dtype=torch.uint8, device=self.dev)
         out = torch.zeros(4, device=self.dev)

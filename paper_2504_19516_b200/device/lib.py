@@ -68,6 +68,8 @@ SIGNATURES = {
     "hp_membw2d": (_i, [_p, _i, _i, _i, _i, _p, _p]),
     "hp_membw_pipe": (_i, [_p, _sz, _i, _i, _i, _p, _p]),
     "hp_membw_ldg": (_i, [_p, _sz, _i, _i, _i, _i, _p, _p]),
+    "hp_membw_pfldg": (_i, [_p, _sz, _i, _i, _i, _i, _p, _p]),
+    "hp_membw_stage": (_i, [_p, _sz, _i, _i, _i, _i, _i, _p, _p]),
     "hp_hmma_rate": (_i, [_i, _i, _i, _i, _p, _p]),
     "hp_membw_mix": (_i, [_p, _sz, _i, _i, _i, _p, _p]),
     "hp_umma2_rate": (_i, [_i, _i, _i, _p, _p]),

@@ -5,6 +5,7 @@ the full GPU; caches sized above L2 so back-to-back launches stream HBM.
 """
 import json
 import math
+import os
 import sys
 
 import torch
@@ -22,15 +23,35 @@ def run(Hq, Hkv, d, B, ctx, sms=148, reps=10):
     nblk = B * pages
     kc = torch.randn(nblk, Hkv, 64, d, dtype=torch.bfloat16, device=dev)
     vc = torch.randn_like(kc)
-    bt = torch.randperm(nblk, device=dev).to(torch.int32).view(B, pages)
+    if os.environ.get("DA_SEQ"):  # measurement: pages laid out in order
+        bt = torch.arange(nblk, device=dev).to(torch.int32).view(B, pages)
+    else:
+        bt = torch.randperm(nblk, device=dev).to(torch.int32).view(B, pages)
     cl = torch.full((B,), ctx, dtype=torch.int32, device=dev)
     q = torch.randn(B, Hq * d, dtype=torch.bfloat16, device=dev)
     o = torch.empty_like(q)
     ws = torch.empty(lib.decode_attn_ws_bytes(B, Hq, d, 64) // 4 + 1, dtype=torch.float32, device=dev)
 
-    def go():
-        lib.decode_attn(q, kc, vc, bt, cl, o, Hq, Hkv, d, 64, 1 / math.sqrt(d), ws=ws, max_ctas=sms)
+    stream = None
+    if os.environ.get("DA_GREEN"):  # measurement: inside a green context of `sms` SMs
+        from paper_2504_19516_b200.device.partition import DECODE, PartitionPool
+        global _POOL
+        if "_POOL" not in globals():
+            _POOL = PartitionPool(0)
+        st = _POOL.phase(DECODE, sms)
+        stream = st.torch_stream
 
+    def go():
+        lib.decode_attn(q, kc, vc, bt, cl, o, Hq, Hkv, d, 64, 1 / math.sqrt(d), ws=ws, max_ctas=sms,
+                        stream=stream)
+
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return _timed(go, reps, B, ctx, Hkv, d, Hq)
+    return _timed(go, reps, B, ctx, Hkv, d, Hq)
+
+
+def _timed(go, reps, B, ctx, Hkv, d, Hq):
     go()
     ts = []
     for _ in range(3):
