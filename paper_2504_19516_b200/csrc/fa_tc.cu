@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
 #pragma unroll
           for (int t = 0; t < 2; ++t)
             if (n[t] > 0) qk(t, ks);
+          if (J == 1) umma_commit(q_empty);  // the prologue's QKs were the unit's last
         }
         for (int j = 0; j < J; ++j) {
           const uint32_t vs = (vt + j) % VST;
@@ -388,7 +389,10 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
           }
           umma_commit(&v_empty[vs]);
           umma_commit(&k_empty[ks_cur]);  // K_j: read by QK(j) of both tiles, all issued
-          if (j == J - 1) umma_commit(q_empty);
+          // Q is read only by QK: free it once the unit's last QK is issued
+          // (j = J - 2), so the producer loads the next unit's Q while this
+          // unit's last PV / softmax / epilogue run, not after them
+          if (j == J - 2) umma_commit(q_empty);
         }
         kt += J;
         vt += J;
@@ -731,6 +735,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FAP_THREADS, 1)
 #pragma unroll
             for (int t = 0; t < 2; ++t)
               if (n[t] > 0) qk(t, ks);
+            if (J == 1) umma_commit_pair(q_empty);
           }
           for (int j = 0; j < J; ++j) {
             const uint32_t vs = (vt + j) % FAP_VST;
@@ -759,7 +764,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FAP_THREADS, 1)
             }
             umma_commit_pair(&v_empty[vs]);
             umma_commit_pair(&k_empty[ks_cur]);
-            if (j == J - 1) umma_commit_pair(q_empty);
+            if (j == J - 2) umma_commit_pair(q_empty);  // last QK issued (see k_fa2)
           }
           kt += J;
           vt += J;

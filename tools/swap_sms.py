@@ -1,5 +1,9 @@
 """Decode (swap-AB stream-K) GEMM GB/s of weights when confined to `sms`
-CTAs, llama3-8b decode batch 32 shapes, L2 flushed.   python tools/swap_sms.py [sms ...]"""
+CTAs, llama3-8b decode batch 32 shapes, L2 flushed.   python tools/swap_sms.py [sms ...]
+SW_GREEN=1: inside a green context of `sms` SMs (the co-run's condition: both
+SMs of a TPC busy) instead of `sms` CTAs on an otherwise idle GPU."""
+import contextlib
+import os
 import sys
 
 import torch
@@ -12,7 +16,13 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 T = 32
 shapes = [("qkv", 6144, 4096, lib.EPI_STORE), ("o_proj", 4096, 4096, lib.EPI_RESID),
           ("up_gate", 28672, 4096, lib.EPI_SILU), ("down", 4096, 14336, lib.EPI_RESID)]
+pool = None
+if os.environ.get("SW_GREEN"):
+    from paper_2504_19516_b200.device.partition import DECODE, PartitionPool
+    pool = PartitionPool(0)
 for sms in [int(a) for a in sys.argv[1:]] or [8, 16, 148]:
+    ctx = torch.cuda.stream(pool.phase(DECODE, sms).torch_stream) if pool else contextlib.nullcontext()
+    ctx.__enter__()
     tot_b, tot_t = 0, 0.0
     for name, N, K, epi in shapes:
         x = torch.randn(T, K, device=dev).to(torch.bfloat16)
@@ -26,7 +36,8 @@ for sms in [int(a) for a in sys.argv[1:]] or [8, 16, 148]:
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            lib.gemm_swap(x, w, y, ws, cnt, epi, resid=r if epi == lib.EPI_RESID else None, max_ctas=sms)
+            lib.gemm_swap(x, w, y, ws, cnt, epi, resid=r if epi == lib.EPI_RESID else None, max_ctas=sms,
+                          stream=torch.cuda.current_stream())
             b.record()
             torch.cuda.synchronize()
             if i >= 2:
@@ -38,3 +49,4 @@ for sms in [int(a) for a in sys.argv[1:]] or [8, 16, 148]:
         print(f"sms {sms:4d} {name:8s} {t * 1e6:8.1f} us {nb / t / 1e9:7.1f} GB/s {nb / t / 1e9 / sms:6.1f} GB/s/SM",
               flush=True)
     print(f"sms {sms:4d} all      {tot_t * 1e6:8.1f} us {tot_b / tot_t / 1e9:7.1f} GB/s {tot_b / tot_t / 1e9 / sms:6.1f} GB/s/SM")
+    ctx.__exit__(None, None, None)
