@@ -331,6 +331,8 @@ def hbm_targets(cr, dm: int, hbm_gbs: float, tf_burst: float) -> dict:
     """Both north-star roofline targets at one co-executed split where the
     decode side holds at least n_d SMs: decode
     attention GB/s and the four prefill GEMMs' TFLOP/s, measured together."""
+    import torch
+
     N = cr.n
     # start from the power state the timed region starts from: right after
     # seconds of full-GPU co-runs the SM clock sits at the power cap (~1.4
