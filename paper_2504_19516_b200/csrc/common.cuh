@@ -422,6 +422,14 @@ HP_DEVICE void mma_bf16_16816(float* d, const uint32_t* a, const uint32_t* b) {
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+// Transpose of an 8x8 b16 matrix across the warp: lane l holds row l/4,
+// columns 2(l%4), 2(l%4)+1 before and after (mma fragment layout).
+HP_DEVICE uint32_t movmatrix_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 HP_DEVICE uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -47,7 +47,6 @@ constexpr int DA_CONSUMERS = 8;
 constexpr int DA_PRODUCERS = HP_DA_PRODUCERS;         // issuing warps (one copy stream each)
 constexpr int DA_THREADS = (DA_CONSUMERS + DA_PRODUCERS) * 32;
 constexpr uint32_t DA_BOX_BYTES = DA_TILE * 64 * 2;   // 64 rows x 128 B
-constexpr int DA_PROW = 72;                           // padded P^T row (bf16)
 constexpr int DA_WREG = 8;                            // block-table window regs per lane
 constexpr int DA_WIN = 32 * DA_WREG;                  // window: pages per unit
 constexpr int DA_MAX_RS = 32;                         // ring slots (tags array size)
@@ -65,7 +64,7 @@ struct DaPlan {
 // G = heads per unit (Gb), NB = 8-head column blocks (1 or 2)
 inline size_t da_fixed_bytes(int D, int G, int NB) {
   const int cb = G * D + 16 * NB;
-  return 1024 + size_t(DA_CONSUMERS) * cb * 4 + size_t(DA_CONSUMERS) * NB * 8 * DA_PROW * 2 +
+  return 1024 + size_t(DA_CONSUMERS) * cb * 4 +
          2 * DA_MAX_RS * 8 + DA_MAX_RS * 4 + 64;
 }
 
@@ -162,8 +161,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* cbuf = reinterpret_cast<float*>(ring + size_t(RS) * HS);
-  __nv_bfloat16* pbuf = reinterpret_cast<__nv_bfloat16*>(cbuf + DA_CONSUMERS * CB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + DA_CONSUMERS * NB * 8 * DA_PROW);
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + DA_CONSUMERS * CB);
   uint64_t* empty = full + DA_MAX_RS;
   // Consumers can reach a slot more than one phase ahead of its producer
   // (8 warps round-robin over the ring), where a parity wait would be
@@ -276,7 +274,6 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   const int g8 = lane >> 2;  // MMA group id
   const int t4 = lane & 3;   // thread in group
   const int mat = lane >> 3;
-  __nv_bfloat16* pw = pbuf + warp * NB * 8 * DA_PROW;
   float* cw = cbuf + warp * CB;
   uint32_t hbase = 0;
 
@@ -341,6 +338,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
       }
 
       for (int i = warp; i < nt; i += DA_CONSUMERS) {
+        uint32_t pf[NB][4][2];  // P^T B fragments of the PV MMA (per 16-token k-step)
         const uint32_t hk = hbase + 2 * i;
         const uint32_t hv = hk + 1;
 #ifdef HP_DA_NOCOMPUTE  // experiment: stream the ring without the math
@@ -414,14 +412,20 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
           m1[nb] = n1;
           l0[nb] *= a0;
           l1[nb] *= a1;
+          // most tiles leave every row max unchanged (a == 1 exactly): skip
+          if (__any_sync(0xffffffffu, (a0 != 1.f) || (a1 != 1.f))) {
 #pragma unroll
-          for (int dm = 0; dm < KK; ++dm) {
-            o[nb][dm][0] *= a0;
-            o[nb][dm][2] *= a0;
-            o[nb][dm][1] *= a1;
-            o[nb][dm][3] *= a1;
+            for (int dm = 0; dm < KK; ++dm) {
+              o[nb][dm][0] *= a0;
+              o[nb][dm][2] *= a0;
+              o[nb][dm][1] *= a1;
+              o[nb][dm][3] *= a1;
+            }
           }
-          __nv_bfloat16* pwb = pw + nb * 8 * DA_PROW;
+          // P^T as the PV MMA's B fragments, transposed in registers: the
+          // lane's packed (token g8 [+8], heads 2t4, 2t4+1) pair is its
+          // fragment of the 8x8 matrix [token][head]; movmatrix.trans hands
+          // it (head g8, tokens 2t4, 2t4+1) -- b0 (tokens 0-7) / b1 (8-15)
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) {
 #pragma unroll
@@ -430,23 +434,11 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
               const float p1 = exp2f(sc[nb][mt][2 * h + 1] - n1);
               l0[nb] += p0;
               l1[nb] += p1;
-              const int tok = mt * 16 + g8 + h * 8;
-              pwb[(2 * t4) * DA_PROW + tok] = __float2bfloat16(p0);
-              pwb[(2 * t4 + 1) * DA_PROW + tok] = __float2bfloat16(p1);
+              pf[nb][mt][h] = movmatrix_trans(pack_bf16(p0, p1));
             }
           }
         }
-        __syncwarp();
         // ---- O^T += V^T . P^T
-        uint32_t pf[NB][4][2];
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-          for (int kt = 0; kt < 4; ++kt) {
-            const __nv_bfloat16* pr = pw + (nb * 8 + g8) * DA_PROW + kt * 16 + 2 * t4;
-            pf[nb][kt][0] = *reinterpret_cast<const uint32_t*>(pr);
-            pf[nb][kt][1] = *reinterpret_cast<const uint32_t*>(pr + 8);
-          }
 #ifdef HP_DA_TRACE
         if (trc) tr[3] = clock64();
 #endif
