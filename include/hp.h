@@ -222,7 +222,7 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
                     void* stream);
 
 /* Kernel timeline traces.  kind 0: k_fa2 CTA 0 softmax/MMA wait stamps
- * (clock64, int64 [12][256]); kind 1: k_gemm_swap_sk per-CTA globaltimer
+ * (clock64, int64 [18][256]: rows 0-11 per KV step, 12-17 per unit); kind 1: k_gemm_swap_sk per-CTA globaltimer
  * stamps (uint64 [grid][6]: entry, prologue done, producer done, MMA done,
  * epilogue done, exit); kind 2 (one-shot, SM-idle measurement of config 2/3):
  * the NEXT hp_gemm / hp_gemm_qkv_rope / hp_prefill_attn(_paged) launch on

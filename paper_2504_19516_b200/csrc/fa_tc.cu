@@ -348,7 +348,10 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
         if (!unit2_of<PAGED>(p, u, x)) continue;
         const int n[2] = {x.nA, x.nB};
         const int J = max(x.nA, x.nB);
+        const bool utr = p.trace && blockIdx.x == 0 && un < 256;
+        if (utr) p.trace[16 * 256 + un] = clock64();
         mbar_wait(q_full, un & 1);
+        if (utr) p.trace[12 * 256 + un] = clock64();
         // prologue: S(0) for both tiles
         {
           const int ks = kt % KST;
@@ -394,6 +397,7 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
           // unit's last PV / softmax / epilogue run, not after them
           if (j == J - 2) umma_commit(q_empty);
         }
+        if (utr) p.trace[13 * 256 + un] = clock64();
         kt += J;
         vt += J;
         ++un;
@@ -503,7 +507,10 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
         if (lane == 0) mbar_arrive(&p_full[t]);
       }
       // epilogue: O / l -> global
+      const bool etr = p.trace && blockIdx.x == 0 && lane == 0 && q4 == 0 && t == 0 && un < 256;
+      if (etr) p.trace[17 * 256 + un] = clock64();
       mbar_wait(&o_full[t], un & 1);
+      if (etr) p.trace[14 * 256 + un] = clock64();
       tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const bool ok = qi < x.len;
@@ -526,6 +533,7 @@ __global__ void __launch_bounds__(FA2_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[t]);
+      if (etr) p.trace[15 * 256 + un] = clock64();
       ++un;
     }
   }
