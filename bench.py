@@ -380,7 +380,13 @@ def study_T(cr, gpu, store, steps: int, dist, coll, sweep: bool = True) -> dict:
         return max(1.0, r0.p50(r0.prefill_layer_s) / r0.p50(r0.decode_layer_s))
 
     ratio = bcast(dist, [cadence(pm, dm)], coll)[0]
+    # each arm from the same power state (a pause before it: after seconds of
+    # co-runs the SM clock sits at the power cap for about a second)
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     co = cr.corun(pm, dm, steps, ratio)
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     tsl = cr.time_sliced(steps, ratio)
     torch.cuda.synchronize()
     out = {"T": T, "split": split, "decode_steps_per_prefill_layer": ratio,
@@ -534,12 +540,20 @@ def main(argv=None) -> int:
     pin_px.copy_(cr.px.cpu())
     pin_dx.copy_(cr.dx.cpu())
     cr.corun_e2e(pm, dm, args.warmup, ratio, pin_px, pin_py, pin_dx, pin_dy)  # warm-up (first-use costs)
-    e2e_res = cr.corun_e2e(pm, dm, args.steps, ratio, pin_px, pin_py, pin_dx, pin_dy)
+    # the same power state the timed region started from (right after seconds
+    # of co-runs the SM clock sits at the power cap for about a second)
+    torch.cuda.synchronize()
+    time.sleep(1.0)
+    with ClockSampler(local) as clk_e2e:
+        e2e_res = cr.corun_e2e(pm, dm, args.steps, ratio, pin_px, pin_py, pin_dx, pin_dy)
     e2e_span, e2e_tokens = job_totals(dist, e2e_res.span_s, e2e_res.tokens, coll)
     h2d = (T * h * 2 * args.steps + e2e_res.decode_steps * DECODE_BATCH * h * 2) // args.steps
     d2h = h2d
 
-    # ---- time-sliced baseline on the timed region's exact work
+    # ---- time-sliced baseline on the timed region's exact work, from the
+    # same power state as the timed region (a pause first)
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     ts_eq = cr.time_sliced(args.steps, ratio)
 
     # ---- SM idle: partition-level (SM-time with no work in either partition)
@@ -653,7 +667,7 @@ def main(argv=None) -> int:
                                                    "64-token tile) is what holds it below that"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_tokens / e2e_span, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "clocks": clk_e2e.summary()},
         "gpu_launches": int(round(args.steps * per_step_launches)),
         "cpu_baseline": cpu,
     }
