@@ -386,6 +386,48 @@ def test_prefill_attn_paged_matches_dense_without_prefix(gen):
     assert torch.equal(o_paged, o_dense)
 
 
+@pytest.mark.parametrize("seq_lens", [[700], [130, 257, 64, 1], [8448]])
+def test_prefill_attn_first_query_row_is_exact_v(seq_lens, gen):
+    # causal query 0 of every sequence sees only key 0: softmax weight exactly
+    # 1, so its output must equal V row 0 bit for bit on both operand paths
+    # (catches any leak of masked keys or a stale / partially landed V tile)
+    from paper_2504_19516_b200.device.layer import KVCache
+
+    Hq, Hkv, d, page = 32, 8, 128, 64
+    T = sum(seq_lens)
+    qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
+    q, kk, vv = qkv[:, :Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
+    starts = [0]
+    for n in seq_lens:
+        starts.append(starts[-1] + n)
+    cu = torch.tensor(starts, dtype=torch.int32, device=DEV)
+    nseq, maxlen = len(seq_lens), max(seq_lens)
+    o_dense = torch.empty(T, Hq * d, device=DEV, dtype=torch.bfloat16)
+    lib.prefill_attn(q, kk, vv, o_dense, cu, nseq, maxlen, Hq, Hkv, d, 1 / math.sqrt(d), max_ctas=148)
+    # paged: each sequence in its own pages, no prefix
+    ppages = [-(-n // page) for n in seq_lens]
+    cache = KVCache(sum(ppages), Hkv, d, DEV)
+    kl = torch.zeros(sum(ppages) * page, Hkv, d, device=DEV, dtype=torch.bfloat16)
+    vl = torch.zeros_like(kl)
+    bt = torch.zeros(nseq, max(ppages), dtype=torch.int32, device=DEV)
+    p0 = 0
+    for i, n in enumerate(seq_lens):
+        kl[p0 * page:p0 * page + n] = kk[starts[i]:starts[i + 1]].reshape(n, Hkv, d)
+        vl[p0 * page:p0 * page + n] = vv[starts[i]:starts[i + 1]].reshape(n, Hkv, d)
+        bt[i, :ppages[i]] = torch.arange(p0, p0 + ppages[i], dtype=torch.int32, device=DEV)
+        p0 += ppages[i]
+    npg = sum(ppages)
+    cache.k.copy_(lib.kv_pack(kl.view(npg, page, Hkv, d).permute(0, 2, 1, 3).contiguous()))
+    cache.v.copy_(lib.kv_pack(vl.view(npg, page, Hkv, d).permute(0, 2, 1, 3).contiguous()))
+    o_paged = torch.empty_like(o_dense)
+    lib.prefill_attn_paged(q, cache.k, cache.v, bt, cu, torch.zeros(nseq, dtype=torch.int32, device=DEV), nseq,
+                           maxlen, o_paged, Hq, Hkv, d, page, 1 / math.sqrt(d), max_ctas=148)
+    for s0 in starts[:-1]:
+        v0 = vv[s0].view(Hkv, d).repeat_interleave(Hq // Hkv, 0).reshape(-1)
+        assert torch.equal(o_dense[s0], v0)
+        assert torch.equal(o_paged[s0], v0)
+
+
 @pytest.mark.parametrize("T,Hq,Hkv,d", [(300, 32, 8, 128), (1024, 4, 2, 64), (77, 8, 2, 128)])
 def test_gemm_qkv_rope_fused_matches_fp32(T, Hq, Hkv, d, gen):
     # hp_gemm_qkv_rope: QKV GEMM + RoPE + paged K/V write in one epilogue
