@@ -223,8 +223,9 @@ int hp_prefill_attn(const void* q, int ldq, const void* k, int ldk, const void* 
 
 /* Kernel timeline traces.  kind 0: k_fa2 CTA 0 softmax/MMA wait stamps
  * (clock64, int64 [18][256]: rows 0-11 per KV step, 12-17 per unit); kind 1: k_gemm_swap_sk per-CTA globaltimer
- * stamps (uint64 [grid][6]: entry, prologue done, producer done, MMA done,
- * epilogue done, exit); kind 2 (one-shot, SM-idle measurement of config 2/3):
+ * stamps (uint64 [grid][10]: entry, prologue done, producer done, MMA done,
+ * epilogue done, exit; then, for the CTA's last split tile: partial written,
+ * arrival counted, partials summed (last arriver), tile emitted); kind 2 (one-shot, SM-idle measurement of config 2/3):
  * the NEXT hp_gemm / hp_gemm_qkv_rope / hp_prefill_attn(_paged) launch on
  * this thread writes per-CTA {smid, start_ns, end_ns} (uint64 [grid][3]) and
  * disarms it.  NULL disables. */

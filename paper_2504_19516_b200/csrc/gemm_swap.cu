@@ -75,7 +75,7 @@ struct SwapParams {
   int* counters;    // [tiles], zero on entry and exit
   const uint8_t* w;  // weights in the tiled layout (hp_tile_weight)
   int epi;
-  unsigned long long* trace;  // optional [grid][6] globaltimer stamps (hp_set_trace; development aid)
+  unsigned long long* trace;  // optional [grid][10] globaltimer stamps (hp_set_trace; development aid)
   // HP_EPI_PEER (row-parallel layers under tensor parallelism): the partial
   // tile goes to slot `rank` of every rank's receive buffer [world][T][N]
   // over peer memory, then flag [rank][tile] := epoch is raised on every rank.
@@ -309,11 +309,14 @@ const int q = warp & 3;
       if (lane == 0) release(acc);
       __threadfence();
       epi_sync();
+      unsigned long long* etr = (p.trace && et == 0) ? p.trace + blockIdx.x * 10 : nullptr;
+      if (etr) etr[6] = globaltimer();  // partial written
       if (et == 0) {
         const int prev = atomicAdd(p.counters + t128, 1);
         *last_flag = (prev == last - first) ? 1 : 0;
       }
       epi_sync();
+      if (etr) etr[7] = globaltimer();  // arrival counted
       if (*last_flag) {
         __threadfence();
         const int ncontrib = last - first + 1;
@@ -365,8 +368,10 @@ const int q = warp & 3;
             V[r * VLD + cc + 3] = a[i].w;
           }
           epi_sync();
+          if (etr) etr[8] = globaltimer();  // partials summed
           emit_chunk<BN>(p, V, mt, nt, c * 32, et, ep);
         }
+        if (etr) etr[9] = globaltimer();  // tile emitted
         if (et == 0) p.counters[t128] = 0;
         publish(t128);
       }
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   using C = SwapCfg<BN>;
   constexpr int STAGES = C::STAGES;
   pdl_trigger();
-  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 6] = globaltimer();
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 10] = globaltimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(SW_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  unsigned long long* tr = p.trace ? p.trace + blockIdx.x * 6 : nullptr;
+  unsigned long long* tr = p.trace ? p.trace + blockIdx.x * 10 : nullptr;
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
 
   const int begin = blockIdx.x * p.ipc;
