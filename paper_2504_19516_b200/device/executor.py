@@ -347,6 +347,12 @@ class B200Executor:
         else:
             ds, ps = self.pool.phase(DECODE, sms), None
         ctrl = torch.cuda.current_stream(self.dev)
+        if not getattr(self, "_bw_warm", False):
+            # first launch of the probe pays module loading / first-use costs
+            with torch.cuda.stream(ds.torch_stream):
+                lib.membw(buf, ds.sms, 1, self._bwout, stream=ds.torch_stream)
+            torch.cuda.synchronize(self.dev)
+            self._bw_warm = True
         start, a, b = _ev(), _ev(), _ev()
         torch.cuda._sleep(300_000)
         start.record(ctrl)
