@@ -263,6 +263,30 @@ def test_decode_attn(ctx, Hq, Hkv, d, max_ctas, page, gen):
         assert (got - ref).abs().max().item() < 2e-2, f"seq {b} ctx {c}"
 
 
+@pytest.mark.parametrize("max_ctas", [8, 148])
+def test_decode_attn_single_token_context_is_exact_v(max_ctas, gen):
+    # a sequence whose context is one cached token must return that token's V
+    # bit for bit (softmax weight exactly 1; any masked slot of the partial
+    # tile leaking in, or a stale ring slot, breaks equality), beside long
+    # neighbours that keep the ring and the split path busy
+    Hq, Hkv, d, page = 32, 8, 128, 64
+    ctx = [1, 2048, 1, 777, 1]
+    B = len(ctx)
+    kc, vc, bt = make_cache(B, ctx, Hkv, d, page, gen)
+    q = bf((B, Hq * d), gen=gen)
+    out = torch.zeros(B, Hq * d, device=DEV, dtype=torch.bfloat16)
+    ctx_t = torch.tensor(ctx, device=DEV, dtype=torch.int32)
+    ws = torch.empty(lib.decode_attn_ws_bytes(B, Hq, d, 256) // 4, device=DEV, dtype=torch.float32)
+    lib.decode_attn(q, lib.kv_pack(kc), lib.kv_pack(vc), bt, ctx_t, out, Hq, Hkv, d, page,
+                    1.0 / math.sqrt(d), ws=ws, max_ctas=max_ctas)
+    for b, c in enumerate(ctx):
+        if c != 1:
+            continue
+        v0 = vc[bt[b, 0].long(), :, 0, :]  # [Hkv, d]: token 0 of the sequence's first page
+        want = v0.repeat_interleave(Hq // Hkv, 0).reshape(-1)
+        assert torch.equal(out[b], want), b
+
+
 # ------------------------------------------------------------- partitions
 def test_wave_stats_native():
     assert lib.wave_stats(216, 2, 108) == (1, 108, 0.0)
