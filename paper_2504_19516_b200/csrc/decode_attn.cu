@@ -189,11 +189,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
     // ------------------------------------------------------------ producers
     const int pw = warp - DA_CONSUMERS;
     // KV is read once per step -- unless sibling head blocks re-read it from L2
-#ifdef HP_DA_NOHINT
-    const uint64_t pol = l2_policy_evict_last();
-#else
     const uint64_t pol = p.HB > 1 ? l2_policy_evict_last() : l2_policy_evict_first();
-#endif
     int win[DA_WREG], winn[DA_WREG];
     auto fetch = [&](int u, int (&w)[DA_WREG]) -> int {  // returns ctx of unit u
       const UnitId id = unit_of(p, u);
@@ -297,12 +293,7 @@ __global__ void __launch_bounds__(DA_THREADS, 1) k_decode_attn(const DecodeParam
   };
   auto acquire = [&](uint32_t h) -> uint32_t {
     const int st = int(h % RS);
-#ifndef HP_DA_SPIN_NS
-#define HP_DA_SPIN_NS 20
-#endif
-    while (ld_volatile_shared(tag + 4u * st) != h) {
-      if (HP_DA_SPIN_NS > 0) __nanosleep(HP_DA_SPIN_NS);
-    }
+    while (ld_volatile_shared(tag + 4u * st) != h) __nanosleep(20);
     mbar_wait(&full[st], (h / RS) & 1);
     return uint32_t(st);
   };
