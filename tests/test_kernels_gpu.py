@@ -138,6 +138,23 @@ def test_gemm_swap_resid_silu(ctas, gen):
     assert rel_err(y2, ref) < 2e-2
 
 
+@pytest.mark.parametrize("ctas", [8, 148])
+def test_gemm_swap_row_independent_within_a_batch_bucket(ctas, gen):
+    # serving determinism: a decode request's output rows must not depend on
+    # which other requests share its step -- within one token bucket (same
+    # BN, hence the same stream-K split and fp32 summation order) the first
+    # 13 rows of a 32-row call equal a 13-row call bit for bit
+    N, K = 4096, 4096
+    x, w = bf((32, K), gen=gen), bf((N, K), 0.05, gen)
+    wt = lib.tile_weight(w)
+    ws, cnt = _ws(N, 32, K, ctas)
+    y32 = torch.empty(32, N, device=DEV, dtype=torch.bfloat16)
+    y13 = torch.empty(13, N, device=DEV, dtype=torch.bfloat16)
+    lib.gemm_swap(x, wt, y32, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
+    lib.gemm_swap(x[:13].contiguous(), wt, y13, ws, cnt, lib.EPI_STORE, max_ctas=ctas)
+    assert torch.equal(y32[:13], y13)
+
+
 # ------------------------------------------------------------- RMSNorm / RoPE
 def test_rmsnorm(gen):
     x, wt = bf((77, 4096), gen=gen), bf((4096,), 1.0, gen)
@@ -285,6 +302,31 @@ def test_decode_attn_single_token_context_is_exact_v(max_ctas, gen):
         v0 = vc[bt[b, 0].long(), :, 0, :]  # [Hkv, d]: token 0 of the sequence's first page
         want = v0.repeat_interleave(Hq // Hkv, 0).reshape(-1)
         assert torch.equal(out[b], want), b
+
+
+def test_decode_attn_page_placement_invariant(gen):
+    # the same logical K/V placed on different physical pages (another block
+    # table) must give bit-identical outputs
+    Hq, Hkv, d, page = 32, 8, 128, 64
+    ctx = [2048, 700, 1, 64, 129]
+    B = len(ctx)
+    kc, vc, bt = make_cache(B, ctx, Hkv, d, page, gen)
+    q = bf((B, Hq * d), gen=gen)
+    ctx_t = torch.tensor(ctx, device=DEV, dtype=torch.int32)
+    ws = torch.empty(lib.decode_attn_ws_bytes(B, Hq, d, 256) // 4, device=DEV, dtype=torch.float32)
+    out1 = torch.zeros(B, Hq * d, device=DEV, dtype=torch.bfloat16)
+    lib.decode_attn(q, lib.kv_pack(kc), lib.kv_pack(vc), bt, ctx_t, out1, Hq, Hkv, d, page, 1 / math.sqrt(d),
+                    ws=ws, max_ctas=148)
+    # move every block to a new physical slot
+    nblk = kc.shape[0]
+    perm = torch.randperm(nblk, device=DEV)
+    kc2, vc2 = torch.empty_like(kc), torch.empty_like(vc)
+    kc2[perm], vc2[perm] = kc, vc
+    bt2 = perm.to(torch.int32)[bt.long()]
+    out2 = torch.zeros_like(out1)
+    lib.decode_attn(q, lib.kv_pack(kc2), lib.kv_pack(vc2), bt2, ctx_t, out2, Hq, Hkv, d, page, 1 / math.sqrt(d),
+                    ws=ws, max_ctas=148)
+    assert torch.equal(out1, out2)
 
 
 # ------------------------------------------------------------- partitions
