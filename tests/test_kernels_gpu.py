@@ -50,6 +50,37 @@ def test_gemm_store(T, N, K, gen):
     assert rel_err(y, ref) < 1e-2
 
 
+def test_prefill_gemm_and_attention_bitwise_invariant_to_partition_and_batch(gen):
+    # the co-run and the time-sliced baseline must compute the same numbers:
+    # prefill GEMM outputs (no split-K below 128 k-blocks) and prefill
+    # attention outputs do not depend on the SM partition, nor -- for the
+    # GEMM -- on which other rows share the call
+    T, N, K = 1024, 4096, 4096
+    x, w = bf((T, K), gen=gen), bf((N, K), 0.05, gen)
+    wt = lib.tile_weight(w)
+    outs = []
+    for sms in (148, 140, 52, 16):
+        y = torch.empty(T, N, device=DEV, dtype=torch.bfloat16)
+        lib.gemm(x, wt, y, lib.EPI_STORE, max_ctas=sms)
+        outs.append(y)
+    for y in outs[1:]:
+        assert torch.equal(outs[0], y)
+    y256 = torch.empty(256, N, device=DEV, dtype=torch.bfloat16)
+    lib.gemm(x[256:512].contiguous(), wt, y256, lib.EPI_STORE, max_ctas=148)
+    assert torch.equal(outs[0][256:512], y256)
+    Hq, Hkv, d = 32, 8, 128
+    qkv = bf((T, (Hq + 2 * Hkv) * d), gen=gen)
+    q, kk, vv = qkv[:, :Hq * d], qkv[:, Hq * d:(Hq + Hkv) * d], qkv[:, (Hq + Hkv) * d:]
+    cu = torch.tensor([0, T], dtype=torch.int32, device=DEV)
+    att = []
+    for sms in (148, 124, 8):
+        o = torch.empty(T, Hq * d, device=DEV, dtype=torch.bfloat16)
+        lib.prefill_attn(q, kk, vv, o, cu, 1, T, Hq, Hkv, d, 1 / math.sqrt(d), max_ctas=sms)
+        att.append(o)
+    for o in att[1:]:
+        assert torch.equal(att[0], o)
+
+
 @pytest.mark.parametrize("max_ctas", [1, 16, 148])
 def test_gemm_grid_sizes(max_ctas, gen):
     T, N, K = 300, 512, 640
